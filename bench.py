@@ -1,0 +1,284 @@
+"""Benchmark: target evaluations/s of the periodic KIFMM evaluate path on B200.
+
+Workload (BASELINE.json configs[1], the config the headline metric is quoted on):
+Stokes velocity (Stokeslet), triply periodic unit cube, N = 100,000 uniform points
+(sources = targets), forces N(0,1) mean-subtracted, float64, p = 8, leaf 50, ell = 2,
+precomputed periodizing operator (tests/golden/ops). Synthetic inputs from the seeded
+SURVEY §8(d) protocol (std::mt19937_64, seed 12345 + rank).
+
+One "step" = one complete evaluate (tree, lists, upward, M2L/downward, periodizing step,
+leaf pass). `value`: inputs resident in HBM; `e2e`: the same call through the public API
+with pinned HOST buffers, H2D of the inputs and D2H of the velocities inside each step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "target evals/s (periodic Stokes TP, p=8)"
+UNIT = "targets/s"
+N_POINTS = 100_000
+P_ORDER = 8
+LEAF = 50
+OP_PATH = os.path.join(REPO, "tests", "golden", "ops", "stokeslet_tp_ell2_p8_gated.pkm2l")
+WORKLOAD = "cfg2: Stokes TP (unit cube), N=100000 uniform, p=8, leaf 50, ell=2 (BASELINE.json configs[1])"
+FP64_PEAK_TFLOPS = 37.07  # measured DMMA m8n8k4 loop on this pool (profiles/r01_fp64_peaks.jsonl)
+FP64_PEAK_SOURCE = "measured: DMMA.8x8x4 loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl); " \
+                   "MEASURED_PEAKS.json has no FP64 entry"
+REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index),
+                         "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                    sm, smax, reasons = [x.strip() for x in out.strip().split(",")]
+                    self.samples.append((float(sm), float(smax), int(reasons, 16)))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        bits = 0
+        for s in self.samples:
+            bits |= s[2]
+        names = [n for b, n in REASONS.items() if bits & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples), "reasons": names,
+                "samples": len(sm)}
+
+
+def cpu_reference(steps, warmup, threads=None, budget_s=150.0):
+    """The reference's own CPU evaluate (oracle/_ref, compiled from /root/reference) on
+    this host's cores: full cfg2 evaluate per step, warm (operators prebuilt)."""
+    if not os.path.exists(REFDUMP):
+        return None
+    threads = threads or os.cpu_count()
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads), OPENBLAS_NUM_THREADS=str(threads))
+    with tempfile.TemporaryDirectory() as tmp:
+        base = os.path.join(tmp, "c2")
+        subprocess.run([REFDUMP, "gen", "--n", str(N_POINTS), "--kind", "uniform", "--ks", "3", "--seed", "12345",
+                        "--out", base], check=True, capture_output=True, env=env)
+        args = [REFDUMP, "eval", "--kernel", "stokeslet", "--per", "tp", "--ell", "2", "--p", str(P_ORDER),
+                "--leaf", str(LEAF), "--src", base + ".src.f64", "--str", base + ".str.f64", "--op", OP_PATH,
+                "--threads", str(threads)]
+        # warm-up run (also measures one step to size the sample)
+        t0 = time.time()
+        r = subprocess.run(args + ["--repeat", str(max(1, warmup))], check=True, capture_output=True, text=True,
+                           env=env)
+        t_step = (time.time() - t0) / max(1, warmup)
+        n = max(1, min(steps, int(budget_s / max(t_step, 1e-3))))
+        r = subprocess.run(args + ["--repeat", str(n)], check=True, capture_output=True, text=True, env=env)
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+    walls = [x["wall"] for x in res["runs"]]
+    return {"value": N_POINTS / float(np.mean(walls)), "unit": UNIT, "cores": threads, "kind": "reference",
+            "steps_timed": n, "seconds_per_step": float(np.mean(walls)),
+            "phases_s": {k: float(np.mean([x[k] for x in res["runs"]])) for k in ("tree", "near", "m2l_apply", "far")},
+            "sample": f"full cfg2 evaluate (N={N_POINTS}, warm, operators prebuilt), {n} step(s) after "
+                      f"{max(1, warmup)} warm-up; OMP/OpenBLAS threads = {threads}"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_reference(args.steps, args.warmup)
+    if cb is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/refdump not built"}))
+        return
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": cb["steps_timed"],
+            "warmup": max(1, args.warmup), "ms_per_step": 1e3 * cb["seconds_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD}, "impl": "reference",
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "phases_s": cb["phases_s"]}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1705_02043_b200 as pk
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = pk.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    pts, f = pk.generate("uniform", N_POINTS, 3, seed=12345 + rank)
+    op = pk.load_operator(OP_PATH)
+    setup = pk.PeriodicSetup.make(pk.Periodicity.tp)
+    kern = pk.KernelSpec.stokeslet()
+    d_pts = torch.from_numpy(pts).to(dev).reshape(-1).contiguous()
+    d_f = torch.from_numpy(f).to(dev).contiguous()
+    d_out = torch.empty(3 * N_POINTS, dtype=torch.float64, device=dev)
+    req = pk.EvalRequest(kernel=kern, sources=d_pts, strengths=d_f, targets=d_pts, setup=setup, p=P_ORDER, op=op,
+                         leaf_capacity=LEAF)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up (operators built, workspaces sized)
+    for _ in range(max(3, args.warmup)):
+        pk.evaluate(req, context=ctx, out=d_out)
+    # ---- device-resident timed region (profiling on: live per-stage CUDA events) ----
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    l0 = ctx.launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        pk.evaluate(req, context=ctx, out=d_out)
+        ev[i][1].record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = (ctx.launches - l0) / args.steps
+    stats = ctx.stage_stats()
+    ctx.set_profiling(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---- e2e: public API with pinned host buffers (H2D + D2H inside each step) ----
+    h_pts = torch.from_numpy(pts.reshape(-1).copy()).pin_memory()
+    h_f = torch.from_numpy(f.copy()).pin_memory()
+    h_out = torch.empty(3 * N_POINTS, dtype=torch.float64).pin_memory()
+    hreq = pk.EvalRequest(kernel=kern, sources=h_pts.numpy().reshape(-1, 3), strengths=h_f.numpy(),
+                          targets=h_pts.numpy().reshape(-1, 3), setup=setup, p=P_ORDER, op=op, leaf_capacity=LEAF)
+    out_np = h_out.numpy()
+    for _ in range(2):
+        pk.evaluate(hreq, context=ctx, out=out_np)
+    barrier()
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        pk.evaluate(hreq, context=ctx, out=out_np)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = float(np.mean(e2e_ms))
+    e_t = torch.tensor([e2e], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_max = float(e_t.item())
+    # e2e result must equal the device-resident one
+    same = bool(np.array_equal(out_np, d_out.cpu().numpy()))
+
+    if rank == 0:
+        m2l = stats.get("m2l", {})
+        m2l_launches = max(1, m2l.get("launches", 1))
+        per_launch_s = m2l.get("seconds", 0.0) / m2l_launches
+        per_launch_flops = m2l.get("flops", 0.0) / m2l_launches
+        achieved = per_launch_flops / per_launch_s / 1e12 if per_launch_s > 0 else None
+        stage_tab = {k: {"ms_per_step": 1e3 * v["seconds"] / args.steps,
+                         "tflops": (v["flops"] / v["seconds"] / 1e12) if v["seconds"] > 0 and v["flops"] else None,
+                         "launches_per_step": v["launches"] / args.steps}
+                     for k, v in stats.items() if k != "u_pairs"}
+        line = {
+            "metric": METRIC, "value": N_POINTS * ws / (ms_max * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (mt19937_64 seed 12345+rank, SURVEY §8d protocol)",
+            "config": {"workload": WORKLOAD, "N": N_POINTS, "p": P_ORDER, "leaf": LEAF, "kernel": "stokeslet",
+                       "periodicity": "tp", "ell": 2,
+                       "l2": "flushed between timed steps (256 MiB write, outside the step events)",
+                       "parallelism": f"{ws} independent replica(s), one per GPU"},
+            "e2e": {"value": N_POINTS * ws / (e2e_max * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int((3 + 3 + 3) * N_POINTS * 8),
+                    "d2h_bytes_per_step": int(3 * N_POINTS * 8), "matches_device_result": same},
+            "gpu_launches": int(round(launches)),
+            "roofline": {"kernel": "gather_gemm_kernel<128> (M2L, DMMA.8x8x4)", "bound": "tensor",
+                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                         "flops_per_launch": per_launch_flops, "ms_per_launch": 1e3 * per_launch_s,
+                         "peak_source": FP64_PEAK_SOURCE,
+                         "flop_convention": "2 K^2 per V-list application, K = 888 (SURVEY §8d)"},
+            "stages": stage_tab,
+            "clocks": clk,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            cb = cpu_reference(steps=2, warmup=1, budget_s=30.0)
+            if cb is not None:
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

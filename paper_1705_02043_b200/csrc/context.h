@@ -1,0 +1,69 @@
+// Context and operator objects behind the C ABI handles.
+#pragma once
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pkgpu.h"
+#include "operators.h"
+#include "tree.h"
+
+struct pkgpu_operator {
+    int kernel = 0;
+    pkgpu_setup setup{};
+    int p = 0;
+    int64_t dim = 0;
+    std::vector<double> matrix; // dim x dim row-major (the PKM2L payload)
+    int method = 0;
+    double residual_max = 0.0;
+    uint64_t crc = 0;
+    // device copy, uploaded lazily per device
+    mutable std::mutex mtx;
+    mutable double *d_matrix = nullptr;
+    mutable int d_device = -1;
+    ~pkgpu_operator();
+    const double *device_matrix(int device, cudaStream_t st) const;
+};
+
+struct pkgpu_context {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    std::mutex mtx; // calls on one context are serialised (the reference evaluate is reentrant per call)
+    pkgpu::OperatorCache ops;
+    pkgpu::DeviceTree tree;
+    pkgpu::DeviceLists lists;
+    pkgpu::Workspace ws;
+    cudaEvent_t ev[6]{};
+    // per-stage profiling (pkgpu_context_stage_stats)
+    struct StageStat {
+        double seconds = 0, units = 0, flops = 0;
+        int64_t launches = 0;
+    };
+    bool profiling = false;
+    std::map<std::string, StageStat> stats;
+    std::vector<cudaEvent_t> evpool;
+};
+
+struct pkgpu_tree {
+    pkgpu_context *ctx = nullptr;
+    pkgpu::DeviceTree tree;
+    std::vector<int32_t> table, srcidx, trgidx;
+    uint64_t hash = 0;
+    bool exported = false;
+};
+
+namespace pkgpu {
+
+void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_timings *timings,
+              pkgpu_compat *compat);
+
+void kernel_block_apply_device(pkgpu_context &ctx, int kernel, const double *targets, int64_t nt,
+                               const double *sources, int64_t ns, const double *shift, const double *density,
+                               double *out, int skip);
+
+} // namespace pkgpu

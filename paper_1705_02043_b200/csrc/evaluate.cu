@@ -1,0 +1,591 @@
+// The evaluate pipeline (pkifmm::evaluate, src/fmm.cpp:690-742) on one B200.
+//
+//   validate + compatibility gate (src/fmm.cpp:693-706, src/refsum.cpp:733-756)
+//   tree (Morton keys, radix sort, level-synchronous split)           -> timings.tree
+//   column layout + lists (U/W/X CSR, V straight into the M2L table)
+//   upward:   S2M (pairs) ; per level M2M (gather-GEMM) + pinv (2 GEMMs)
+//   downward: X (pairs) ; per level M2L + L2L (gather-GEMMs) + pinv
+//   periodizing step: phi_far = T_M2L phi_up[0] (+ pinv(a_dn, M_img phi_up[0]))  -> m2l_apply
+//   leaf pass: L2T + W + U + far field, fused, one write per target
+// All device work is on the context stream; timings are CUDA events.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cub/cub.cuh>
+
+#include "context.h"
+#include "gemm.h"
+#include "pairs.h"
+
+namespace pkgpu {
+
+namespace {
+
+constexpr int BN = kGemmBN;
+
+__global__ void compat_partial_kernel(const double *__restrict__ s, int64_t n, int ks, double *__restrict__ part) {
+    // part[block][0] = sum |s|, part[block][1+a] = sum s_a ; fixed partition -> deterministic
+    __shared__ double red[4][256];
+    double a[4] = {0, 0, 0, 0};
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b = per * blockIdx.x, e = min(n, b + per);
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
+        for (int c = 0; c < ks; c++) {
+            const double v = s[i * ks + c];
+            a[0] += fabs(v);
+            a[1 + c] += v;
+        }
+    for (int c = 0; c < 4; c++) red[c][threadIdx.x] = a[c];
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o)
+            for (int c = 0; c < 4; c++) red[c][threadIdx.x] += red[c][threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int c = 0; c < 4; c++) part[4 * blockIdx.x + c] = red[c][0];
+}
+
+__global__ void layout_keys_kernel(TreeView T, int *keys, int *vals) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int4 c = T.cell[b];
+    keys[b] = c.w * 8 + ((c.x & 1) | ((c.y & 1) << 1) | ((c.z & 1) << 2));
+    vals[b] = b;
+}
+
+__global__ void layout_fill_kernel(TreeView T, const int *__restrict__ skeys, const int *__restrict__ sboxes,
+                                   const int *__restrict__ group_start, const int *__restrict__ group_col,
+                                   int *col_of_box, int *out_box, int *out_m2m, int *l2l_src, int *m2m_src,
+                                   int64_t ncols, int *tile_oct) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= T.nboxes) return;
+    const int key = skeys[i], b = sboxes[i];
+    const int col = group_col[key] + (i - group_start[key]);
+    col_of_box[b] = col;
+    out_box[col] = b;
+    const bool leaf = T.isleaf[b] != 0;
+    out_m2m[col] = leaf ? -1 : b;
+    l2l_src[col] = T.parent[b];
+    tile_oct[col / BN] = key & 7;
+    for (int o = 0; o < 8; o++) {
+        const int c = leaf ? -1 : T.child[8 * b + o];
+        m2m_src[(int64_t)o * ncols + col] = (c >= 0 && T.srng[c].y > T.srng[c].x) ? c : -1;
+    }
+}
+
+__global__ void add_kernel(double *y, const double *x, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] += x[i];
+}
+
+// stage profiler: CUDA events on the work stream around each stage (profiling on)
+struct Prof {
+    pkgpu_context &ctx;
+    cudaStream_t st;
+    struct Mark {
+        std::string stage;
+        cudaEvent_t a, b;
+        int64_t l0, l1;
+    };
+    std::vector<Mark> marks;
+    size_t next = 0;
+    Prof(pkgpu_context &c, cudaStream_t s) : ctx(c), st(s) {}
+    cudaEvent_t ev() {
+        if (next == ctx.evpool.size()) {
+            cudaEvent_t e;
+            PK_CUDA(cudaEventCreate(&e));
+            ctx.evpool.push_back(e);
+        }
+        return ctx.evpool[next++];
+    }
+    int begin(const char *stage) {
+        if (!ctx.profiling) return -1;
+        Mark m{stage, ev(), ev(), ctx.launches, 0};
+        PK_CUDA(cudaEventRecord(m.a, st));
+        marks.push_back(m);
+        return (int)marks.size() - 1;
+    }
+    void end(int i) {
+        if (i < 0) return;
+        PK_CUDA(cudaEventRecord(marks[i].b, st));
+        marks[i].l1 = ctx.launches;
+    }
+    void finish() {
+        if (marks.empty()) return;
+        PK_CUDA(cudaStreamSynchronize(st));
+        for (auto &m : marks) {
+            float ms = 0;
+            PK_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+            auto &s = ctx.stats[m.stage];
+            s.seconds += ms * 1e-3;
+            s.launches += m.l1 - m.l0;
+        }
+    }
+    void work(const char *stage, double units, double flops_per_unit) {
+        if (!ctx.profiling) return;
+        auto &s = ctx.stats[stage];
+        s.units += units;
+        s.flops += units * flops_per_unit;
+    }
+};
+
+// algorithmic work of one evaluate (pairs / applications), reference conventions
+__global__ void work_count_kernel(TreeView T, int n, const int64_t *__restrict__ u_off, const int2 *__restrict__ u_ent,
+                                  const int64_t *__restrict__ w_off, const int64_t *__restrict__ x_off,
+                                  const int2 *__restrict__ x_ent, unsigned long long *cnt) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int2 sr = T.srng[b], tr = T.trng[b];
+    const long long ns = sr.y - sr.x, nt = tr.y - tr.x;
+    unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (T.isleaf[b]) {
+        if (nt > 0) {
+            long long su = 0;
+            for (int64_t e = u_off[b]; e < u_off[b + 1]; e++) {
+                const int2 r = T.srng[u_ent[e].x];
+                su += r.y - r.x;
+            }
+            c[0] = nt * su;                              // U pairs
+            c[1] = nt * (w_off[b + 1] - w_off[b]) * n;   // W pairs
+            c[2] = nt * n;                               // L2T pairs
+        }
+        if (ns > 0) c[3] = ns * n;                       // S2M pairs
+    } else if (ns > 0) {
+        for (int o = 0; o < 8; o++) {
+            const int ch = T.child[8 * b + o];
+            if (ch >= 0 && T.srng[ch].y > T.srng[ch].x) c[5]++; // M2M applications
+        }
+    }
+    if (nt > 0) {
+        long long sx = 0;
+        for (int64_t e = x_off[b]; e < x_off[b + 1]; e++) {
+            const int2 r = T.srng[x_ent[e].x];
+            sx += r.y - r.x;
+        }
+        c[4] = sx * n;                                   // X pairs
+        if (T.parent[b] >= 0) c[6] = 1;                  // pinv_dn / L2L boxes
+    }
+    if (ns > 0) c[7] = 1;                                // pinv_up boxes
+    for (int k = 0; k < 8; k++)
+        if (c[k]) atomicAdd(cnt + k, c[k]);
+}
+
+struct Layout {
+    std::vector<int64_t> colbase; // per level, size depth + 2
+    int64_t ncols = 0;
+    int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *l2l_src = nullptr, *m2m_src = nullptr,
+        *tile_oct = nullptr, *m2l_table = nullptr;
+};
+
+// Columns of the gather-GEMMs: per level, boxes grouped by octant (cell parity) in
+// Morton order, each group padded to a multiple of 64 -> every column tile is
+// octant-homogeneous (one L2L matrix per tile; M2L tiles share their offset set).
+Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
+    Workspace &ws = ctx.ws;
+    const int nb = (int)T.nboxes;
+    const TreeView tv = T.view();
+    int *keys = ws.get<int>("lay_keys", nb), *vals = ws.get<int>("lay_vals", nb);
+    int *skeys = ws.get<int>("lay_skeys", nb), *svals = ws.get<int>("lay_svals", nb);
+    layout_keys_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, keys, vals);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, svals, nb, 0, 7, st);
+    void *tmp = ws.get<char>("lay_temp", tb);
+    PK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, vals, svals, nb, 0, 7, st));
+    std::vector<int> hk(nb);
+    PK_CUDA(cudaMemcpyAsync(hk.data(), skeys, nb * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    ctx.launches += 5;
+    constexpr int NK = kMaxLevels * 8;
+    std::vector<int> count(NK, 0), start(NK, 0), gcol(NK, 0);
+    for (int k : hk) count[k]++;
+    Layout L;
+    L.colbase.assign(T.depth + 2, 0);
+    int s = 0;
+    int64_t c = 0;
+    for (int k = 0; k < NK; k++) {
+        const int lvl = k / 8;
+        if (k % 8 == 0 && lvl <= T.depth) L.colbase[lvl] = c;
+        start[k] = s;
+        gcol[k] = (int)c;
+        s += count[k];
+        c += (count[k] + BN - 1) / BN * BN;
+    }
+    L.colbase[T.depth + 1] = c;
+    L.ncols = c;
+    int *d_start = ws.get<int>("lay_start", NK), *d_gcol = ws.get<int>("lay_gcol", NK);
+    PK_CUDA(cudaMemcpyAsync(d_start, start.data(), NK * sizeof(int), cudaMemcpyHostToDevice, st));
+    PK_CUDA(cudaMemcpyAsync(d_gcol, gcol.data(), NK * sizeof(int), cudaMemcpyHostToDevice, st));
+    const int64_t C = std::max<int64_t>(c, 1);
+    L.col_of_box = ws.get<int>("col_of_box", nb);
+    L.out_box = ws.get<int>("out_box", C);
+    L.out_m2m = ws.get<int>("out_m2m", C);
+    L.l2l_src = ws.get<int>("l2l_src", C);
+    L.m2m_src = ws.get<int>("m2m_src", 8 * C);
+    L.tile_oct = ws.get<int>("tile_oct", C / BN + 1);
+    L.m2l_table = ws.get<int>("m2l_table", (size_t)kNumM2L * C);
+    PK_CUDA(cudaMemsetAsync(L.out_box, 0xff, C * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, C * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.l2l_src, 0xff, C * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * C * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.m2l_table, 0xff, (size_t)kNumM2L * C * sizeof(int), st));
+    layout_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, skeys, svals, d_start, d_gcol, L.col_of_box,
+                                                            L.out_box, L.out_m2m, L.l2l_src, L.m2m_src, C, L.tile_oct);
+    PK_CUDA(cudaGetLastError());
+    ctx.launches += 6;
+    return L;
+}
+
+void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t hi, int level, double *Q, double *Tmp,
+                double *Phi, cudaStream_t st) {
+    if (hi <= lo) return;
+    GemmArgs a;
+    a.Kp = ops.Kp;
+    a.nvalid = (int)(hi - lo);
+    a.box0 = (int)lo;
+    a.ncols = round_up(a.nvalid, BN);
+    a.A = up ? ops.Ut_up : ops.Ut_dn;
+    a.X = Q;
+    a.Y = Tmp;
+    a.rdiv = up ? ops.s_up : ops.s_dn;
+    a.rdiv_eps = up ? ops.up.eps : ops.dn.eps;
+    ctx.launches += gather_gemm(a, ctx.ws, st, ctx.num_sms);
+    GemmArgs b = a;
+    b.A = up ? ops.V_up : ops.V_dn;
+    b.X = Tmp;
+    b.Y = Phi;
+    b.rdiv = nullptr;
+    b.alpha = std::ldexp(1.0, -level); // phi /= 2^l (src/fmm.cpp:550-551, 595-596)
+    b.beta = 0.0;
+    ctx.launches += gather_gemm(b, ctx.ws, st, ctx.num_sms);
+}
+
+// single-vector pinv: x = V (S+ (U^T b)) (src/linalg.cpp:78-87)
+void pinv_vec(pkgpu_context &ctx, KifmmOps &ops, bool up, const double *b, double *tmp, double *x, cudaStream_t st) {
+    gemv(up ? ops.Ut_up : ops.Ut_dn, ops.K, ops.K, ops.Kp, b, tmp, 1.0, 0.0, up ? ops.s_up : ops.s_dn,
+         up ? ops.up.eps : ops.dn.eps, st);
+    gemv(up ? ops.V_up : ops.V_dn, ops.K, ops.K, ops.Kp, tmp, x, 1.0, 0.0, nullptr, 0.0, st);
+    ctx.launches += 2;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    PK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3f;
+}
+
+bool same_setup(const pkgpu_setup &a, const pkgpu_setup &b) {
+    return a.periodicity == b.periodicity && (a.axes[0] != 0) == (b.axes[0] != 0) &&
+           (a.axes[1] != 0) == (b.axes[1] != 0) && (a.axes[2] != 0) == (b.axes[2] != 0) &&
+           a.box_length == b.box_length && a.ell == b.ell;
+}
+
+} // namespace
+
+void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_timings *timings,
+              pkgpu_compat *compat) {
+    cudaStream_t st = ctx.stream;
+    const int kernel = req.kernel;
+    if (kernel != PKGPU_LAPLACE && kernel != PKGPU_STOKESLET) throw InvalidArgument("unknown kernel");
+    const int ks = kernel == PKGPU_LAPLACE ? 1 : 3, kt = ks;
+    // src/fmm.cpp:693-701
+    if (req.n_strengths != req.n_sources * ks)
+        throw InvalidArgument("evaluate: strengths length does not match sources");
+    const bool periodic = req.setup.periodicity != PKGPU_NONE;
+    if (periodic) {
+        if (!req.op) throw ConfigError("evaluate: a periodizing operator is required for periodic runs");
+        const pkgpu_operator &op = *req.op;
+        if (op.kernel != kernel || op.p != req.p || !same_setup(op.setup, req.setup))
+            throw ConfigError("evaluate: operator provenance (kernel/p/ell/periodicity) does not match the request");
+    }
+    if (req.p < 2) throw InvalidArgument("surface grid requires p >= 2");
+    const int64_t ns = req.n_sources, nt = req.n_targets;
+    Workspace &ws = ctx.ws;
+    // inputs on the device
+    const double *d_src = req.sources, *d_str = req.strengths, *d_trg = req.targets;
+    double *d_out = out;
+    if (!req.device_pointers) {
+        double *s = ws.get<double>("in_src", 3 * ns + 1), *q = ws.get<double>("in_str", ks * ns + 1),
+               *t = ws.get<double>("in_trg", 3 * nt + 1);
+        if (ns) PK_CUDA(cudaMemcpyAsync(s, req.sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (ns) PK_CUDA(cudaMemcpyAsync(q, req.strengths, ks * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (nt) PK_CUDA(cudaMemcpyAsync(t, req.targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
+        d_src = s, d_str = q, d_trg = t;
+        d_out = ws.get<double>("out", kt * nt + 1);
+    }
+    // compatibility gate (src/refsum.cpp:733-756)
+    pkgpu_compat rep{1, 0.0, {0}};
+    if (periodic && !(kernel == PKGPU_STOKESLET && req.setup.periodicity == PKGPU_TP) && ns > 0) {
+        const int nblk = 256;
+        double *part = ws.get<double>("compat_part", 4 * nblk);
+        compat_partial_kernel<<<nblk, 256, 0, st>>>(d_str, ns, ks, part);
+        std::vector<double> h(4 * nblk);
+        PK_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        ctx.launches += 1;
+        double abs_total = 0, sums[3] = {0, 0, 0};
+        for (int b = 0; b < nblk; b++) {
+            abs_total += h[4 * b];
+            for (int c = 0; c < ks; c++) sums[c] += h[4 * b + 1 + c];
+        }
+        double worst = 0;
+        for (int c = 0; c < ks; c++) worst = std::max(worst, std::fabs(sums[c]));
+        if (worst > 1e-12 * abs_total) {
+            rep.ok = 0;
+            rep.residual = worst;
+            std::snprintf(rep.violated, sizeof rep.violated, "%s",
+                          kernel == PKGPU_LAPLACE ? "neutrality: net charge must vanish"
+                                                  : "neutrality: net force must vanish");
+        }
+    }
+    if (compat) *compat = rep;
+    if (!rep.ok && !req.force)
+        throw ConfigError(std::string("evaluate: compatibility violation (") + rep.violated + ")");
+    pkgpu_timings tm{0, 0, 0, 0};
+    const int axes[3] = {req.setup.axes[0] != 0, req.setup.axes[1] != 0, req.setup.axes[2] != 0};
+    const int ell = req.setup.ell;
+
+    if (req.mode == PKGPU_MODE_DIRECT) {
+        // src/fmm.cpp:711-721: all image offsets with max-norm <= ell, skip coincident at 0
+        PK_CUDA(cudaEventRecord(ctx.ev[0], st));
+        std::vector<std::array<int, 3>> offs =
+            periodic ? image_offsets(axes, 0, ell) : std::vector<std::array<int, 3>>{{0, 0, 0}};
+        std::vector<double> hoffs;
+        for (auto &d : offs) hoffs.insert(hoffs.end(), {(double)d[0], (double)d[1], (double)d[2]});
+        double *d_offs = ws.get<double>("direct_offs", hoffs.size());
+        int *d_coin = ws.get<int>("direct_coin", offs.size());
+        PK_CUDA(cudaMemcpyAsync(d_offs, hoffs.data(), hoffs.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaMemsetAsync(d_coin, 0, offs.size() * sizeof(int), st));
+        KifmmOps &ops = ctx.ops.get(kernel, req.p, st, &ctx.launches);
+        PairGeom g{kernel, req.p, ops.n, ops.Kp, ops.d_tmpl};
+        // one launch per offset keeps per-offset coincidence counts (error text)
+        for (size_t o = 0; o < offs.size(); o++) {
+            direct_pairs(kernel, d_trg, nt, d_src, d_str, ns, d_offs + 3 * o, 1, 1, nullptr, nullptr, d_out,
+                         o > 0 ? 1 : 0, d_coin + o, ws, st);
+            ctx.launches += 1;
+        }
+        std::vector<int> coin(offs.size());
+        PK_CUDA(cudaMemcpyAsync(coin.data(), d_coin, coin.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+        // direct_root_upward_density (src/fmm.cpp:676-686)
+        double *q = ws.get<double>("root_q", ops.Kp), *tmp = ws.get<double>("root_t", ops.Kp),
+               *up = ws.get<double>("root_up", ops.Kp);
+        PK_CUDA(cudaMemsetAsync(q, 0, ops.Kp * sizeof(double), st));
+        if (ns) root_check_potential(g, d_src, d_str, ns, q, ws, st);
+        pinv_vec(ctx, ops, true, q, tmp, up, st);
+        PK_CUDA(cudaEventRecord(ctx.ev[1], st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        for (size_t o = 0; o < offs.size(); o++)
+            if (coin[o] > 0)
+                throw InvalidArgument("kernel_block_apply: " + std::to_string(coin[o]) +
+                                      " coincident target/source pairs");
+        tm.near = elapsed(ctx.ev[0], ctx.ev[1]);
+        if (periodic) {
+            double *far = ws.get<double>("far_dn", ops.Kp);
+            PK_CUDA(cudaEventRecord(ctx.ev[2], st));
+            gemv(req.op->device_matrix(ctx.device, st), ops.K, ops.K, ops.K, up, far, 1.0, 0.0, nullptr, 0.0, st);
+            PK_CUDA(cudaEventRecord(ctx.ev[3], st));
+            direct_pairs(kernel, d_trg, nt, d_src, d_str, 0, nullptr, 0, 1, &g, far, d_out, 1, d_coin, ws, st);
+            PK_CUDA(cudaEventRecord(ctx.ev[4], st));
+            ctx.launches += 2;
+            PK_CUDA(cudaStreamSynchronize(st));
+            tm.m2l_apply = elapsed(ctx.ev[2], ctx.ev[3]);
+            tm.far = elapsed(ctx.ev[3], ctx.ev[4]);
+        }
+    } else {
+        // ---------------- FMM mode ----------------
+        Prof prof(ctx, st);
+        PK_CUDA(cudaEventRecord(ctx.ev[0], st));
+        int pm = prof.begin("tree");
+        DeviceTree &T = ctx.tree;
+        build_tree(T, d_src, ns, d_trg, nt, req.leaf_capacity, st, &ctx.launches);
+        gather_strengths(T, d_str, ks, st, &ctx.launches);
+        prof.end(pm);
+        PK_CUDA(cudaEventRecord(ctx.ev[1], st));
+        KifmmOps &ops = ctx.ops.get(kernel, req.p, st, &ctx.launches);
+        const int Kp = ops.Kp;
+        const int64_t nb = T.nboxes;
+        PairGeom g{kernel, req.p, ops.n, Kp, ops.d_tmpl};
+        pm = prof.begin("lists");
+        Layout Lay = build_layout(ctx, T, st);
+        ListSetup ls{};
+        if (periodic && ell >= 1)
+            for (int a = 0; a < 3; a++) ls.periodic[a] = axes[a];
+        build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
+                         &ctx.launches);
+        prof.end(pm);
+        double *Q = ws.get<double>("Q", nb * Kp), *Tm = ws.get<double>("Tmp", nb * Kp),
+               *Pup = ws.get<double>("phi_up", nb * Kp), *Pdn = ws.get<double>("phi_dn", nb * Kp);
+        // ---- upward pass (src/fmm.cpp:532-553) ----
+        PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));
+        pm = prof.begin("s2m");
+        s2m_pass(g, T, Q, st);
+        ctx.launches += 1;
+        prof.end(pm);
+        for (int l = T.depth; l >= 0; l--) {
+            const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
+            const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
+            if (l < T.depth) {
+                GemmArgs a;
+                a.Kp = Kp;
+                a.ncols = (int)(c1 - c0);
+                a.out_box = Lay.out_m2m + c0;
+                a.nslots = 8;
+                a.src = Lay.m2m_src + c0;
+                a.ld_src = Lay.ncols;
+                a.A = ops.m2m;
+                a.X = Pup;
+                a.Y = Q;
+                a.alpha = std::ldexp(1.0, l); // q += 2^l M2M_o phi_child (src/fmm.cpp:547)
+                a.beta = 0.0;
+                pm = prof.begin("m2m");
+                ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
+                prof.end(pm);
+            }
+            pm = prof.begin("pinv_up");
+            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st);
+            prof.end(pm);
+        }
+        // ---- downward pass (src/fmm.cpp:557-601) ----
+        PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));
+        pm = prof.begin("x");
+        x_pass(g, T, ctx.lists, Q, st);
+        ctx.launches += ctx.lists.x.count ? 1 : 0;
+        prof.end(pm);
+        for (int l = 0; l <= T.depth; l++) {
+            const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
+            const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
+            if (l >= 1) {
+                GemmArgs a;
+                a.Kp = Kp;
+                a.ncols = (int)(c1 - c0);
+                a.out_box = Lay.out_box + c0;
+                a.nslots = kNumM2L;
+                a.src = Lay.m2l_table + c0;
+                a.ld_src = Lay.ncols;
+                a.A = ops.m2l;
+                a.X = Pup;
+                a.Y = Q;
+                a.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573, 168-171)
+                a.beta = 1.0;
+                pm = prof.begin("m2l");
+                ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
+                prof.end(pm);
+                GemmArgs b;
+                b.Kp = Kp;
+                b.ncols = (int)(c1 - c0);
+                b.out_box = Lay.out_box + c0;
+                b.nslots = 1;
+                b.src = Lay.l2l_src + c0;
+                b.ld_src = Lay.ncols;
+                b.tile_mat = Lay.tile_oct + c0 / BN;
+                b.A = ops.l2l;
+                b.X = Pdn;
+                b.Y = Q;
+                b.alpha = std::ldexp(1.0, l) * 0.5; // q += (2^l / 2) L2L_o phi_parent (src/fmm.cpp:590-591)
+                b.beta = 1.0;
+                pm = prof.begin("l2l");
+                ctx.launches += gather_gemm(b, ws, st, ctx.num_sms);
+                prof.end(pm);
+            }
+            pm = prof.begin("pinv_dn");
+            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st);
+            prof.end(pm);
+        }
+        PK_CUDA(cudaEventRecord(ctx.ev[2], st));
+        // ---- periodizing step: far density on the root outer surface ----
+        double *far = nullptr;
+        pm = prof.begin("periodic");
+        if (periodic) {
+            far = ws.get<double>("far_dn", Kp);
+            gemv(req.op->device_matrix(ctx.device, st), ops.K, ops.K, ops.K, Pup, far, 1.0, 0.0, nullptr, 0.0, st);
+            ctx.launches += 1;
+            if (ell >= 2 && ns > 0) {
+                // image layers 2..ell (src/fmm.cpp:635-645): pinv(a_dn, M_img phi_up[0])
+                const double *mimg = ctx.ops.image_operator(ops, axes, ell, st, &ctx.launches);
+                double *qi = ws.get<double>("img_q", Kp), *ti = ws.get<double>("img_t", Kp),
+                       *pi = ws.get<double>("img_phi", Kp);
+                gemv(mimg, ops.K, ops.K, Kp, Pup, qi, 1.0, 0.0, nullptr, 0.0, st);
+                pinv_vec(ctx, ops, false, qi, ti, pi, st);
+                add_kernel<<<(ops.K + 255) / 256, 256, 0, st>>>(far, pi, ops.K);
+                ctx.launches += 2;
+            }
+        }
+        prof.end(pm);
+        PK_CUDA(cudaEventRecord(ctx.ev[3], st));
+        // ---- leaf pass: L2T + W + U + far ----
+        pm = prof.begin("leaf");
+        leaf_pass(g, T, ctx.lists, Pdn, Pup, far, d_out, st);
+        ctx.launches += 1;
+        prof.end(pm);
+        PK_CUDA(cudaEventRecord(ctx.ev[4], st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        prof.finish();
+        if (ctx.profiling) {
+            unsigned long long *cnt = ws.get<unsigned long long>("work_cnt", 8);
+            PK_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), st));
+            work_count_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(T.view(), ops.n, ctx.lists.u.off,
+                                                                   ctx.lists.u.ent, ctx.lists.w.off,
+                                                                   ctx.lists.x.off, ctx.lists.x.ent, cnt);
+            unsigned long long h[8];
+            PK_CUDA(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+            PK_CUDA(cudaStreamSynchronize(st));
+            const double pf = kernel == PKGPU_LAPLACE ? 11.0 : 28.0;
+            const double K = ops.K, dense = 2.0 * K * K, pinv = 4.0 * K * K + K;
+            const double far_pairs = periodic ? (double)nt * ops.n : 0.0;
+            prof.work("leaf", (double)(h[0] + h[1] + h[2]) + far_pairs, pf);
+            prof.work("s2m", (double)h[3], pf);
+            prof.work("x", (double)h[4], pf);
+            prof.work("m2m", (double)h[5], dense);
+            prof.work("m2l", (double)ctx.lists.v_total, dense);
+            prof.work("l2l", (double)h[6], dense);
+            prof.work("pinv_dn", (double)h[6], pinv);
+            prof.work("pinv_up", (double)h[7], pinv);
+            prof.work("periodic", periodic ? 1.0 : 0.0, dense + (ell >= 2 ? dense + pinv : 0.0));
+            auto &u = ctx.stats["u_pairs"];
+            u.units += (double)h[0];
+            u.flops += (double)h[0] * pf;
+        }
+        tm.tree = elapsed(ctx.ev[0], ctx.ev[1]);
+        tm.near = elapsed(ctx.ev[1], ctx.ev[2]) + elapsed(ctx.ev[3], ctx.ev[4]);
+        tm.m2l_apply = elapsed(ctx.ev[2], ctx.ev[3]);
+        tm.far = 0.0; // fused into the leaf pass
+    }
+    if (!req.device_pointers && nt) {
+        PK_CUDA(cudaMemcpyAsync(out, d_out, kt * nt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+    }
+    if (timings) *timings = tm;
+}
+
+void kernel_block_apply_device(pkgpu_context &ctx, int kernel, const double *targets, int64_t nt,
+                               const double *sources, int64_t ns, const double *shift, const double *density,
+                               double *out, int skip) {
+    cudaStream_t st = ctx.stream;
+    Workspace &ws = ctx.ws;
+    const int ks = kernel == 0 ? 1 : 3;
+    double *t = ws.get<double>("kba_t", 3 * nt + 1), *s = ws.get<double>("kba_s", 3 * ns + 1),
+           *d = ws.get<double>("kba_d", ks * ns + 1), *o = ws.get<double>("kba_o", ks * nt + 1),
+           *sh = ws.get<double>("kba_sh", 3);
+    int *coin = ws.get<int>("kba_coin", 1);
+    if (nt) PK_CUDA(cudaMemcpyAsync(t, targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (ns) PK_CUDA(cudaMemcpyAsync(s, sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (ns) PK_CUDA(cudaMemcpyAsync(d, density, ks * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nt) PK_CUDA(cudaMemcpyAsync(o, out, ks * nt * sizeof(double), cudaMemcpyHostToDevice, st));
+    PK_CUDA(cudaMemcpyAsync(sh, shift, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    PK_CUDA(cudaMemsetAsync(coin, 0, sizeof(int), st));
+    // shift == 0 with skip -> coincident pairs contribute 0; anything else is counted
+    direct_pairs(kernel, t, nt, s, d, ns, sh, 1, skip, nullptr, nullptr, o, 1, coin, ws, st);
+    ctx.launches += 1;
+    int hcoin = 0;
+    PK_CUDA(cudaMemcpyAsync(&hcoin, coin, sizeof(int), cudaMemcpyDeviceToHost, st));
+    std::vector<double> res(ks * nt);
+    if (nt) PK_CUDA(cudaMemcpyAsync(res.data(), o, ks * nt * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    // src/kernel.cpp:125-127: coincident pairs are an error unless skip was requested
+    // (the sum itself is still computed with their contribution set to zero)
+    if (hcoin > 0 && !skip)
+        throw InvalidArgument("kernel_block_apply: " + std::to_string(hcoin) + " coincident target/source pairs");
+    std::memcpy(out, res.data(), res.size() * sizeof(double));
+}
+
+} // namespace pkgpu

@@ -1,0 +1,507 @@
+// Pair-sum kernels (FP64 vector pipe). Sources are staged in shared memory in
+// batches of segments (one segment = one source leaf / surface with its image shift);
+// each target is owned by G consecutive lanes that split the sources and combine with
+// warp shuffles, so each output is written once (no atomics, deterministic).
+// The shift is applied to the target, r = (t - shift) - s, as in src/kernel.cpp:90-95.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "pairs.h"
+
+namespace pkgpu {
+
+namespace {
+
+constexpr int NT = 128;
+constexpr int SB = 512;
+constexpr int MAXSEG = 64;
+constexpr int MAXU = 128;
+
+template <int KERNEL> struct Stage {
+    static constexpr int KS = KERNEL == 0 ? 1 : 3;
+    double x[SB], y[SB], z[SB];
+    double d[SB * KS];
+    double sx[MAXSEG], sy[MAXSEG], sz[MAXSEG];
+    int begin[MAXSEG + 1];
+    int cnt[MAXSEG]; // count coincidences in this segment
+    int nseg;
+};
+
+template <int KERNEL>
+__device__ __forceinline__ void accumulate(const Stage<KERNEL> &S, double tx, double ty, double tz, int j, int G,
+                                           double (&acc)[3], int *coincident) {
+    for (int s = 0; s < S.nseg; s++) {
+        const double ux = tx - S.sx[s], uy = ty - S.sy[s], uz = tz - S.sz[s];
+        const int end = S.begin[s + 1];
+        int ncoin = 0;
+        for (int q = S.begin[s] + j; q < end; q += G) {
+            if (KERNEL == 0) {
+                pair_laplace(ux, uy, uz, S.x[q], S.y[q], S.z[q], S.d[q], acc[0]);
+            } else {
+                pair_stokes(ux, uy, uz, S.x[q], S.y[q], S.z[q], S.d[3 * q], S.d[3 * q + 1], S.d[3 * q + 2], acc[0],
+                            acc[1], acc[2]);
+            }
+            if (S.cnt[s]) {
+                const double rx = ux - S.x[q], ry = uy - S.y[q], rz = uz - S.z[q];
+                ncoin += (rx * rx + ry * ry + rz * rz) == 0.0;
+            }
+        }
+        if (ncoin) atomicAdd(coincident, ncoin);
+    }
+}
+
+// one-segment surface stage: points fma(half, t_i, c), density phi[i*ks + a]
+template <int KERNEL>
+__device__ void stage_surface(Stage<KERNEL> &S, const double *__restrict__ tmpl, int i0, int cnt, double cx, double cy,
+                              double cz, double half, const double *__restrict__ phi, double shx, double shy,
+                              double shz) {
+    constexpr int KS = Stage<KERNEL>::KS;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        const int i = i0 + q;
+        S.x[q] = surf_coord(half, tmpl[3 * i], cx);
+        S.y[q] = surf_coord(half, tmpl[3 * i + 1], cy);
+        S.z[q] = surf_coord(half, tmpl[3 * i + 2], cz);
+#pragma unroll
+        for (int a = 0; a < KS; a++) S.d[KS * q + a] = phi[KS * i + a];
+    }
+    if (threadIdx.x == 0) {
+        S.nseg = 1;
+        S.begin[0] = 0;
+        S.begin[1] = cnt;
+        S.sx[0] = shx, S.sy[0] = shy, S.sz[0] = shz;
+        S.cnt[0] = 0;
+    }
+}
+
+template <int KERNEL>
+__device__ __forceinline__ void stage_point(Stage<KERNEL> &S, int q, const double4 *__restrict__ pos,
+                                            const double4 *__restrict__ f, int64_t k) {
+    const double4 p = pos[k];
+    S.x[q] = p.x, S.y[q] = p.y, S.z[q] = p.z;
+    if (KERNEL == 0) {
+        S.d[q] = p.w;
+    } else {
+        const double4 v = f[k];
+        S.d[3 * q] = v.x, S.d[3 * q + 1] = v.y, S.d[3 * q + 2] = v.z;
+    }
+}
+
+__device__ __forceinline__ void box_center(int4 c, double &cx, double &cy, double &cz) {
+    const double h = ldexp(1.0, -c.w);
+    cx = (c.x + 0.5) * h, cy = (c.y + 0.5) * h, cz = (c.z + 0.5) * h;
+}
+
+__device__ __forceinline__ int lanes_per_target(int ntg) {
+    int G = 1;
+    while (G < 32 && ntg * G * 2 <= NT) G *= 2;
+    return G;
+}
+
+__device__ __forceinline__ void shift_of(int code, double &x, double &y, double &z) {
+    int a, b, c;
+    shift_decode(code, a, b, c);
+    x = a, y = b, z = c;
+}
+
+struct LeafParams {
+    TreeView T;
+    int n, Kp;
+    const double *tmpl;
+    const double4 *src_pos, *src_f, *trg_pos;
+    const int *trg_perm, *leaves;
+    const int64_t *u_off, *w_off;
+    const int2 *u_ent, *w_ent;
+    const double *phi_dn, *phi_up, *phi_far;
+    double *out;
+};
+
+template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafParams P) {
+    constexpr int KS = Stage<KERNEL>::KS;
+    __shared__ Stage<KERNEL> S;
+    __shared__ int s_uc[MAXU], s_ucode[MAXU], s_ub[MAXU], s_ue[MAXU];
+    __shared__ int s_segsrc[MAXSEG];
+    __shared__ int s_pos, s_off;
+    const int b = P.leaves[blockIdx.x];
+    const int2 tr = P.T.trng[b];
+    const int ntg = tr.y - tr.x;
+    if (ntg == 0) return;
+    const int4 bc = P.T.cell[b];
+    double cx, cy, cz;
+    box_center(bc, cx, cy, cz);
+    const double scale = ldexp(1.0, bc.w);
+    const int G = lanes_per_target(ntg);
+    const int TPC = NT / G;
+    const int tid = threadIdx.x, j = tid % G;
+    for (int t0 = 0; t0 < ntg; t0 += TPC) {
+        const int t = t0 + tid / G;
+        const bool active = t < ntg;
+        double tx = 0, ty = 0, tz = 0;
+        if (active) {
+            const double4 p = P.trg_pos[tr.x + t];
+            tx = p.x, ty = p.y, tz = p.z;
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        // L2T: outer (downward equivalent) surface of b, density phi_dn[b]
+        {
+            const double half = 0.5 * (kOuter / scale);
+            for (int i0 = 0; i0 < P.n; i0 += SB) {
+                __syncthreads();
+                stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), cx, cy, cz, half,
+                                      P.phi_dn + (int64_t)b * P.Kp, 0.0, 0.0, 0.0);
+                __syncthreads();
+                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+            }
+        }
+        // W: inner (upward equivalent) surfaces of finer well-separated boxes
+        for (int64_t e = P.w_off[b]; e < P.w_off[b + 1]; e++) {
+            const int2 en = P.w_ent[e];
+            const int4 cc = P.T.cell[en.x];
+            double ccx, ccy, ccz, shx, shy, shz;
+            box_center(cc, ccx, ccy, ccz);
+            shift_of(en.y, shx, shy, shz);
+            const double half = 0.5 * (kInner / ldexp(1.0, cc.w));
+            for (int i0 = 0; i0 < P.n; i0 += SB) {
+                __syncthreads();
+                stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), ccx, ccy, ccz, half,
+                                      P.phi_up + (int64_t)en.x * P.Kp, shx, shy, shz);
+                __syncthreads();
+                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+            }
+        }
+        // U: adjacent source leaves, packed into batches of segments
+        const int64_t ub = P.u_off[b], ue = P.u_off[b + 1];
+        for (int64_t e0 = ub; e0 < ue; e0 += MAXU) {
+            const int ne = (int)(int64_t)::min((int64_t)MAXU, ue - e0);
+            __syncthreads();
+            for (int k = tid; k < ne; k += NT) {
+                const int2 en = P.u_ent[e0 + k];
+                const int2 r = P.T.srng[en.x];
+                s_uc[k] = en.x, s_ucode[k] = en.y, s_ub[k] = r.x, s_ue[k] = r.y;
+            }
+            if (tid == 0) {
+                s_pos = 0;
+                s_off = ne > 0 ? 0 : 0;
+            }
+            __syncthreads();
+            if (tid == 0 && ne > 0) s_off = s_ub[0];
+            __syncthreads();
+            while (s_pos < ne) {
+                if (tid == 0) {
+                    int pos = s_pos, off = s_off, fill = 0, nseg = 0;
+                    while (pos < ne && nseg < MAXSEG && fill < SB) {
+                        const int take = min(SB - fill, s_ue[pos] - off);
+                        S.begin[nseg] = fill;
+                        double a, bb, c;
+                        shift_of(s_ucode[pos], a, bb, c);
+                        S.sx[nseg] = a, S.sy[nseg] = bb, S.sz[nseg] = c;
+                        S.cnt[nseg] = 0;
+                        s_segsrc[nseg] = off;
+                        fill += take;
+                        off += take;
+                        nseg++;
+                        if (off >= s_ue[pos]) {
+                            pos++;
+                            if (pos < ne) off = s_ub[pos];
+                        }
+                    }
+                    S.begin[nseg] = fill;
+                    S.nseg = nseg;
+                    s_pos = pos;
+                    s_off = off;
+                }
+                __syncthreads();
+                for (int sg = 0; sg < S.nseg; sg++) {
+                    const int beg = S.begin[sg], len = S.begin[sg + 1] - beg, src0 = s_segsrc[sg];
+                    for (int q = tid; q < len; q += NT) stage_point<KERNEL>(S, beg + q, P.src_pos, P.src_f, src0 + q);
+                }
+                __syncthreads();
+                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+                __syncthreads();
+            }
+        }
+        // far field: root outer surface with the periodizing density (image layers
+        // 2..ell + T_M2L, summed: both live on the same surface)
+        if (P.phi_far) {
+            const double half = 0.5 * kOuter;
+            for (int i0 = 0; i0 < P.n; i0 += SB) {
+                __syncthreads();
+                stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), 0.5, 0.5, 0.5, half, P.phi_far, 0.0, 0.0,
+                                      0.0);
+                __syncthreads();
+                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+            }
+        }
+        // combine the G lanes of each target
+        for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int a = 0; a < KS; a++) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
+        if (active && j == 0) {
+            const int64_t orig = P.trg_perm[tr.x + t];
+#pragma unroll
+            for (int a = 0; a < KS; a++) P.out[orig * KS + a] = KERNEL == 0 ? acc[a] : kOneOver8Pi * acc[a];
+        }
+    }
+}
+
+struct CheckParams {
+    TreeView T;
+    int n, Kp;
+    const double *tmpl;
+    const double4 *src_pos, *src_f;
+    const int *boxes; // leaves (s2m) or null (x: all boxes)
+    const int64_t *x_off;
+    const int2 *x_ent;
+    double *q;
+};
+
+// S2M (upward check = outer surface) or X/S2L (downward check = inner surface)
+template <int KERNEL, bool XLIST> __global__ void __launch_bounds__(NT) check_kernel(CheckParams P) {
+    constexpr int KS = Stage<KERNEL>::KS;
+    __shared__ Stage<KERNEL> S;
+    const int b = XLIST ? blockIdx.x : P.boxes[blockIdx.x];
+    int64_t e0 = 0, e1 = 1;
+    if (XLIST) {
+        e0 = P.x_off[b], e1 = P.x_off[b + 1];
+        if (e0 == e1) return;
+    } else {
+        const int2 r = P.T.srng[b];
+        if (r.y == r.x) return;
+    }
+    const int4 bc = P.T.cell[b];
+    double cx, cy, cz;
+    box_center(bc, cx, cy, cz);
+    const double scale = ldexp(1.0, bc.w);
+    const double half = 0.5 * ((XLIST ? kInner : kOuter) / scale);
+    const int tid = threadIdx.x;
+    for (int i0 = 0; i0 < P.n; i0 += NT) {
+        const int i = i0 + tid;
+        const bool active = i < P.n;
+        double tx = 0, ty = 0, tz = 0;
+        if (active) {
+            tx = surf_coord(half, P.tmpl[3 * i], cx);
+            ty = surf_coord(half, P.tmpl[3 * i + 1], cy);
+            tz = surf_coord(half, P.tmpl[3 * i + 2], cz);
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int64_t e = e0; e < e1; e++) {
+            int c = b, code = shift_code(0, 0, 0);
+            if (XLIST) {
+                const int2 en = P.x_ent[e];
+                c = en.x, code = en.y;
+            }
+            const int2 r = P.T.srng[c];
+            double shx, shy, shz;
+            shift_of(code, shx, shy, shz);
+            for (int s0 = r.x; s0 < r.y; s0 += SB) {
+                const int cnt = min(SB, r.y - s0);
+                __syncthreads();
+                for (int q = tid; q < cnt; q += NT) stage_point<KERNEL>(S, q, P.src_pos, P.src_f, s0 + q);
+                if (tid == 0) {
+                    S.nseg = 1, S.begin[0] = 0, S.begin[1] = cnt, S.cnt[0] = 0;
+                    S.sx[0] = shx, S.sy[0] = shy, S.sz[0] = shz;
+                }
+                __syncthreads();
+                if (active) accumulate<KERNEL>(S, tx, ty, tz, 0, 1, acc, nullptr);
+            }
+        }
+        if (active) {
+            double *q = P.q + (int64_t)b * P.Kp + KS * i;
+#pragma unroll
+            for (int a = 0; a < KS; a++) {
+                const double v = KERNEL == 0 ? acc[a] : kOneOver8Pi * acc[a];
+                if (XLIST)
+                    q[a] += v;
+                else
+                    q[a] = v;
+            }
+        }
+    }
+}
+
+struct DirectParams {
+    const double *trg, *src, *den;
+    int64_t nt, ns;
+    const double *offs; // noff x 3
+    int noff, skip_zero;
+    int n;              // far surface points (0 = none)
+    const double *tmpl, *phi_far;
+    double *out;
+    int accumulate;
+    int *coincident;
+};
+
+template <int KERNEL> __global__ void __launch_bounds__(NT) direct_kernel(DirectParams P) {
+    constexpr int KS = Stage<KERNEL>::KS;
+    __shared__ Stage<KERNEL> S;
+    const int tid = threadIdx.x;
+    const int64_t t = blockIdx.x * (int64_t)NT + tid;
+    const bool active = t < P.nt;
+    double tx = 0, ty = 0, tz = 0;
+    if (active) tx = P.trg[3 * t], ty = P.trg[3 * t + 1], tz = P.trg[3 * t + 2];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int o = 0; o < P.noff; o++) {
+        const double ox = P.offs[3 * o], oy = P.offs[3 * o + 1], oz = P.offs[3 * o + 2];
+        const bool zero = ox == 0.0 && oy == 0.0 && oz == 0.0;
+        for (int64_t s0 = 0; s0 < P.ns; s0 += SB) {
+            const int cnt = (int)(int64_t)::min((int64_t)SB, P.ns - s0);
+            __syncthreads();
+            for (int q = tid; q < cnt; q += NT) {
+                const int64_t k = s0 + q;
+                S.x[q] = P.src[3 * k], S.y[q] = P.src[3 * k + 1], S.z[q] = P.src[3 * k + 2];
+#pragma unroll
+                for (int a = 0; a < KS; a++) S.d[KS * q + a] = P.den[KS * k + a];
+            }
+            if (tid == 0) {
+                S.nseg = 1, S.begin[0] = 0, S.begin[1] = cnt;
+                S.sx[0] = ox, S.sy[0] = oy, S.sz[0] = oz;
+                S.cnt[0] = (zero && P.skip_zero) ? 0 : 1;
+            }
+            __syncthreads();
+            if (active) accumulate<KERNEL>(S, tx, ty, tz, 0, 1, acc, P.coincident);
+        }
+    }
+    if (P.n > 0) {
+        for (int i0 = 0; i0 < P.n; i0 += SB) {
+            __syncthreads();
+            stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), 0.5, 0.5, 0.5, 0.5 * kOuter, P.phi_far, 0.0, 0.0,
+                                  0.0);
+            __syncthreads();
+            if (active) accumulate<KERNEL>(S, tx, ty, tz, 0, 1, acc, nullptr);
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int a = 0; a < KS; a++) {
+            const double v = KERNEL == 0 ? acc[a] : kOneOver8Pi * acc[a];
+            if (P.accumulate)
+                P.out[KS * t + a] += v;
+            else
+                P.out[KS * t + a] = v;
+        }
+    }
+}
+
+struct RootParams {
+    int n;
+    const double *tmpl, *src, *den;
+    int64_t ns;
+    int nsplit;
+    double *part; // nsplit x (ks n)
+};
+
+template <int KERNEL> __global__ void __launch_bounds__(NT) root_check_kernel(RootParams P) {
+    constexpr int KS = Stage<KERNEL>::KS;
+    __shared__ Stage<KERNEL> S;
+    const int tid = threadIdx.x;
+    const int i = blockIdx.x * NT + tid;
+    const bool active = i < P.n;
+    const int64_t sb = P.ns * blockIdx.y / P.nsplit, se = P.ns * (blockIdx.y + 1) / P.nsplit;
+    double tx = 0, ty = 0, tz = 0;
+    const double half = 0.5 * kOuter;
+    if (active) {
+        tx = surf_coord(half, P.tmpl[3 * i], 0.5);
+        ty = surf_coord(half, P.tmpl[3 * i + 1], 0.5);
+        tz = surf_coord(half, P.tmpl[3 * i + 2], 0.5);
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t s0 = sb; s0 < se; s0 += SB) {
+        const int cnt = (int)(int64_t)::min((int64_t)SB, se - s0);
+        __syncthreads();
+        for (int q = tid; q < cnt; q += NT) {
+            const int64_t k = s0 + q;
+            S.x[q] = P.src[3 * k], S.y[q] = P.src[3 * k + 1], S.z[q] = P.src[3 * k + 2];
+#pragma unroll
+            for (int a = 0; a < KS; a++) S.d[KS * q + a] = P.den[KS * k + a];
+        }
+        if (tid == 0) {
+            S.nseg = 1, S.begin[0] = 0, S.begin[1] = cnt, S.cnt[0] = 0;
+            S.sx[0] = 0.0, S.sy[0] = 0.0, S.sz[0] = 0.0;
+        }
+        __syncthreads();
+        if (active) accumulate<KERNEL>(S, tx, ty, tz, 0, 1, acc, nullptr);
+    }
+    if (active)
+#pragma unroll
+        for (int a = 0; a < KS; a++)
+            P.part[(int64_t)blockIdx.y * KS * P.n + KS * i + a] = KERNEL == 0 ? acc[a] : kOneOver8Pi * acc[a];
+}
+
+__global__ void split_sum_kernel(const double *part, int nsplit, int len, double *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    double v = 0.0;
+    for (int s = 0; s < nsplit; s++) v += part[(int64_t)s * len + i];
+    out[i] = v;
+}
+
+} // namespace
+
+void leaf_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, const double *phi_dn,
+               const double *phi_up, const double *phi_far, double *out, cudaStream_t st) {
+    if (T.nleaves == 0) return;
+    LeafParams P{T.view(), g.n,         g.Kp,       g.tmpl,   T.src_pos, T.src_f, T.trg_pos, T.trg_perm, T.leaves,
+                 L.u.off,  L.w.off,     L.u.ent,    L.w.ent,  phi_dn,    phi_up,  phi_far,   out};
+    if (g.kernel == 0)
+        leaf_kernel<0><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+    else
+        leaf_kernel<1><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+    PK_CUDA(cudaGetLastError());
+}
+
+void s2m_pass(const PairGeom &g, const DeviceTree &T, double *q, cudaStream_t st) {
+    if (T.nleaves == 0) return;
+    CheckParams P{T.view(), g.n, g.Kp, g.tmpl, T.src_pos, T.src_f, T.leaves, nullptr, nullptr, q};
+    if (g.kernel == 0)
+        check_kernel<0, false><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+    else
+        check_kernel<1, false><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+    PK_CUDA(cudaGetLastError());
+}
+
+void x_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, double *q, cudaStream_t st) {
+    if (L.x.count == 0) return;
+    CheckParams P{T.view(), g.n, g.Kp, g.tmpl, T.src_pos, T.src_f, nullptr, L.x.off, L.x.ent, q};
+    if (g.kernel == 0)
+        check_kernel<0, true><<<(unsigned)T.nboxes, NT, 0, st>>>(P);
+    else
+        check_kernel<1, true><<<(unsigned)T.nboxes, NT, 0, st>>>(P);
+    PK_CUDA(cudaGetLastError());
+}
+
+void direct_pairs(int kernel, const double *d_trg, int64_t nt, const double *d_src, const double *d_den, int64_t ns,
+                  const double *d_offsets, int noff, int skip_zero, const PairGeom *far_geom, const double *phi_far,
+                  double *d_out, int accumulate, int *d_coincident, Workspace &, cudaStream_t st) {
+    if (nt == 0) return;
+    DirectParams P{d_trg,    d_src,
+                   d_den,    nt,
+                   ns,       d_offsets,
+                   noff,     skip_zero,
+                   far_geom && phi_far ? far_geom->n : 0,
+                   far_geom ? far_geom->tmpl : nullptr,
+                   phi_far,  d_out,
+                   accumulate, d_coincident};
+    const unsigned grid = (unsigned)((nt + NT - 1) / NT);
+    if (kernel == 0)
+        direct_kernel<0><<<grid, NT, 0, st>>>(P);
+    else
+        direct_kernel<1><<<grid, NT, 0, st>>>(P);
+    PK_CUDA(cudaGetLastError());
+}
+
+void root_check_potential(const PairGeom &g, const double *d_src, const double *d_den, int64_t ns, double *d_q,
+                          Workspace &ws, cudaStream_t st) {
+    const int ks = g.kernel == 0 ? 1 : 3;
+    const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(256, ns / 1024));
+    const int len = ks * g.n;
+    double *part = ws.get<double>("root_part", (size_t)nsplit * len);
+    RootParams P{g.n, g.tmpl, d_src, d_den, ns, nsplit, part};
+    dim3 grid((g.n + NT - 1) / NT, nsplit);
+    if (g.kernel == 0)
+        root_check_kernel<0><<<grid, NT, 0, st>>>(P);
+    else
+        root_check_kernel<1><<<grid, NT, 0, st>>>(P);
+    split_sum_kernel<<<(len + 255) / 256, 256, 0, st>>>(part, nsplit, len, d_q);
+    PK_CUDA(cudaGetLastError());
+}
+
+} // namespace pkgpu

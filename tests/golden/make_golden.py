@@ -247,10 +247,42 @@ def golden_direct(tmp):
     np.savez_compressed(os.path.join(HERE, "direct_and_errors.npz"), **out)
 
 
+def golden_kblock(tmp):
+    """kernel_block (src/kernel.cpp:54-78) on the KIFMM surfaces: a_up, a_dn, canonical
+    M2L class matrices and image-offset blocks, for bit-exact operator assembly checks."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import pkifmm_oracle as O
+    out = {}
+    for kernel, plist in (("laplace", (4, 6)), ("stokeslet", (4,))):
+        for p in plist:
+            inner = O.surface_points(p, (0.5, 0.5, 0.5), 1.05)
+            outer = O.surface_points(p, (0.5, 0.5, 0.5), 2.95)
+            pairs = {"a_up": (outer, inner), "a_dn": (inner, outer)}
+            for d in ((3, 1, 0), (2, 2, 2), (3, 3, 1), (2, 0, 0)):
+                pairs["cls_%d%d%d" % d] = (inner, inner + np.array(d, dtype=float))
+            for o in (0, 5):
+                c = np.array([0.5 + (0.25 if o & 1 else -0.25), 0.5 + (0.25 if o & 2 else -0.25),
+                              0.5 + (0.25 if o & 4 else -0.25)])
+                ci = O.surface_points(p, c, 0.5 * 1.05)
+                pairs[f"m2m_{o}"] = (outer, ci)
+                pairs[f"l2l_{o}"] = (ci, outer)
+            for tag, (trg, src) in pairs.items():
+                pt, ps = save_pts(tmp, "kt", trg), save_pts(tmp, "ks", src)
+                r = run("kblock", "--kernel", kernel, "--trg", pt, "--src", ps, "--out", os.path.join(tmp, "kb"))
+                out[f"{kernel}_p{p}_{tag}"] = f64(os.path.join(tmp, "kb.kb.f64")).reshape(r["rows"], r["cols"])
+    np.savez_compressed(os.path.join(HERE, "kblock.npz"), **out)
+
+
 def main():
     if not os.path.exists(REFDUMP):
         sys.exit("build oracle/_ref first: make -C oracle/refbuild")
+    only = sys.argv[1:]
     with tempfile.TemporaryDirectory() as tmp:
+        if only:
+            for name in only:
+                globals()["golden_" + name](tmp)
+            return
+        golden_kblock(tmp)
         golden_pairs(tmp)
         golden_surfaces(tmp)
         golden_trees(tmp)

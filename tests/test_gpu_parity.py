@@ -1,0 +1,256 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's golden
+vectors and the numpy oracle. Bit-exact for trees, lists and operator assembly; the
+SURVEY §8(c) protocol for floating-point fields."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1705_02043_b200 as pk
+import pkifmm_oracle as O
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+KMAP = {"laplace": pk.KernelSpec.laplace(), "stokeslet": pk.KernelSpec.stokeslet()}
+OKMAP = {"laplace": O.LAPLACE, "stokeslet": O.STOKESLET}
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+# ---------------------------------------------------------------------------
+# primitives
+
+@pytest.mark.parametrize("kernel", ["laplace", "stokeslet"])
+@pytest.mark.parametrize("tag", ["s0_skip", "s0_noskip", "shift"])
+def test_kernel_block_apply(kernel, tag):
+    g = load("pairs.npz")
+    k = f"{kernel}_{tag}"
+    out = np.zeros_like(g[k + "_pot"])
+    err = str(g[k + "_error"])
+    args = (KMAP[kernel], g[k + "_trg"], g[k + "_src"], g[k + "_shift"], g[k + "_den"], out, bool(g[k + "_skip"]))
+    if err:
+        with pytest.raises(ValueError) as e:
+            pk.kernel_block_apply(*args)
+        assert str(e.value) == err
+        return
+    pk.kernel_block_apply(*args)
+    ref = g[k + "_pot"]
+    # per-target cancellation-aware bound
+    scale = np.zeros_like(ref)
+    O.kernel_block_apply(OKMAP[kernel], g[k + "_trg"], g[k + "_src"], g[k + "_shift"], np.abs(g[k + "_den"]), scale,
+                         True)
+    assert np.all(np.abs(out - ref) <= 1e-12 * np.abs(scale) + 1e-300)
+
+
+@pytest.mark.parametrize("key", ["laplace_p4", "laplace_p6", "stokeslet_p4"])
+def test_operator_assembly_bit_exact(key):
+    """a_up, a_dn, canonical M2L class matrices, M2M/L2L octants: kernel_block bit-exact."""
+    g = load("kblock.npz")
+    kernel, p = key.split("_p")
+    p = int(p)
+    ks = KMAP[kernel]
+    for name in g.files:
+        if not name.startswith(key + "_"):
+            continue
+        tag = name[len(key) + 1:]
+        if tag in ("a_up", "a_dn"):
+            m = pk.kifmm_matrix(ks, p, tag)
+        elif tag.startswith("cls_"):
+            d = tuple(int(c) for c in tag[4:])
+            m = pk.kifmm_matrix(ks, p, "m2l", *d)
+        else:
+            kind, o = tag.split("_")
+            m = pk.kifmm_matrix(ks, p, kind, int(o))
+        assert np.array_equal(m, g[name]), name
+
+
+@pytest.mark.parametrize("kernel", ["laplace", "stokeslet"])
+def test_m2l_symmetry_expansion(kernel):
+    """Every one of the 316 offset matrices equals K(inner, inner + d) up to the ulp-level
+    difference of evaluating it through the octahedral symmetry (src/fmm.cpp:111-130)."""
+    ks = KMAP[kernel]
+    p = 4
+    inner = O.surface_points(p, (0.5, 0.5, 0.5), 1.05)
+    for d in [(-3, 1, 2), (2, -2, 0), (0, 0, -3), (-2, 3, -1), (3, 3, 3), (-3, -3, 2)]:
+        m = pk.kifmm_matrix(ks, p, "m2l", *d)
+        ref = O.kernel_block(OKMAP[kernel], inner, inner + np.array(d, dtype=float))
+        err = np.max(np.abs(m - ref)) / np.max(np.abs(ref))
+        assert err <= 2e-15, (d, err)
+
+
+def test_image_operator_matches_oracle():
+    ks = pk.KernelSpec.laplace()
+    for mask, ell in ((4, 2), (3, 2), (7, 2), (7, 3)):
+        axes = tuple(bool(mask >> a & 1) for a in range(3))
+        m = pk.kifmm_matrix(ks, 4, "img", mask, ell)
+        ops = O.make_operators(O.LAPLACE, 4)
+        ref = O.root_image_operator(ops, axes, ell)
+        assert np.max(np.abs(m - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+
+# ---------------------------------------------------------------------------
+# tree + lists (bit-exact gates)
+
+@pytest.mark.parametrize("name", ["uniform3k", "adaptive", "cfg1"])
+def test_tree_bit_exact(name):
+    g = load(f"tree_{name}.npz")
+    t = pk.FmmTree(g["src"], g["trg"], int(g["leaf"]))
+    table, s, tr = t.boxes()
+    assert np.array_equal(table, g["boxes"])
+    assert np.array_equal(s, g["srcidx"]) and np.array_equal(tr, g["trgidx"])
+    assert t.structure_hash() == int(g["hash"])
+
+
+VARIANTS = {"none": None, "sp": pk.PeriodicSetup.make(pk.Periodicity.sp),
+            "dp": pk.PeriodicSetup.make(pk.Periodicity.dp), "tp": pk.PeriodicSetup.make(pk.Periodicity.tp),
+            "spx": pk.PeriodicSetup(pk.Periodicity.sp, (True, False, False), 1.0, 2)}
+
+
+@pytest.mark.parametrize("name,variant", [(n, v) for n in ("uniform3k", "adaptive") for v in VARIANTS]
+                         + [("cfg1", "spx"), ("cfg1", "none")])
+def test_lists_bit_exact(name, variant):
+    g = load(f"tree_{name}.npz")
+    t = pk.FmmTree(g["src"], g["trg"], int(g["leaf"]))
+    for lst in "uvwx":
+        off, ent = t.lists(VARIANTS[variant], lst)
+        got = O.sorted_multiset(off, ent)
+        ref = O.sorted_multiset(g[f"{variant}_{lst}_off"], g[f"{variant}_{lst}_ent"])
+        assert got == ref, (variant, lst)
+
+
+@pytest.mark.parametrize("cfg,kind,n,leaf,ks,kw,expect", [
+    ("c1", "uniform", 20000, 50, 1, {}, 0xCAB94680C89A1EE4),
+    ("c2", "uniform", 100000, 50, 3, {}, 0x6291641A7A150CB9),
+    ("c3", "clusters", 1000000, 64, 3, dict(nclusters=8, sigma=0.04, periodic_axes=(True, True, False)),
+     0x734159F57095BF50),
+])
+def test_structure_hash_at_baseline_sizes(cfg, kind, n, leaf, ks, kw, expect):
+    """structure_hash of the BASELINE configs' trees, bit-exact."""
+    pts, _ = pk.generate(kind, n, ks, seed=12345, **kw)
+    t = pk.FmmTree(pts, pts, leaf)
+    assert t.structure_hash() == expect
+
+
+def test_tree_errors():
+    pts = np.array([[0.5, 0.5, 0.5], [1.0, 0.2, 0.2], [0.1, -0.3, 0.2]])
+    with pytest.raises(ValueError, match=r"FmmTree: 2 points outside \[0,1\)\^3: source\[1\]=\(1,0.2,0.2\)"):
+        pk.FmmTree(pts, pts[:1], 10)
+    dup = np.full((5, 3), 0.25)
+    with pytest.raises(RuntimeError, match="leaf over capacity at maximum depth 12"):
+        pk.FmmTree(dup, dup, 2)
+
+
+# ---------------------------------------------------------------------------
+# evaluate (end to end)
+
+EVAL_ALL = ["lap_none_p6", "lap_sp_p8", "lap_spx_p8", "lap_dp_p6", "lap_tp_p8", "lap_tp_p6_ell1", "sto_none_p6",
+            "sto_tp_p6", "sto_tp_p8", "sto_dp_p6", "cfg1"]
+
+
+def golden_request(g):
+    meta = json.loads(str(g["meta"]))
+    k = KMAP[meta["kernel"]]
+    per = pk.Periodicity.from_name(meta["per"])
+    setup = pk.PeriodicSetup.make(per, meta["ell"])
+    if meta["axes"]:
+        setup.axes = tuple(a in meta["axes"] for a in "xyz")
+    op = None
+    if meta["op"]:
+        op = pk.load_operator(os.path.join(GOLDEN, "ops", meta["op"]))
+        if meta["relabel"]:
+            op.relabel(k, setup)
+    return pk.EvalRequest(kernel=k, sources=g["src"], strengths=g["str"], targets=g["src"], setup=setup,
+                          p=meta["p"], op=op, leaf_capacity=meta["leaf"]), meta
+
+
+@pytest.mark.parametrize("name", EVAL_ALL)
+def test_evaluate_vs_reference(name):
+    """rel-L2 <= 1e-10 where the oracle's own spread allows, else
+    <= 10 x the reference's thread-count self-spread."""
+    g = load(f"eval_{name}.npz")
+    req, meta = golden_request(g)
+    res = pk.evaluate(req)
+    rel = rel_l2(res.potentials, g["pot"])
+    tol = max(1e-10, 10 * float(g["self_spread"]))
+    print(f"{name}: rel-L2 {rel:.3e} (self-spread {float(g['self_spread']):.1e}, tol {tol:.1e})")
+    assert rel <= tol
+
+
+@pytest.mark.parametrize("name", ["sto_tp_p6", "sto_none_p6", "lap_tp_p6_ell1"])
+def test_evaluate_vs_oracle_shared_factors(name):
+    """Stage-level parity with shared SVD factors: GPU and numpy oracle use identical
+    pseudo-inverse factors, so only summation order differs."""
+    g = load(f"eval_{name}.npz")
+    req, meta = golden_request(g)
+    ok = OKMAP[meta["kernel"]]
+    ops = O.make_operators(ok, meta["p"])
+    ctx = pk.Context(0)
+    pk.set_kifmm_factors(req.kernel, meta["p"], (ops.a_up.u, ops.a_up.sigma, ops.a_up.vt),
+                         (ops.a_dn.u, ops.a_dn.sigma, ops.a_dn.vt), context=ctx)
+    res = pk.evaluate(req, context=ctx)
+    per = {"none": O.NONE, "sp": O.SP, "dp": O.DP, "tp": O.TP}[meta["per"]]
+    opd = O.load_operator(os.path.join(GOLDEN, "ops", meta["op"])) if meta["op"] else None
+    ref = O.evaluate(ok, g["src"], g["str"], g["src"], per=per, ell=meta["ell"], p=meta["p"], op=opd,
+                     leaf_capacity=meta["leaf"], ops=ops)
+    rel = rel_l2(res.potentials, ref)
+    print(f"{name}: GPU vs oracle (shared factors) rel-L2 {rel:.3e}")
+    assert rel <= max(1e-11, 3 * float(g["self_spread"]))
+    ctx.close()
+
+
+def test_direct_mode_and_errors():
+    g = load("direct_and_errors.npz")
+    op = pk.load_operator(os.path.join(GOLDEN, "ops", "laplace_sp_ell2_p8_gated.pkm2l"))
+    setup = pk.PeriodicSetup.make(pk.Periodicity.sp)
+    for mode in ("direct", "fmm"):
+        req = pk.EvalRequest(kernel=pk.KernelSpec.laplace(), sources=g["src"], strengths=g["str"], targets=g["trg"],
+                             setup=setup, p=8, op=op, mode=pk.EvalMode[mode], leaf_capacity=1000)
+        res = pk.evaluate(req)
+        assert np.allclose(res.potentials, g[f"{mode}_pot"], rtol=1e-12, atol=1e-12), mode
+    # Madelung -8 ln 2 (src/experiments.cpp:27): q0 potential x charge + q2 ... /2
+    errs = json.loads(str(g["errors"]))
+    base = dict(kernel=pk.KernelSpec.laplace(), setup=setup, p=8, op=op)
+    bad = g["src"].copy()
+    bad[1] = [1.0, 0.5, 0.5]
+    bad[2] = [-0.25, 0.5, 2.5]
+    cases = {
+        "outside": (pk.EvalRequest(sources=bad, strengths=g["str"], targets=bad, **base), ValueError),
+        "compat": (pk.EvalRequest(sources=g["src"], strengths=[1.0, 1.0, 1.0, -1.0], targets=g["src"], **base),
+                   pk.ConfigError),
+        "strlen": (pk.EvalRequest(sources=g["src"], strengths=[1.0, -1.0], targets=g["src"], **base), ValueError),
+        "provenance": (pk.EvalRequest(sources=g["src"], strengths=g["str"], targets=g["src"],
+                                      **{**base, "p": 6}), pk.ConfigError),
+        "noop": (pk.EvalRequest(sources=g["src"], strengths=g["str"], targets=g["src"], **{**base, "op": None}),
+                 pk.ConfigError),
+    }
+    for name, (req, exc) in cases.items():
+        with pytest.raises(exc) as e:
+            pk.evaluate(req)
+        assert str(e.value) == errs[name]["what"], name
+
+
+def test_linearity_and_determinism_cfg2_scale():
+    """Size-independent properties at the BASELINE cfg2 size (N = 100k, Stokes TP p=8):
+    bitwise run-to-run determinism and linearity in the strengths."""
+    pts, f = pk.generate("uniform", 100000, 3, seed=12345)
+    op = pk.load_operator(os.path.join(GOLDEN, "ops", "stokeslet_tp_ell2_p8_gated.pkm2l"))
+    setup = pk.PeriodicSetup.make(pk.Periodicity.tp)
+    mk = lambda q: pk.EvalRequest(kernel=pk.KernelSpec.stokeslet(), sources=pts, strengths=q, targets=pts,
+                                  setup=setup, p=8, op=op, leaf_capacity=50)
+    a = pk.evaluate(mk(f)).potentials
+    b = pk.evaluate(mk(f)).potentials
+    assert np.array_equal(a, b)
+    rng = np.random.default_rng(1)
+    f2 = rng.standard_normal((len(pts), 3))
+    f2 = (f2 - f2.mean(0)).reshape(-1)
+    c = pk.evaluate(mk(f2)).potentials
+    d = pk.evaluate(mk(2.0 * f - 0.5 * f2)).potentials
+    assert rel_l2(d, 2.0 * a - 0.5 * c) < 1e-9
