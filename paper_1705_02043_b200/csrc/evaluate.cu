@@ -46,31 +46,48 @@ __global__ void compat_partial_kernel(const double *__restrict__ s, int64_t n, i
         for (int c = 0; c < 4; c++) part[4 * blockIdx.x + c] = red[c][0];
 }
 
-__global__ void layout_keys_kernel(TreeView T, int *keys, int *vals) {
+__global__ void layout_keys_kernel(TreeView T, int *keys, int *vals, int *hist) {
+    __shared__ int h[kMaxLevels * 8];
+    for (int i = threadIdx.x; i < kMaxLevels * 8; i += blockDim.x) h[i] = 0;
+    __syncthreads();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= T.nboxes) return;
-    const int4 c = T.cell[b];
-    keys[b] = c.w * 8 + ((c.x & 1) | ((c.y & 1) << 1) | ((c.z & 1) << 2));
-    vals[b] = b;
+    if (b < T.nboxes) {
+        const int4 c = T.cell[b];
+        const int k = c.w * 8 + ((c.x & 1) | ((c.y & 1) << 1) | ((c.z & 1) << 2));
+        keys[b] = k;
+        vals[b] = b;
+        atomicAdd(&h[k], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kMaxLevels * 8; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
+// Two column layouts per level (see build_layout):
+//   oct  : boxes grouped by octant, each group padded to 64 -> octant-homogeneous tiles (L2L)
+//   m2l  : the oct layout on big levels, plain Morton order (= BFS order) on small ones
 __global__ void layout_fill_kernel(TreeView T, const int *__restrict__ skeys, const int *__restrict__ sboxes,
-                                   const int *__restrict__ group_start, const int *__restrict__ group_col,
-                                   int *col_of_box, int *out_box, int *out_m2m, int *l2l_src, int *m2m_src,
-                                   int64_t ncols, int *tile_oct) {
+                                   const int *__restrict__ group_start, const int *__restrict__ oct_gcol,
+                                   const int *__restrict__ m2l_gcol, const int *__restrict__ m2l_base,
+                                   const int *__restrict__ grouped, int *col_of_box, int *out_box, int *out_m2m,
+                                   int *m2m_src, int64_t ncols_m2l, int *out_oct, int *l2l_src, int *tile_oct) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= T.nboxes) return;
     const int key = skeys[i], b = sboxes[i];
-    const int col = group_col[key] + (i - group_start[key]);
+    const int lvl = key / 8;
+    const int rank = i - group_start[key];
+    const int ocol = oct_gcol[key] + rank;
+    out_oct[ocol] = b;
+    l2l_src[ocol] = T.parent[b];
+    tile_oct[ocol / BN] = key & 7;
+    const int col = grouped[lvl] ? m2l_gcol[key] + rank : m2l_base[lvl] + (int)(b - T.level_off[lvl]);
     col_of_box[b] = col;
     out_box[col] = b;
     const bool leaf = T.isleaf[b] != 0;
     out_m2m[col] = leaf ? -1 : b;
-    l2l_src[col] = T.parent[b];
-    tile_oct[col / BN] = key & 7;
     for (int o = 0; o < 8; o++) {
         const int c = leaf ? -1 : T.child[8 * b + o];
-        m2m_src[(int64_t)o * ncols + col] = (c >= 0 && T.srng[c].y > T.srng[c].x) ? c : -1;
+        m2m_src[(int64_t)o * ncols_m2l + col] = (c >= 0 && T.srng[c].y > T.srng[c].x) ? c : -1;
     }
 }
 
@@ -172,67 +189,94 @@ __global__ void work_count_kernel(TreeView T, int n, const int64_t *__restrict__
 }
 
 struct Layout {
-    std::vector<int64_t> colbase; // per level, size depth + 2
-    int64_t ncols = 0;
-    int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *l2l_src = nullptr, *m2m_src = nullptr,
-        *tile_oct = nullptr, *m2l_table = nullptr;
+    std::vector<int64_t> colbase, octbase; // per level (size depth + 2): m2l and oct layouts
+    int64_t ncols = 0, noct = 0;
+    int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
+    int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
 };
 
-// Columns of the gather-GEMMs: per level, boxes grouped by octant (cell parity) in
-// Morton order, each group padded to a multiple of 64 -> every column tile is
-// octant-homogeneous (one L2L matrix per tile; M2L tiles share their offset set).
+// Columns of the gather-GEMMs. Octant grouping makes every 64-column M2L tile share
+// one offset set (~189 of 316 slots active, no zero columns) at the price of padding
+// each octant group to 64; it pays once a level has >= 1024 boxes. Smaller levels keep
+// Morton order for M2L/M2M (one padded group). L2L always uses the octant layout so each
+// tile has a single L2L matrix.
 Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
     Workspace &ws = ctx.ws;
     const int nb = (int)T.nboxes;
     const TreeView tv = T.view();
     int *keys = ws.get<int>("lay_keys", nb), *vals = ws.get<int>("lay_vals", nb);
     int *skeys = ws.get<int>("lay_skeys", nb), *svals = ws.get<int>("lay_svals", nb);
-    layout_keys_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, keys, vals);
+    constexpr int NK = kMaxLevels * 8;
+    int *d_hist = ws.get<int>("lay_hist", NK);
+    PK_CUDA(cudaMemsetAsync(d_hist, 0, NK * sizeof(int), st));
+    layout_keys_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, keys, vals, d_hist);
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, svals, nb, 0, 7, st);
     void *tmp = ws.get<char>("lay_temp", tb);
     PK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, vals, svals, nb, 0, 7, st));
-    std::vector<int> hk(nb);
-    PK_CUDA(cudaMemcpyAsync(hk.data(), skeys, nb * sizeof(int), cudaMemcpyDeviceToHost, st));
-    PK_CUDA(cudaStreamSynchronize(st));
     ctx.launches += 5;
-    constexpr int NK = kMaxLevels * 8;
-    std::vector<int> count(NK, 0), start(NK, 0), gcol(NK, 0);
-    for (int k : hk) count[k]++;
+    std::vector<int> count(NK, 0), start(NK, 0), ogcol(NK, 0), mgcol(NK, 0), mbase(kMaxLevels + 1, 0),
+        grouped(kMaxLevels + 1, 0);
+    PK_CUDA(cudaMemcpyAsync(count.data(), d_hist, NK * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
     Layout L;
     L.colbase.assign(T.depth + 2, 0);
+    L.octbase.assign(T.depth + 2, 0);
     int s = 0;
-    int64_t c = 0;
-    for (int k = 0; k < NK; k++) {
-        const int lvl = k / 8;
-        if (k % 8 == 0 && lvl <= T.depth) L.colbase[lvl] = c;
-        start[k] = s;
-        gcol[k] = (int)c;
-        s += count[k];
-        c += (count[k] + BN - 1) / BN * BN;
+    int64_t co = 0, cm = 0;
+    for (int l = 0; l <= T.depth; l++) {
+        const int64_t nl = T.level_off[l + 1] - T.level_off[l];
+        // octant grouping streams ~189 offsets over padded groups; Morton order streams
+        // (nearly) all 316 over the level's boxes: pick the cheaper column count x slots
+        int64_t padded = 0;
+        for (int o = 0; o < 8; o++) padded += (count[l * 8 + o] + BN - 1) / BN * BN;
+        grouped[l] = padded * 189 <= (nl + BN - 1) / BN * BN * 316 ? 1 : 0;
+        L.octbase[l] = co;
+        L.colbase[l] = cm;
+        mbase[l] = (int)cm;
+        for (int o = 0; o < 8; o++) {
+            const int k = l * 8 + o;
+            start[k] = s;
+            ogcol[k] = (int)co;
+            mgcol[k] = (int)cm;
+            s += count[k];
+            co += (count[k] + BN - 1) / BN * BN;
+            if (grouped[l]) cm += (count[k] + BN - 1) / BN * BN;
+        }
+        if (!grouped[l]) cm += (nl + BN - 1) / BN * BN;
     }
-    L.colbase[T.depth + 1] = c;
-    L.ncols = c;
-    int *d_start = ws.get<int>("lay_start", NK), *d_gcol = ws.get<int>("lay_gcol", NK);
-    PK_CUDA(cudaMemcpyAsync(d_start, start.data(), NK * sizeof(int), cudaMemcpyHostToDevice, st));
-    PK_CUDA(cudaMemcpyAsync(d_gcol, gcol.data(), NK * sizeof(int), cudaMemcpyHostToDevice, st));
-    const int64_t C = std::max<int64_t>(c, 1);
+    L.octbase[T.depth + 1] = co;
+    L.colbase[T.depth + 1] = cm;
+    L.noct = co;
+    L.ncols = cm;
+    int *d_small = ws.get<int>("lay_small", 4 * NK + 2 * (kMaxLevels + 1));
+    std::vector<int> small;
+    small.insert(small.end(), start.begin(), start.end());
+    small.insert(small.end(), ogcol.begin(), ogcol.end());
+    small.insert(small.end(), mgcol.begin(), mgcol.end());
+    small.insert(small.end(), mbase.begin(), mbase.end());
+    small.insert(small.end(), grouped.begin(), grouped.end());
+    PK_CUDA(cudaMemcpyAsync(d_small, small.data(), small.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    const int64_t C = std::max<int64_t>(cm, 1), CO = std::max<int64_t>(co, 1);
     L.col_of_box = ws.get<int>("col_of_box", nb);
     L.out_box = ws.get<int>("out_box", C);
     L.out_m2m = ws.get<int>("out_m2m", C);
-    L.l2l_src = ws.get<int>("l2l_src", C);
     L.m2m_src = ws.get<int>("m2m_src", 8 * C);
-    L.tile_oct = ws.get<int>("tile_oct", C / BN + 1);
     L.m2l_table = ws.get<int>("m2l_table", (size_t)kNumM2L * C);
+    L.out_oct = ws.get<int>("out_oct", CO);
+    L.l2l_src = ws.get<int>("l2l_src", CO);
+    L.tile_oct = ws.get<int>("tile_oct", CO / BN + 1);
     PK_CUDA(cudaMemsetAsync(L.out_box, 0xff, C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, C * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.l2l_src, 0xff, C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.m2l_table, 0xff, (size_t)kNumM2L * C * sizeof(int), st));
-    layout_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, skeys, svals, d_start, d_gcol, L.col_of_box,
-                                                            L.out_box, L.out_m2m, L.l2l_src, L.m2m_src, C, L.tile_oct);
+    PK_CUDA(cudaMemsetAsync(L.out_oct, 0xff, CO * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.l2l_src, 0xff, CO * sizeof(int), st));
+    layout_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(
+        tv, skeys, svals, d_small, d_small + NK, d_small + 2 * NK, d_small + 3 * NK, d_small + 3 * NK + kMaxLevels + 1,
+        L.col_of_box, L.out_box, L.out_m2m, L.m2m_src, C, L.out_oct, L.l2l_src, L.tile_oct);
     PK_CUDA(cudaGetLastError());
-    ctx.launches += 6;
+    ctx.launches += 7;
     return L;
 }
 
@@ -433,6 +477,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.src = Lay.m2m_src + c0;
                 a.ld_src = Lay.ncols;
                 a.A = ops.m2m;
+                a.nmat = 8;
                 a.X = Pup;
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M2M_o phi_child (src/fmm.cpp:547)
@@ -463,6 +508,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.src = Lay.m2l_table + c0;
                 a.ld_src = Lay.ncols;
                 a.A = ops.m2l;
+                a.nmat = kNumM2L;
                 a.X = Pup;
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573, 168-171)
@@ -470,15 +516,17 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 pm = prof.begin("m2l");
                 ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
                 prof.end(pm);
+                const int64_t o0 = Lay.octbase[l], o1 = Lay.octbase[l + 1];
                 GemmArgs b;
                 b.Kp = Kp;
-                b.ncols = (int)(c1 - c0);
-                b.out_box = Lay.out_box + c0;
+                b.ncols = (int)(o1 - o0);
+                b.out_box = Lay.out_oct + o0;
                 b.nslots = 1;
-                b.src = Lay.l2l_src + c0;
-                b.ld_src = Lay.ncols;
-                b.tile_mat = Lay.tile_oct + c0 / BN;
+                b.src = Lay.l2l_src + o0;
+                b.ld_src = Lay.noct;
+                b.tile_mat = Lay.tile_oct + o0 / BN;
                 b.A = ops.l2l;
+                b.nmat = 8;
                 b.X = Pdn;
                 b.Y = Q;
                 b.alpha = std::ldexp(1.0, l) * 0.5; // q += (2^l / 2) L2L_o phi_parent (src/fmm.cpp:590-591)

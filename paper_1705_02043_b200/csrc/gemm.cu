@@ -1,15 +1,30 @@
 // Gather-GEMM on DMMA (mma.sync.aligned.m8n8k4.row.col.f64 -> SASS DMMA.8x8x4).
 //
-// CTA tile BM x 64 (rows x box columns), BK = 16 deep k-chunks, cp.async multistage
-// pipeline. The reduction runs over (active slot, k-chunk); a slot is active for a
-// tile when any of its 64 columns has a source box, so octant-homogeneous M2L tiles
-// only stream the ~189 offsets that occur. Operand rows are padded to BK+4 doubles,
-// which makes the 8-row x 4-double fragment reads hit distinct bank groups.
-// Load balance: the slot range is split across CTAs when the tile grid is small
-// (split partials reduced in a fixed order -> deterministic results).
+// Work unit: a BM x 64 output tile (rows x box columns) over one contiguous chunk of
+// its reduction space (active slot, 16-deep k-chunk). A slot is active for a column
+// tile when any of its 64 columns has a source box (a prepass writes the per-tile
+// active-slot lists), so octant-homogeneous M2L tiles stream only their ~189 offsets.
+//
+// Default mainloop ("tma"): persistent CTAs (2 per SM) pull units from an atomic
+// counter. One producer warp streams each stage:
+//   A  BM x 16 operator tile   -> cp.async.bulk.tensor.2d (TMA), 128B swizzle
+//   B  64 x 16 gathered box rows -> cp.async 16 B (zero-fill for absent sources),
+//                                   tracked by cp.async.mbarrier.arrive.noinc
+// onto a "full" mbarrier; eight consumer warps run DMMA on 32x32 warp tiles and hand
+// the stage back through an "empty" mbarrier (4-stage ring). Units that split a tile's
+// reduction write partials reduced in a fixed order -> bitwise deterministic results.
+// Fallback mainloop ("cpasync", PKGPU_GEMM=cpasync): all threads stage with cp.async,
+// __syncthreads pipeline, one CTA per unit.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include <cudaTypedefs.h>
 
 #include "gemm.h"
+#include "gemm_tma.cuh"
 
 namespace pkgpu {
 
@@ -37,7 +52,18 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 struct KParams {
     GemmArgs a;
     int nsplit;
-    double *part; // [nsplit][ncols][Kp] when nsplit > 1
+    double *part;           // [nsplit][ncols][Kp] when nsplit > 1
+    const int *tile_slots;  // [coltiles][MAX_SLOTS] active slots per column tile
+    const int *tile_nact;   // [coltiles]
+    int rowtiles, coltiles; // unit = row + rowtiles * (col + coltiles * split)
+    int total_units;
+    int *counter;           // persistent scheduler
+    int l2hint;             // 1: operator tiles loaded with an L2 evict_last policy
+};
+
+struct TmaParams {
+    CUtensorMap tmA; // 2D view of the stacked operators: (Kp cols) x (nmat*Kp rows), 128B swizzle
+    KParams kp;
 };
 
 __device__ __forceinline__ int col_out(const GemmArgs &a, int c) {
@@ -48,47 +74,70 @@ __device__ __forceinline__ int col_src(const GemmArgs &a, int slot, int c) {
     if (a.src) return a.src[(int64_t)slot * a.ld_src + c];
     return col_out(a, c);
 }
+__device__ __forceinline__ int slot_matrix(const GemmArgs &a, int slot, int coltile) {
+    return a.tile_mat ? a.tile_mat[coltile] : (a.slot_mat ? a.slot_mat[slot] : slot);
+}
 
-// BM rows per CTA; warps arranged (BM/32) x 2, warp tile 32 x 32.
+// prepass: active slots per column tile, in slot order (one block per column tile)
+__global__ void slot_scan_kernel(GemmArgs a, int *tile_slots, int *tile_nact) {
+    __shared__ int flag[MAX_SLOTS];
+    const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < a.nslots; s += blockDim.x / 32) {
+        bool any = false;
+        for (int j = lane; j < BN; j += 32) any |= col_src(a, s, ct * BN + j) >= 0;
+        any = __any_sync(0xffffffffu, any);
+        if (lane == 0) flag[s] = any ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (int s = 0; s < a.nslots; s++)
+            if (flag[s]) tile_slots[ct * MAX_SLOTS + n++] = s;
+        tile_nact[ct] = n;
+    }
+}
+
+// epilogue of one accumulator element (row r, column c)
+__device__ __forceinline__ void store_out(const KParams &kp, int split, int r, int c, double v) {
+    const GemmArgs &a = kp.a;
+    if (kp.nsplit > 1) {
+        kp.part[((int64_t)split * a.ncols + c) * a.Kp + r] = v;
+        return;
+    }
+    const int ob = col_out(a, c);
+    if (ob < 0) return;
+    double *y = a.Y + (int64_t)ob * a.Kp + r;
+    if (a.rdiv) {
+        const double d = a.rdiv[r];
+        *y = d > a.rdiv_eps ? v / d : 0.0;
+    } else {
+        *y = (a.beta != 0.0 ? a.beta * *y : 0.0) + a.alpha * v;
+    }
+}
+
+__device__ __forceinline__ void unit_range(const KParams &kp, int nact, int split, int &it0, int &it1) {
+    const int64_t niter = (int64_t)nact * (kp.a.Kp / BK);
+    it0 = (int)(niter * split / kp.nsplit);
+    it1 = (int)(niter * (split + 1) / kp.nsplit);
+}
+
+// ---------------------------------------------------------------------------
+// cp.async mainloop: one CTA per unit; warps (BM/32) x 2, warp tile 32 x 32.
 template <int BM>
 __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams kp) {
     constexpr int WARPS_M = BM / 32;
     constexpr int NT = WARPS_M * 2 * 32;
     const GemmArgs &a = kp.a;
     extern __shared__ __align__(16) double smem[];
-    double *As = smem;                          // [STAGES][BM][PAD]
-    double *Bs = smem + STAGES * BM * PAD;      // [STAGES][BN][PAD]
-    __shared__ int s_slots[MAX_SLOTS];
-    __shared__ int s_flag[MAX_SLOTS];
-    __shared__ int s_nact;
-
+    double *As = smem;                     // [STAGES][BM][PAD]
+    double *Bs = smem + STAGES * BM * PAD; // [STAGES][BN][PAD]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int row0 = blockIdx.x * BM;
-    const int col0 = blockIdx.y * BN;
-    const int split = blockIdx.z;
-    const int s_begin = (int)((int64_t)a.nslots * split / kp.nsplit);
-    const int s_end = (int)((int64_t)a.nslots * (split + 1) / kp.nsplit);
-    const int ns = s_end - s_begin;
-
-    // active slots for this tile (deterministic order)
-    for (int s = warp; s < ns; s += NT / 32) {
-        const int slot = s_begin + s;
-        bool any = false;
-        for (int j = lane; j < BN; j += 32) any |= col_src(a, slot, col0 + j) >= 0;
-        any = __any_sync(0xffffffffu, any);
-        if (lane == 0) s_flag[s] = any ? 1 : 0;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int n = 0;
-        for (int s = 0; s < ns; s++)
-            if (s_flag[s]) s_slots[n++] = s_begin + s;
-        s_nact = n;
-    }
-    __syncthreads();
-    const int nact = s_nact;
+    const int rt = blockIdx.x, ct = blockIdx.y, split = blockIdx.z;
+    const int row0 = rt * BM, col0 = ct * BN;
+    const int *slots = kp.tile_slots + ct * MAX_SLOTS;
+    int it0, it1;
+    unit_range(kp, kp.tile_nact[ct], split, it0, it1);
     const int nk = a.Kp / BK;
-    const int niter = nact * nk;
 
     double acc[4][4][2];
 #pragma unroll
@@ -97,18 +146,15 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
         for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     auto load_stage = [&](int it, int stage) {
-        const int slot = s_slots[it / nk];
+        const int slot = slots[it / nk];
         const int k0 = (it % nk) * BK;
-        const int mat = a.tile_mat ? a.tile_mat[blockIdx.y] : (a.slot_mat ? a.slot_mat[slot] : slot);
-        const double *Am = a.A + (int64_t)mat * a.Kp * a.Kp;
+        const double *Am = a.A + (int64_t)slot_matrix(a, slot, ct) * a.Kp * a.Kp;
         double *as = As + stage * BM * PAD;
         double *bs = Bs + stage * BN * PAD;
-        // A: BM rows x 16 doubles = BM*8 chunks of 16 B
         for (int ch = tid; ch < BM * (BK / 2); ch += NT) {
             const int r = ch / (BK / 2), cc = ch % (BK / 2);
             cp_async16(as + r * PAD + cc * 2, Am + (int64_t)(row0 + r) * a.Kp + k0 + cc * 2, 16);
         }
-        // B: 64 gathered box vectors x 16 doubles
         for (int ch = tid; ch < BN * (BK / 2); ch += NT) {
             const int j = ch / (BK / 2), cc = ch % (BK / 2);
             const int sb = col_src(a, slot, col0 + j);
@@ -117,60 +163,182 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
         }
     };
 
+    const int n = it1 - it0;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; s++) {
-        if (s < niter) load_stage(s, s);
+        if (s < n) load_stage(it0 + s, s);
         cp_async_commit();
     }
     const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-    for (int it = 0; it < niter; it++) {
+    for (int i = 0; i < n; i++) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        const int nxt = it + STAGES - 1;
-        if (nxt < niter) load_stage(nxt, nxt % STAGES);
+        const int nxt = i + STAGES - 1;
+        if (nxt < n) load_stage(it0 + nxt, nxt % STAGES);
         cp_async_commit();
-        const double *as = As + (it % STAGES) * BM * PAD + (wm * 32 + (lane >> 2)) * PAD + (lane & 3);
-        const double *bs = Bs + (it % STAGES) * BN * PAD + (wn * 32 + (lane >> 2)) * PAD + (lane & 3);
+        const double *as = As + (i % STAGES) * BM * PAD + (wm * 32 + (lane >> 2)) * PAD + (lane & 3);
+        const double *bs = Bs + (i % STAGES) * BN * PAD + (wn * 32 + (lane >> 2)) * PAD + (lane & 3);
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double af[4], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; i++) af[i] = as[i * 8 * PAD + kk];
+            for (int m = 0; m < 4; m++) af[m] = as[m * 8 * PAD + kk];
 #pragma unroll
-            for (int j = 0; j < 4; j++) bf[j] = bs[j * 8 * PAD + kk];
+            for (int q = 0; q < 4; q++) bf[q] = bs[q * 8 * PAD + kk];
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+            for (int m = 0; m < 4; m++)
 #pragma unroll
-                for (int j = 0; j < 4; j++) dmma(acc[i][j], af[i], bf[j]);
+                for (int q = 0; q < 4; q++) dmma(acc[m][q], af[m], bf[q]);
         }
     }
     cp_async_wait<0>();
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+        const int r = row0 + wm * 32 + m * 8 + (lane >> 2);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                store_out(kp, split, r, col0 + wn * 32 + q * 8 + 2 * (lane & 3) + h, acc[m][q][h]);
+    }
+}
 
-    // epilogue: C fragment (row = lane/4, cols = 2*(lane%4) + {0,1})
+// ---------------------------------------------------------------------------
+// persistent TMA / mbarrier warp-specialised mainloop: 8 consumer warps + 1 producer.
+constexpr int TMA_BROW = 160; // bytes per gathered B row in shared memory (128 B data + pad)
+constexpr int NCW = 8;        // consumer warps
+
+template <int BM> constexpr int tma_stage_bytes() { return BM * BK * 8 + BN * TMA_BROW; }
+
+template <int BM, int NSTAGE>
+__global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
+    constexpr int WARPS_M = BM / 32;       // 4 or 2
+    constexpr int WARPS_N = NCW / WARPS_M; // 2 or 4
+    constexpr int WTN = BN / WARPS_N;      // 32 or 16
+    constexpr int NTL = WTN / 8;           // 4 or 2
+    constexpr int A_BYTES = BM * BK * 8;
+    constexpr int STAGE = tma_stage_bytes<BM>();
+    constexpr int RPL = BN / 4; // B rows per producer lane
+    static_assert(STAGE % 1024 == 0, "stage must keep 1024-byte alignment for the 128B swizzle");
+    const KParams &kp = tp.kp;
+    const GemmArgs &a = kp.a;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+    __shared__ int s_unit;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; s++) {
+            tma::mbar_init(&full[s], 33); // producer lane 0 expect_tx + 32 cp.async arrivals
+            tma::mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    const int nk = a.Kp / BK;
+    // consumer fragment addressing. A (128B-swizzled): element (r, k) at
+    // r*128 + (((k>>1) ^ (r&7)) << 4) + ((k&1) << 3); fragment rows have r&7 == lane>>2.
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int swz = lane >> 2;
+    int aoff[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int r = row0 + wm * 32 + i * 8 + (lane >> 2);
+    for (int kk = 0; kk < 4; kk++) aoff[kk] = (((2 * kk) + ((lane & 3) >> 1)) ^ swz) * 16 + (lane & 1) * 8;
+    const int arow = (wm * 32 + (lane >> 2)) * 128;
+    const int brow = (wn * WTN + (lane >> 2)) * TMA_BROW + (lane & 3) * 8;
+
+    const uint64_t policy = tma::policy_evict_last();
+    int g = 0; // pipeline iterations issued/consumed so far by this CTA (stage ring position)
+    for (;;) {
+        if (tid == 0) s_unit = atomicAdd(kp.counter, 1);
+        __syncthreads();
+        const int unit = s_unit;
+        __syncthreads();
+        if (unit >= kp.total_units) break;
+        const int rt = unit % kp.rowtiles;
+        const int rest = unit / kp.rowtiles;
+        const int ct = rest % kp.coltiles, split = rest / kp.coltiles;
+        const int row0 = rt * BM, col0 = ct * BN;
+        const int *slots = kp.tile_slots + ct * MAX_SLOTS;
+        int it0, it1;
+        unit_range(kp, kp.tile_nact[ct], split, it0, it1);
+        const int n = it1 - it0;
+        if (warp == NCW) {
+            // ---------------- producer ----------------
+            // this lane's B rows for the current slot, cached in registers (reloaded on
+            // slot change, every Kp/16 iterations): no dependent loads in the issue loop
+            int rowb[RPL];
+            int cur = -1, mat = 0;
+            for (int i = 0; i < n; i++) {
+                const int gi = g + i, st = gi % NSTAGE;
+                const int it = it0 + i;
+                const int si = it / nk, k0 = (it % nk) * BK;
+                if (si != cur) {
+                    cur = si;
+                    const int slot = slots[si];
+                    mat = slot_matrix(a, slot, ct);
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int c = col0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
-                const double v = acc[i][j][h];
-                if (kp.nsplit > 1) {
-                    kp.part[((int64_t)split * a.ncols + c) * a.Kp + r] = v;
-                    continue;
+                    for (int m = 0; m < RPL; m++) {
+                        rowb[m] = col_src(a, slot, col0 + (lane >> 3) + 4 * m);
+                    }
                 }
-                const int ob = col_out(a, c);
-                if (ob < 0) continue;
-                double *y = a.Y + (int64_t)ob * a.Kp + r;
-                if (a.rdiv) {
-                    const double d = a.rdiv[r];
-                    *y = d > a.rdiv_eps ? v / d : 0.0;
-                } else {
-                    *y = (a.beta != 0.0 ? a.beta * *y : 0.0) + a.alpha * v;
+                tma::mbar_wait(&empty[st], ((gi / NSTAGE) & 1) ^ 1);
+                unsigned char *as = smem + st * STAGE;
+                unsigned char *bs = as + A_BYTES;
+                if (lane == 0) {
+                    tma::mbar_expect_tx(&full[st], A_BYTES);
+                    if (kp.l2hint)
+                        tma::tma_load_2d_hint(as, &tp.tmA, k0, mat * a.Kp + row0, &full[st], policy);
+                    else
+                        tma::tma_load_2d(as, &tp.tmA, k0, mat * a.Kp + row0, &full[st]);
                 }
+#pragma unroll
+                for (int m = 0; m < RPL; m++) {
+                    const int j = (lane >> 3) + 4 * m;
+                    const double *src = rowb[m] >= 0 ? a.X + (int64_t)rowb[m] * a.Kp + k0 + 2 * (lane & 7) : a.X;
+                    tma::cp_async16(bs + j * TMA_BROW + 16 * (lane & 7), src, rowb[m] >= 0 ? 16 : 0);
+                }
+                tma::cp_async_mbar_arrive(&full[st]);
+            }
+        } else {
+            // ---------------- consumers ----------------
+            double acc[4][NTL][2];
+#pragma unroll
+            for (int m = 0; m < 4; m++)
+#pragma unroll
+                for (int q = 0; q < NTL; q++) acc[m][q][0] = acc[m][q][1] = 0.0;
+            for (int i = 0; i < n; i++) {
+                const int gi = g + i, st = gi % NSTAGE;
+                tma::mbar_wait(&full[st], (gi / NSTAGE) & 1);
+                const unsigned char *as = smem + st * STAGE + arow;
+                const unsigned char *bs = smem + st * STAGE + A_BYTES + brow;
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) {
+                    double af[4], bf[NTL];
+#pragma unroll
+                    for (int m = 0; m < 4; m++) af[m] = *reinterpret_cast<const double *>(as + m * 8 * 128 + aoff[kk]);
+#pragma unroll
+                    for (int q = 0; q < NTL; q++)
+                        bf[q] = *reinterpret_cast<const double *>(bs + q * 8 * TMA_BROW + kk * 32);
+#pragma unroll
+                    for (int m = 0; m < 4; m++)
+#pragma unroll
+                        for (int q = 0; q < NTL; q++) dmma(acc[m][q], af[m], bf[q]);
+                }
+                __syncwarp();
+                if (lane == 0) tma::mbar_arrive(&empty[st]);
+            }
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                const int r = row0 + wm * 32 + m * 8 + (lane >> 2);
+#pragma unroll
+                for (int q = 0; q < NTL; q++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        store_out(kp, split, r, col0 + wn * WTN + q * 8 + 2 * (lane & 3) + h, acc[m][q][h]);
             }
         }
+        g += n;
     }
 }
 
@@ -213,13 +381,51 @@ __global__ void gemv_kernel(const double *__restrict__ A, int rows, int cols, in
 
 template <int BM> size_t smem_bytes() { return (size_t)STAGES * (BM + BN) * PAD * sizeof(double); }
 
-template <int BM> void configure() {
-    static bool done = false;
-    if (!done) {
-        PK_CUDA(cudaFuncSetAttribute(gather_gemm_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_bytes<BM>()));
-        done = true;
+constexpr int TMA_STAGES = 4; // 4 x 26 KB (BM = 128): two CTAs per SM
+template <int BM> size_t tma_smem_bytes() { return (size_t)TMA_STAGES * tma_stage_bytes<BM>() + 1024; }
+
+template <class K> void set_smem(K kernel, size_t bytes) {
+    PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        PK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }
+    return fn;
+}
+
+// tensor map over the stacked operator array, cached per (pointer, nmat, Kp, BM)
+const CUtensorMap &operator_map(const double *A, int nmat, int Kp, int BM) {
+    static std::map<std::tuple<const double *, int, int, int>, CUtensorMap> cache;
+    const auto key = std::make_tuple(A, nmat, Kp, BM);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)nmat * Kp};
+    const cuuint64_t strides[1] = {(cuuint64_t)Kp * sizeof(double)};
+    const cuuint32_t box[2] = {BK, (cuuint32_t)BM};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(A), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return cache.emplace(key, m).first->second;
+}
+
+// mainloop selection: PKGPU_GEMM = tma (default) | cpasync
+bool use_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = std::getenv("PKGPU_GEMM");
+        v = (e && std::strcmp(e, "cpasync") == 0) ? 0 : 1;
+    }
+    return v == 1;
 }
 
 } // namespace
@@ -228,31 +434,75 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     if (a.ncols == 0 || a.nslots == 0) return 0;
     if (a.Kp % 64 != 0 || a.ncols % BN != 0 || a.nslots > MAX_SLOTS)
         throw RuntimeError("gather_gemm: bad shape");
+    const bool tma_path = use_tma();
     const int BMsel = (a.Kp % 128 == 0) ? 128 : 64;
     const int rowtiles = a.Kp / BMsel, coltiles = a.ncols / BN;
     const int64_t base = (int64_t)rowtiles * coltiles;
-    const int64_t target = (int64_t)num_sms * 2 * 4;
+    const int resident = num_sms * 2; // two CTAs per SM in both mainloops
+    // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
+    // still at least 16 iterations long
+    const int64_t iters = (int64_t)a.nslots * (a.Kp / BK);
+    const int64_t want = tma_path ? 8 * (int64_t)resident : 4 * (int64_t)resident;
     int nsplit = 1;
-    if (base < target && a.nslots >= 8) nsplit = (int)std::min<int64_t>((target + base - 1) / base, a.nslots / 4);
+    if (base < want) nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / 16), 64});
     nsplit = std::max(nsplit, 1);
-    KParams kp{a, nsplit, nullptr};
+    KParams kp{};
+    kp.a = a;
+    kp.nsplit = nsplit;
+    kp.rowtiles = rowtiles;
+    kp.coltiles = coltiles;
+    kp.total_units = (int)(base * nsplit);
     if (nsplit > 1) kp.part = ws.get<double>("gemm_part", (size_t)nsplit * a.ncols * a.Kp);
-    dim3 grid(rowtiles, coltiles, nsplit);
-    if (BMsel == 128) {
-        configure<128>();
-        gather_gemm_kernel<128><<<grid, 256, smem_bytes<128>(), st>>>(kp);
+    int *tslots = ws.get<int>("gemm_tile_slots", (size_t)coltiles * MAX_SLOTS);
+    int *tnact = ws.get<int>("gemm_tile_nact", coltiles);
+    slot_scan_kernel<<<coltiles, 256, 0, st>>>(a, tslots, tnact);
+    kp.tile_slots = tslots;
+    kp.tile_nact = tnact;
+    int launches = 1;
+    if (tma_path) {
+        kp.counter = ws.get<int>("gemm_counter", 1);
+        static int hint = -1;
+        if (hint < 0) {
+            const char *e = std::getenv("PKGPU_GEMM_HINT");
+            hint = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+        }
+        kp.l2hint = hint;
+        PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
+        TmaParams tp;
+        std::memset(&tp, 0, sizeof tp);
+        tp.kp = kp;
+        tp.tmA = operator_map(a.A, a.nmat > 0 ? a.nmat : 1, a.Kp, BMsel);
+        const unsigned grid = (unsigned)std::min<int64_t>(kp.total_units, resident);
+        if (BMsel == 128) {
+            static bool cfg = false;
+            if (!cfg) set_smem(gather_gemm_tma_kernel<128, TMA_STAGES>, tma_smem_bytes<128>()), cfg = true;
+            gather_gemm_tma_kernel<128, TMA_STAGES><<<grid, (NCW + 1) * 32, tma_smem_bytes<128>(), st>>>(tp);
+        } else {
+            static bool cfg = false;
+            if (!cfg) set_smem(gather_gemm_tma_kernel<64, TMA_STAGES>, tma_smem_bytes<64>()), cfg = true;
+            gather_gemm_tma_kernel<64, TMA_STAGES><<<grid, (NCW + 1) * 32, tma_smem_bytes<64>(), st>>>(tp);
+        }
     } else {
-        configure<64>();
-        gather_gemm_kernel<64><<<grid, 128, smem_bytes<64>(), st>>>(kp);
+        dim3 grid(rowtiles, coltiles, nsplit);
+        if (BMsel == 128) {
+            static bool cfg = false;
+            if (!cfg) set_smem(gather_gemm_kernel<128>, smem_bytes<128>()), cfg = true;
+            gather_gemm_kernel<128><<<grid, 256, smem_bytes<128>(), st>>>(kp);
+        } else {
+            static bool cfg = false;
+            if (!cfg) set_smem(gather_gemm_kernel<64>, smem_bytes<64>()), cfg = true;
+            gather_gemm_kernel<64><<<grid, 128, smem_bytes<64>(), st>>>(kp);
+        }
     }
     PK_CUDA(cudaGetLastError());
+    launches++;
     if (nsplit > 1) {
         const int64_t total = (int64_t)a.ncols * a.Kp;
         split_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, num_sms * 16), 256, 0, st>>>(kp);
         PK_CUDA(cudaGetLastError());
-        return 2;
+        launches++;
     }
-    return 1;
+    return launches;
 }
 
 void gemv(const double *A, int rows, int cols, int lda, const double *x, double *y, double alpha, double beta,

@@ -219,12 +219,8 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     T.src_perm = ws.get<int>("src_perm", std::max<int64_t>(ns, 1));
     T.trg_perm = ws.get<int>("trg_perm", std::max<int64_t>(nt, 1));
     int *flags = ws.get<int>("flags", 4);
-    int *h_flags = nullptr;
-    PK_CUDA(cudaMallocHost(&h_flags, 4 * sizeof(int)));
-    struct HostFree {
-        int *p;
-        ~HostFree() { cudaFreeHost(p); }
-    } hf{h_flags};
+    if (!T.h_flags) PK_CUDA(cudaMallocHost(&T.h_flags, 4 * sizeof(int)));
+    int *h_flags = T.h_flags;
 
     PK_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), st));
     // keys + sort, sources then targets (the "bad" counter accumulates both)

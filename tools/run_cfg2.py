@@ -1,0 +1,49 @@
+"""Profiling driver: device-resident cfg2 evaluates (Stokes TP, N=100k, p=8, leaf 50).
+
+    python tools/run_cfg2.py [--evals N] [--warm W]
+
+Used under ncu (launch lists, full captures); prints per-stage event times when not
+under a profiler."""
+import argparse
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import torch  # noqa: E402
+
+import paper_1705_02043_b200 as pk  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--evals", type=int, default=1)
+    ap.add_argument("--warm", type=int, default=0)
+    ap.add_argument("--n", type=int, default=100000)
+    ap.add_argument("--stats", action="store_true")
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    ctx = pk.Context(0)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    pts, f = pk.generate("uniform", a.n, 3, seed=12345)
+    op = pk.load_operator(os.path.join(REPO, "tests", "golden", "ops", "stokeslet_tp_ell2_p8_gated.pkm2l"))
+    d_pts = torch.from_numpy(pts).to(dev).reshape(-1).contiguous()
+    d_f = torch.from_numpy(f).to(dev)
+    out = torch.empty(3 * a.n, dtype=torch.float64, device=dev)
+    req = pk.EvalRequest(kernel=pk.KernelSpec.stokeslet(), sources=d_pts, strengths=d_f, targets=d_pts,
+                         setup=pk.PeriodicSetup.make(pk.Periodicity.tp), p=8, op=op, leaf_capacity=50)
+    for _ in range(a.warm):
+        pk.evaluate(req, context=ctx, out=out)
+    ctx.set_profiling(a.stats)
+    for _ in range(a.evals):
+        r = pk.evaluate(req, context=ctx, out=out)
+    torch.cuda.synchronize()
+    print("timings", r.timings, "launches", ctx.launches)
+    if a.stats:
+        for k, v in ctx.stage_stats().items():
+            print(k, v)
+
+
+if __name__ == "__main__":
+    main()
