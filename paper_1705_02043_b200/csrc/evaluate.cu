@@ -69,8 +69,8 @@ __global__ void layout_keys_kernel(TreeView T, int *keys, int *vals, int *hist) 
 __global__ void layout_fill_kernel(TreeView T, const int *__restrict__ skeys, const int *__restrict__ sboxes,
                                    const int *__restrict__ group_start, const int *__restrict__ oct_gcol,
                                    const int *__restrict__ m2l_gcol, const int *__restrict__ m2l_base,
-                                   const int *__restrict__ grouped, int *col_of_box, int *out_box, int *out_m2m,
-                                   int *m2m_src, int64_t ncols_m2l, int *out_oct, int *l2l_src, int *tile_oct) {
+                                   const int *__restrict__ grouped, int *col_of_box, int *out_box, int *out_oct,
+                                   int *l2l_src, int *tile_oct) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= T.nboxes) return;
     const int key = skeys[i], b = sboxes[i];
@@ -83,11 +83,29 @@ __global__ void layout_fill_kernel(TreeView T, const int *__restrict__ skeys, co
     const int col = grouped[lvl] ? m2l_gcol[key] + rank : m2l_base[lvl] + (int)(b - T.level_off[lvl]);
     col_of_box[b] = col;
     out_box[col] = b;
-    const bool leaf = T.isleaf[b] != 0;
-    out_m2m[col] = leaf ? -1 : b;
+}
+
+// M2M columns: internal boxes with sources only (src/fmm.cpp:536, 546), BFS order,
+// per level padded to 64
+__global__ void m2m_flags_kernel(TreeView T, int *flags, int *level_count) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const bool f = !T.isleaf[b] && T.srng[b].y > T.srng[b].x;
+    flags[b] = f ? 1 : 0;
+    if (f) atomicAdd(&level_count[T.cell[b].w], 1);
+}
+
+__global__ void m2m_fill_kernel(TreeView T, const int *__restrict__ list, int n, const int *__restrict__ list_start,
+                                const int *__restrict__ col_base, int64_t ncols, int *out, int *src) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int b = list[p];
+    const int l = T.cell[b].w;
+    const int col = col_base[l] + (p - list_start[l]);
+    out[col] = b;
     for (int o = 0; o < 8; o++) {
-        const int c = leaf ? -1 : T.child[8 * b + o];
-        m2m_src[(int64_t)o * ncols_m2l + col] = (c >= 0 && T.srng[c].y > T.srng[c].x) ? c : -1;
+        const int c = T.child[8 * b + o];
+        src[(int64_t)o * ncols + col] = (c >= 0 && T.srng[c].y > T.srng[c].x) ? c : -1;
     }
 }
 
@@ -189,17 +207,18 @@ __global__ void work_count_kernel(TreeView T, int n, const int64_t *__restrict__
 }
 
 struct Layout {
-    std::vector<int64_t> colbase, octbase; // per level (size depth + 2): m2l and oct layouts
-    int64_t ncols = 0, noct = 0;
+    std::vector<int64_t> colbase, octbase, m2mbase; // per level (size depth + 2): m2l, oct, m2m layouts
+    int64_t ncols = 0, noct = 0, nm2m = 0;
     int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
     int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
 };
 
 // Columns of the gather-GEMMs. Octant grouping makes every 64-column M2L tile share
 // one offset set (~189 of 316 slots active, no zero columns) at the price of padding
-// each octant group to 64; it pays once a level has >= 1024 boxes. Smaller levels keep
-// Morton order for M2L/M2M (one padded group). L2L always uses the octant layout so each
-// tile has a single L2L matrix.
+// each octant group to 64; a level uses it when that streams fewer (column x slot)
+// pairs than Morton order with (nearly) all 316 offsets active. L2L always uses the
+// octant layout so each tile has a single L2L matrix. M2M gets its own compact layout
+// of internal boxes with sources.
 Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
     Workspace &ws = ctx.ws;
     const int nb = (int)T.nboxes;
@@ -260,23 +279,58 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
     const int64_t C = std::max<int64_t>(cm, 1), CO = std::max<int64_t>(co, 1);
     L.col_of_box = ws.get<int>("col_of_box", nb);
     L.out_box = ws.get<int>("out_box", C);
-    L.out_m2m = ws.get<int>("out_m2m", C);
-    L.m2m_src = ws.get<int>("m2m_src", 8 * C);
     L.m2l_table = ws.get<int>("m2l_table", (size_t)kNumM2L * C);
     L.out_oct = ws.get<int>("out_oct", CO);
     L.l2l_src = ws.get<int>("l2l_src", CO);
     L.tile_oct = ws.get<int>("tile_oct", CO / BN + 1);
     PK_CUDA(cudaMemsetAsync(L.out_box, 0xff, C * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, C * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.m2l_table, 0xff, (size_t)kNumM2L * C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.out_oct, 0xff, CO * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.l2l_src, 0xff, CO * sizeof(int), st));
     layout_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(
         tv, skeys, svals, d_small, d_small + NK, d_small + 2 * NK, d_small + 3 * NK, d_small + 3 * NK + kMaxLevels + 1,
-        L.col_of_box, L.out_box, L.out_m2m, L.m2m_src, C, L.out_oct, L.l2l_src, L.tile_oct);
+        L.col_of_box, L.out_box, L.out_oct, L.l2l_src, L.tile_oct);
     PK_CUDA(cudaGetLastError());
-    ctx.launches += 7;
+    // ---- M2M layout: internal boxes with sources, compacted in BFS order ----
+    int *flags = ws.get<int>("m2m_flags", nb), *list = ws.get<int>("m2m_list", nb);
+    int *lcount = ws.get<int>("m2m_lcount", kMaxLevels + 1), *nsel = ws.get<int>("m2m_nsel", 1);
+    PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
+    m2m_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, flags, lcount);
+    size_t fb = 0;
+    cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st);
+    void *ftmp = ws.get<char>("m2m_sel_temp", fb);
+    PK_CUDA(cub::DeviceSelect::Flagged(ftmp, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st));
+    std::vector<int> lc(kMaxLevels + 1, 0);
+    PK_CUDA(cudaMemcpyAsync(lc.data(), lcount, lc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> lstart(kMaxLevels + 1, 0), cbase(kMaxLevels + 1, 0);
+    L.m2mbase.assign(T.depth + 2, 0);
+    int64_t cmm = 0;
+    int nint = 0;
+    for (int l = 0; l <= T.depth; l++) {
+        lstart[l] = nint;
+        cbase[l] = (int)cmm;
+        L.m2mbase[l] = cmm;
+        nint += lc[l];
+        cmm += (lc[l] + BN - 1) / BN * BN;
+    }
+    L.m2mbase[T.depth + 1] = cmm;
+    L.nm2m = cmm;
+    const int64_t CM = std::max<int64_t>(cmm, 1);
+    L.out_m2m = ws.get<int>("out_m2m", CM);
+    L.m2m_src = ws.get<int>("m2m_src", 8 * CM);
+    int *d_m2m_small = ws.get<int>("m2m_small", 2 * (kMaxLevels + 1));
+    std::vector<int> msmall(lstart);
+    msmall.insert(msmall.end(), cbase.begin(), cbase.end());
+    PK_CUDA(cudaMemcpyAsync(d_m2m_small, msmall.data(), msmall.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, CM * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * CM * sizeof(int), st));
+    if (nint > 0)
+        m2m_fill_kernel<<<blocks_for(nint, 256), 256, 0, st>>>(tv, list, nint, d_m2m_small, d_m2m_small + kMaxLevels + 1,
+                                                               CM, L.out_m2m, L.m2m_src);
+    PK_CUDA(cudaGetLastError());
+    ctx.launches += 11;
+    PK_CUDA(cudaStreamSynchronize(st)); // host vectors above are read by async copies
     return L;
 }
 
@@ -467,15 +521,15 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         prof.end(pm);
         for (int l = T.depth; l >= 0; l--) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
-            const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (l < T.depth) {
+            const int64_t c0 = Lay.m2mbase[l], c1 = Lay.m2mbase[l + 1];
+            if (c1 > c0) {
                 GemmArgs a;
                 a.Kp = Kp;
                 a.ncols = (int)(c1 - c0);
                 a.out_box = Lay.out_m2m + c0;
                 a.nslots = 8;
                 a.src = Lay.m2m_src + c0;
-                a.ld_src = Lay.ncols;
+                a.ld_src = Lay.nm2m;
                 a.A = ops.m2m;
                 a.nmat = 8;
                 a.X = Pup;

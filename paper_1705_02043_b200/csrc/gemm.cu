@@ -58,7 +58,6 @@ struct KParams {
     int rowtiles, coltiles; // unit = row + rowtiles * (col + coltiles * split)
     int total_units;
     int *counter;           // persistent scheduler
-    int l2hint;             // 1: operator tiles loaded with an L2 evict_last policy
 };
 
 struct TmaParams {
@@ -100,6 +99,7 @@ __global__ void slot_scan_kernel(GemmArgs a, int *tile_slots, int *tile_nact) {
 // epilogue of one accumulator element (row r, column c)
 __device__ __forceinline__ void store_out(const KParams &kp, int split, int r, int c, double v) {
     const GemmArgs &a = kp.a;
+    if (r >= a.Kp) return; // zero-filled operator rows of the last row tile
     if (kp.nsplit > 1) {
         kp.part[((int64_t)split * a.ncols + c) * a.Kp + r] = v;
         return;
@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
         double *bs = Bs + stage * BN * PAD;
         for (int ch = tid; ch < BM * (BK / 2); ch += NT) {
             const int r = ch / (BK / 2), cc = ch % (BK / 2);
-            cp_async16(as + r * PAD + cc * 2, Am + (int64_t)(row0 + r) * a.Kp + k0 + cc * 2, 16);
+            const bool in = row0 + r < a.Kp;
+            cp_async16(as + r * PAD + cc * 2, in ? Am + (int64_t)(row0 + r) * a.Kp + k0 + cc * 2 : Am, in ? 16 : 0);
         }
         for (int ch = tid; ch < BN * (BK / 2); ch += NT) {
             const int j = ch / (BK / 2), cc = ch % (BK / 2);
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
     __shared__ int s_unit;
+    __shared__ int s_rowsrc[BN]; // producer: source box of each B row for the current slot
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -247,7 +249,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
     const int arow = (wm * 32 + (lane >> 2)) * 128;
     const int brow = (wn * WTN + (lane >> 2)) * TMA_BROW + (lane & 3) * 8;
 
-    const uint64_t policy = tma::policy_evict_last();
     int g = 0; // pipeline iterations issued/consumed so far by this CTA (stage ring position)
     for (;;) {
         if (tid == 0) s_unit = atomicAdd(kp.counter, 1);
@@ -267,7 +268,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
             // ---------------- producer ----------------
             // this lane's B rows for the current slot, cached in registers (reloaded on
             // slot change, every Kp/16 iterations): no dependent loads in the issue loop
-            int rowb[RPL];
             int cur = -1, mat = 0;
             for (int i = 0; i < n; i++) {
                 const int gi = g + i, st = gi % NSTAGE;
@@ -277,26 +277,23 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
                     cur = si;
                     const int slot = slots[si];
                     mat = slot_matrix(a, slot, ct);
-#pragma unroll
-                    for (int m = 0; m < RPL; m++) {
-                        rowb[m] = col_src(a, slot, col0 + (lane >> 3) + 4 * m);
-                    }
+                    __syncwarp();
+                    for (int j = lane; j < BN; j += 32) s_rowsrc[j] = col_src(a, slot, col0 + j);
+                    __syncwarp();
                 }
                 tma::mbar_wait(&empty[st], ((gi / NSTAGE) & 1) ^ 1);
                 unsigned char *as = smem + st * STAGE;
                 unsigned char *bs = as + A_BYTES;
                 if (lane == 0) {
                     tma::mbar_expect_tx(&full[st], A_BYTES);
-                    if (kp.l2hint)
-                        tma::tma_load_2d_hint(as, &tp.tmA, k0, mat * a.Kp + row0, &full[st], policy);
-                    else
-                        tma::tma_load_2d(as, &tp.tmA, k0, mat * a.Kp + row0, &full[st]);
+                    tma::tma_load_3d(as, &tp.tmA, k0, row0, mat, &full[st]);
                 }
 #pragma unroll
                 for (int m = 0; m < RPL; m++) {
                     const int j = (lane >> 3) + 4 * m;
-                    const double *src = rowb[m] >= 0 ? a.X + (int64_t)rowb[m] * a.Kp + k0 + 2 * (lane & 7) : a.X;
-                    tma::cp_async16(bs + j * TMA_BROW + 16 * (lane & 7), src, rowb[m] >= 0 ? 16 : 0);
+                    const int rb = s_rowsrc[j];
+                    const double *src = rb >= 0 ? a.X + (int64_t)rb * a.Kp + k0 + 2 * (lane & 7) : a.X;
+                    tma::cp_async16(bs + j * TMA_BROW + 16 * (lane & 7), src, rb >= 0 ? 16 : 0);
                 }
                 tma::cp_async_mbar_arrive(&full[st]);
             }
@@ -407,11 +404,11 @@ const CUtensorMap &operator_map(const double *A, int nmat, int Kp, int BM) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     CUtensorMap m;
-    const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)nmat * Kp};
-    const cuuint64_t strides[1] = {(cuuint64_t)Kp * sizeof(double)};
-    const cuuint32_t box[2] = {BK, (cuuint32_t)BM};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(A), dims, strides, box,
+    const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)Kp, (cuuint64_t)nmat};
+    const cuuint64_t strides[2] = {(cuuint64_t)Kp * sizeof(double), (cuuint64_t)Kp * Kp * sizeof(double)};
+    const cuuint32_t box[3] = {BK, (cuuint32_t)BM, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(A), dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -435,8 +432,15 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     if (a.Kp % 64 != 0 || a.ncols % BN != 0 || a.nslots > MAX_SLOTS)
         throw RuntimeError("gather_gemm: bad shape");
     const bool tma_path = use_tma();
-    const int BMsel = (a.Kp % 128 == 0) ? 128 : 64;
-    const int rowtiles = a.Kp / BMsel, coltiles = a.ncols / BN;
+    // 128-row tiles for every K: the TMA zero-fills operator rows past Kp (3D tensor map,
+    // out-of-bounds) and the epilogue drops them. BM = 64 tiles only stream half the
+    // operator per stage and run the DMMA pipe at ~60% of the 128-row tiles' rate.
+    static const int bm_env = [] {
+        const char *e = std::getenv("PKGPU_GEMM_BM"); // 64: legacy half-height tiles (comparison runs)
+        return (e && std::strcmp(e, "64") == 0) ? 64 : 128;
+    }();
+    const int BMsel = bm_env;
+    const int rowtiles = (a.Kp + BMsel - 1) / BMsel, coltiles = a.ncols / BN;
     const int64_t base = (int64_t)rowtiles * coltiles;
     const int resident = num_sms * 2; // two CTAs per SM in both mainloops
     // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
@@ -461,12 +465,6 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     int launches = 1;
     if (tma_path) {
         kp.counter = ws.get<int>("gemm_counter", 1);
-        static int hint = -1;
-        if (hint < 0) {
-            const char *e = std::getenv("PKGPU_GEMM_HINT");
-            hint = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
-        }
-        kp.l2hint = hint;
         PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
         TmaParams tp;
         std::memset(&tp, 0, sizeof tp);
