@@ -110,6 +110,31 @@ pkgpu_status pkgpu_context_stage_stats(pkgpu_context *ctx, const char *stage, do
 pkgpu_status pkgpu_evaluate(pkgpu_context *ctx, const pkgpu_request *req, double *out, pkgpu_timings *timings,
                             pkgpu_compat *compat, char *err, size_t errlen);
 
+/* ---- multi-GPU: Morton-range partition ---------------------------- */
+/* Every rank receives the full request (inputs replicated, so the near-field source halo
+ * is implicit) and builds the same tree. Rank r owns a contiguous Morton range of leaves
+ * (its targets). It runs the upward pass over its own leaves only; because the upward
+ * chain is linear in the sources, the complete equivalent densities (root density
+ * included) are the SUM over ranks, exchanged with one allreduce. The downward pass and
+ * the leaf pass then run for the boxes intersecting the rank's range; the outputs
+ * (each target written by exactly one rank, zeros elsewhere) are summed by a second
+ * allreduce so every rank returns the full potentials.
+ *   alloc     : device memory the collective can operate on (e.g. a torch tensor)
+ *   allreduce : in-place elementwise sum over ranks of count doubles; the work stream
+ *               is synchronised before the call and must be safe to use after return. */
+typedef void *(*pkgpu_alloc_fn)(void *user, size_t bytes);
+typedef int (*pkgpu_allreduce_fn)(void *user, double *device_buf, int64_t count, void *stream);
+typedef struct {
+    int rank, nranks;
+    pkgpu_alloc_fn alloc;
+    pkgpu_allreduce_fn allreduce;
+    void *user;
+} pkgpu_partition;
+
+pkgpu_status pkgpu_evaluate_partitioned(pkgpu_context *ctx, const pkgpu_request *req, const pkgpu_partition *part,
+                                        double *out, pkgpu_timings *timings, pkgpu_compat *compat, char *err,
+                                        size_t errlen);
+
 /* ---- periodizing operator (include/pkifmm/periodize.hpp:22-33) -------------------- */
 /* load_operator (src/periodize.cpp:231-278): PKM2L magic, header, payload CRC-64/XZ. */
 pkgpu_status pkgpu_operator_load(const char *path, pkgpu_operator **op, char *err, size_t errlen);

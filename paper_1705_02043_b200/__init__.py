@@ -26,7 +26,8 @@ __all__ = [
     "KernelType", "KernelSpec", "Periodicity", "PeriodicSetup", "EvalMode", "EvalRequest", "EvalResult",
     "EvalTimings", "CompatReport", "PeriodizingOperator", "ConfigError", "CudaError", "Context", "FmmTree",
     "evaluate", "load_operator", "kernel_block_apply", "surface_points", "surface_point_count", "generate",
-    "set_kifmm_factors", "get_kifmm_factors", "kifmm_matrix", "crc64", "lib", "LIB_PATH",
+    "set_kifmm_factors", "get_kifmm_factors", "kifmm_matrix", "crc64", "lib", "LIB_PATH", "TorchDistComm",
+    "ThreadComm",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpkgpu.so")
@@ -54,6 +55,15 @@ class _Request(ctypes.Structure):
                 ("targets", ctypes.c_void_p), ("setup", _Setup), ("p", ctypes.c_int), ("op", ctypes.c_void_p),
                 ("mode", ctypes.c_int), ("leaf_capacity", ctypes.c_int), ("force", ctypes.c_int),
                 ("device_pointers", ctypes.c_int)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
+
+class _Partition(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("alloc", _ALLOC_FN),
+                ("allreduce", _ALLREDUCE_FN), ("user", ctypes.c_void_p)]
 
 
 class _Timings(ctypes.Structure):
@@ -85,6 +95,8 @@ _SIGNATURES = {
                                                  ctypes.POINTER(I64)]),
     "pkgpu_evaluate": (ctypes.c_int, [P, ctypes.POINTER(_Request), P, ctypes.POINTER(_Timings),
                                       ctypes.POINTER(_Compat), ERR, SZ]),
+    "pkgpu_evaluate_partitioned": (ctypes.c_int, [P, ctypes.POINTER(_Request), P, P, ctypes.POINTER(_Timings),
+                                                  ctypes.POINTER(_Compat), ERR, SZ]),
     "pkgpu_operator_load": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(P), ERR, SZ]),
     "pkgpu_operator_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_Setup), ctypes.c_int, P, I64,
                                              ctypes.POINTER(P), ERR, SZ]),
@@ -424,9 +436,13 @@ def _is_torch_cuda(x):
     return hasattr(x, "is_cuda") and getattr(x, "is_cuda")
 
 
-def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None) -> EvalResult:
+def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None, comm=None) -> EvalResult:
     """pkifmm::evaluate (src/fmm.cpp:690-742): near field over ell image layers + far
-    field through the periodizing operator, on the GPU."""
+    field through the periodizing operator, on the GPU.
+
+    comm: optional communicator (TorchDistComm / ThreadComm) -> Morton-range partitioned
+    evaluation across ranks (pkgpu_evaluate_partitioned); every rank passes the full
+    request and receives the full potentials."""
     ctx = context or default_context()
     k = request.kernel
     dev = _is_torch_cuda(request.sources)
@@ -461,10 +477,117 @@ def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None) 
         optr = out.ctypes.data
     r.n_sources, r.n_strengths, r.n_targets = ns, nq, nt
     tm, cp, err = _Timings(), _Compat(), _errbuf()
-    _check(lib().pkgpu_evaluate(ctx._h, ctypes.byref(r), ctypes.c_void_p(optr), ctypes.byref(tm),
-                                ctypes.byref(cp), err, 1024), err)
+    if comm is not None and comm.nranks > 1:
+        comm.begin_call()
+        part = _Partition(comm.rank, comm.nranks, comm.c_alloc, comm.c_allreduce, None)
+        try:
+            st = lib().pkgpu_evaluate_partitioned(ctx._h, ctypes.byref(r), ctypes.byref(part), ctypes.c_void_p(optr),
+                                                  ctypes.byref(tm), ctypes.byref(cp), err, 1024)
+        finally:
+            comm.end_call()
+        if comm.error is not None:
+            raise comm.error
+        _check(st, err)
+    else:
+        _check(lib().pkgpu_evaluate(ctx._h, ctypes.byref(r), ctypes.c_void_p(optr), ctypes.byref(tm),
+                                    ctypes.byref(cp), err, 1024), err)
     return EvalResult(out, EvalTimings(tm.tree, tm.near, tm.m2l_apply, tm.far),
                       CompatReport(bool(cp.ok), cp.violated.decode(), cp.residual))
+
+
+# ---------------------------------------------------------------------------
+# communicators for the partitioned path (pkgpu_evaluate_partitioned)
+
+class _CommBase:
+    """Supplies the two callbacks of pkgpu_partition: device allocation (torch tensors, so
+    the collective can run on them) and an in-place sum over ranks."""
+
+    def __init__(self, rank, nranks, device=0):
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self._bufs = {}
+        self.error = None
+        self.c_alloc = _ALLOC_FN(self._alloc)
+        self.c_allreduce = _ALLREDUCE_FN(self._allreduce)
+
+    def begin_call(self):
+        self._bufs.clear()
+        self.error = None
+
+    def end_call(self):
+        self._bufs.clear()
+
+    def _alloc(self, user, nbytes):
+        try:
+            import torch
+            dev = torch.device("cpu") if self.device == "cpu" else torch.device("cuda", self.device)
+            t = torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.float64, device=dev)
+            self._bufs[t.data_ptr()] = t
+            return t.data_ptr()
+        except Exception as e:  # never let an exception cross the C boundary
+            self.error = e
+            return None
+
+    def _allreduce(self, user, ptr, count, stream):
+        try:
+            self.allreduce(self._bufs[ptr][:count])
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+    def allreduce(self, t):
+        raise NotImplementedError
+
+
+class TorchDistComm(_CommBase):
+    """torch.distributed (NCCL over NVLink on the GPU box) communicator."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        super().__init__(rank, n, device if device is not None else int(os.environ.get("LOCAL_RANK", "0")))
+        self.group = group
+
+    def allreduce(self, t):
+        import torch
+        import torch.distributed as dist
+        dist.all_reduce(t, group=self.group)
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+
+
+class ThreadComm:
+    """In-process emulation of R ranks as host threads sharing one GPU (tests): the sum
+    runs between host barriers, no kernel ever waits on another rank's kernel."""
+
+    def __init__(self, nranks, device=0):
+        import threading
+        self.nranks, self.device = nranks, device
+        self.barrier = threading.Barrier(nranks)
+        self.slots = [None] * nranks
+        self.result = None
+
+    def rank(self, r):
+        outer = self
+
+        class _Rank(_CommBase):
+            def allreduce(self, t):
+                import torch
+                torch.cuda.synchronize()
+                outer.slots[r] = t
+                outer.barrier.wait()
+                if r == 0:
+                    acc = outer.slots[0].clone()
+                    for s in outer.slots[1:]:
+                        acc += s
+                    outer.result = acc
+                    torch.cuda.synchronize()
+                outer.barrier.wait()
+                t.copy_(outer.result)
+                torch.cuda.synchronize()
+                outer.barrier.wait()
+
+        return _Rank(r, self.nranks, self.device)
 
 
 # ---------------------------------------------------------------------------

@@ -320,6 +320,16 @@ pkgpu_status pkgpu_evaluate(pkgpu_context *ctx, const pkgpu_request *req, double
     });
 }
 
+pkgpu_status pkgpu_evaluate_partitioned(pkgpu_context *ctx, const pkgpu_request *req, const pkgpu_partition *part,
+                                        double *out, pkgpu_timings *timings, pkgpu_compat *compat, char *err,
+                                        size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        PK_CUDA(cudaSetDevice(ctx->device));
+        evaluate(*ctx, *req, out, timings, compat, part);
+    });
+}
+
 pkgpu_status pkgpu_operator_load(const char *path, pkgpu_operator **op, char *err, size_t errlen) {
     return guarded(err, errlen, [&] { *op = load_pkm2l(path); });
 }

@@ -60,7 +60,7 @@ struct pkgpu_tree {
 namespace pkgpu {
 
 void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_timings *timings,
-              pkgpu_compat *compat);
+              pkgpu_compat *compat, const pkgpu_partition *part = nullptr);
 
 void kernel_block_apply_device(pkgpu_context &ctx, int kernel, const double *targets, int64_t nt,
                                const double *sources, int64_t ns, const double *shift, const double *density,

@@ -86,13 +86,73 @@ __global__ void layout_fill_kernel(TreeView T, const int *__restrict__ skeys, co
 }
 
 // M2M columns: internal boxes with sources only (src/fmm.cpp:536, 546), BFS order,
-// per level padded to 64
-__global__ void m2m_flags_kernel(TreeView T, int *flags, int *level_count) {
+// per level padded to 64 (restricted to `mask` boxes in partitioned runs)
+__global__ void m2m_flags_kernel(TreeView T, const int *__restrict__ mask, int *flags, int *level_count) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= T.nboxes) return;
-    const bool f = !T.isleaf[b] && T.srng[b].y > T.srng[b].x;
+    const bool f = !T.isleaf[b] && T.srng[b].y > T.srng[b].x && (!mask || mask[b]);
     flags[b] = f ? 1 : 0;
     if (f) atomicAdd(&level_count[T.cell[b].w], 1);
+}
+
+// ---- Morton-range partition (pkgpu_evaluate_partitioned) ----
+// leaves -> full 36-bit Morton start key (DFS order once sorted)
+__global__ void leaf_key_kernel(TreeView T, const int *__restrict__ leaves, int nleaves, unsigned long long *keys,
+                                int *vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nleaves) return;
+    const int b = leaves[i];
+    keys[i] = T.prefix[b] << (3 * (kMaxDepth - T.cell[b].w));
+    vals[i] = b;
+}
+
+// box -> does its DFS leaf interval meet [lo, hi)?  own[b]: leaf owned by this rank
+__global__ void part_mask_kernel(TreeView T, const unsigned long long *__restrict__ lkeys, int nleaves, int lo, int hi,
+                                 int *in, int *own) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int sh = 3 * (kMaxDepth - T.cell[b].w);
+    const unsigned long long k0 = T.prefix[b] << sh, k1 = (T.prefix[b] + 1ull) << sh;
+    int a = 0, e = nleaves;
+    while (a < e) { // first leaf key >= k0
+        const int m = (a + e) >> 1;
+        if (lkeys[m] < k0)
+            a = m + 1;
+        else
+            e = m;
+    }
+    int c = a, f = nleaves;
+    while (c < f) { // first leaf key >= k1
+        const int m = (c + f) >> 1;
+        if (lkeys[m] < k1)
+            c = m + 1;
+        else
+            f = m;
+    }
+    in[b] = (a < hi && c > lo) ? 1 : 0;
+    own[b] = (T.isleaf[b] && a >= lo && a < hi) ? 1 : 0;
+}
+
+__global__ void flags_by_level_kernel(TreeView T, const int *__restrict__ mask, int *level_count) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    if (mask[b]) atomicAdd(&level_count[T.cell[b].w], 1);
+}
+
+__global__ void level_list_fill_kernel(TreeView T, const int *__restrict__ list, int n, const int *__restrict__ start,
+                                       const int *__restrict__ base, int *out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int b = list[p];
+    const int l = T.cell[b].w;
+    out[base[l] + (p - start[l])] = b;
+}
+
+__global__ void mask_oct_kernel(const int *__restrict__ mask, int64_t n, int *out_oct, int *l2l_src) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const int b = out_oct[c];
+    if (b >= 0 && !mask[b]) out_oct[c] = -1, l2l_src[c] = -1;
 }
 
 __global__ void m2m_fill_kernel(TreeView T, const int *__restrict__ list, int n, const int *__restrict__ list_start,
@@ -219,7 +279,7 @@ struct Layout {
 // pairs than Morton order with (nearly) all 316 offsets active. L2L always uses the
 // octant layout so each tile has a single L2L matrix. M2M gets its own compact layout
 // of internal boxes with sources.
-Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
+Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cudaStream_t st) {
     Workspace &ws = ctx.ws;
     const int nb = (int)T.nboxes;
     const TreeView tv = T.view();
@@ -295,7 +355,11 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
     int *flags = ws.get<int>("m2m_flags", nb), *list = ws.get<int>("m2m_list", nb);
     int *lcount = ws.get<int>("m2m_lcount", kMaxLevels + 1), *nsel = ws.get<int>("m2m_nsel", 1);
     PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
-    m2m_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, flags, lcount);
+    if (mask) {
+        mask_oct_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(mask, CO, L.out_oct, L.l2l_src);
+        ctx.launches += 1;
+    }
+    m2m_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, mask, flags, lcount);
     size_t fb = 0;
     cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st);
     void *ftmp = ws.get<char>("m2m_sel_temp", fb);
@@ -334,14 +398,97 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, cudaStream_t st) {
     return L;
 }
 
+// Morton-range partition of the leaves for rank r of R (pkgpu_evaluate_partitioned):
+// `in` marks boxes whose subtree meets the rank's leaves, `own` its leaves; `act`
+// lists the `in` boxes per level (padded to 64 with -1) for the pseudo-inverses, and
+// `leaves` the owned leaves for the leaf pass.
+struct Partition {
+    bool on = false;
+    int *in = nullptr, *own = nullptr;
+    int *act = nullptr;
+    std::vector<int64_t> actbase; // per level column base into act
+    int *leaves = nullptr;
+    int nleaves = 0;
+};
+
+void compact(pkgpu_context &ctx, const int *flags, int n, int *list, int *count_dev, const char *tag, cudaStream_t st) {
+    size_t fb = 0;
+    cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, list, count_dev, n, st);
+    void *tmp = ctx.ws.get<char>(std::string("cmp_") + tag, fb);
+    PK_CUDA(cub::DeviceSelect::Flagged(tmp, fb, cub::CountingInputIterator<int>(0), flags, list, count_dev, n, st));
+    ctx.launches += 2;
+}
+
+Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int nranks, cudaStream_t st) {
+    Workspace &ws = ctx.ws;
+    Partition P;
+    P.on = true;
+    const int nb = (int)T.nboxes, nl = (int)T.nleaves;
+    const TreeView tv = T.view();
+    // leaves in DFS (Morton) order; equal leaf counts per rank
+    unsigned long long *k_in = ws.get<unsigned long long>("pt_kin", nl), *k_out = ws.get<unsigned long long>("pt_kout", nl);
+    int *v_in = ws.get<int>("pt_vin", nl), *v_out = ws.get<int>("pt_vout", nl);
+    leaf_key_kernel<<<blocks_for(nl, 256), 256, 0, st>>>(tv, T.leaves, nl, k_in, v_in);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, nl, 0, 36, st);
+    void *tmp = ws.get<char>("pt_sort", tb);
+    PK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, v_out, nl, 0, 36, st));
+    const int lo = (int)((int64_t)nl * rank / nranks), hi = (int)((int64_t)nl * (rank + 1) / nranks);
+    P.in = ws.get<int>("pt_in", nb);
+    P.own = ws.get<int>("pt_own", nb);
+    part_mask_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, k_out, nl, lo, hi, P.in, P.own);
+    // owned leaves
+    P.leaves = ws.get<int>("pt_leaves", std::max(nl, 1));
+    int *cnt = ws.get<int>("pt_cnt", 2);
+    compact(ctx, P.own, nb, P.leaves, cnt, "own", st);
+    // per-level lists of boxes meeting the range
+    int *lcount = ws.get<int>("pt_lcount", kMaxLevels + 1), *list = ws.get<int>("pt_list", nb);
+    PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
+    flags_by_level_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, P.in, lcount);
+    compact(ctx, P.in, nb, list, cnt + 1, "in", st);
+    int h[2];
+    std::vector<int> lc(kMaxLevels + 1);
+    PK_CUDA(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaMemcpyAsync(lc.data(), lcount, lc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    P.nleaves = h[0];
+    std::vector<int> start(kMaxLevels + 1, 0), base(kMaxLevels + 1, 0);
+    P.actbase.assign(T.depth + 2, 0);
+    int s = 0;
+    int64_t c = 0;
+    for (int l = 0; l <= T.depth; l++) {
+        start[l] = s, base[l] = (int)c, P.actbase[l] = c;
+        s += lc[l];
+        c += (lc[l] + BN - 1) / BN * BN;
+    }
+    P.actbase[T.depth + 1] = c;
+    P.act = ws.get<int>("pt_act", std::max<int64_t>(c, 1));
+    PK_CUDA(cudaMemsetAsync(P.act, 0xff, std::max<int64_t>(c, 1) * sizeof(int), st));
+    int *d_sb = ws.get<int>("pt_sb", 2 * (kMaxLevels + 1));
+    std::vector<int> sb(start);
+    sb.insert(sb.end(), base.begin(), base.end());
+    PK_CUDA(cudaMemcpyAsync(d_sb, sb.data(), sb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (h[1] > 0)
+        level_list_fill_kernel<<<blocks_for(h[1], 256), 256, 0, st>>>(tv, list, h[1], d_sb, d_sb + kMaxLevels + 1,
+                                                                      P.act);
+    ctx.launches += 6;
+    PK_CUDA(cudaStreamSynchronize(st));
+    return P;
+}
+
 void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t hi, int level, double *Q, double *Tmp,
-                double *Phi, cudaStream_t st) {
-    if (hi <= lo) return;
+                double *Phi, cudaStream_t st, const Partition *P = nullptr) {
     GemmArgs a;
     a.Kp = ops.Kp;
-    a.nvalid = (int)(hi - lo);
-    a.box0 = (int)lo;
-    a.ncols = round_up(a.nvalid, BN);
+    if (P && P->on) { // only the boxes meeting this rank's leaves
+        a.out_box = P->act + P->actbase[level];
+        a.ncols = (int)(P->actbase[level + 1] - P->actbase[level]);
+    } else {
+        a.nvalid = (int)(hi - lo);
+        a.box0 = (int)lo;
+        a.ncols = round_up(a.nvalid, BN);
+    }
+    if (a.ncols <= 0) return;
     a.A = up ? ops.Ut_up : ops.Ut_dn;
     a.X = Q;
     a.Y = Tmp;
@@ -381,8 +528,15 @@ bool same_setup(const pkgpu_setup &a, const pkgpu_setup &b) {
 } // namespace
 
 void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_timings *timings,
-              pkgpu_compat *compat) {
+              pkgpu_compat *compat, const pkgpu_partition *part) {
     cudaStream_t st = ctx.stream;
+    const bool partitioned = part && part->nranks > 1;
+    if (partitioned) {
+        if (part->rank < 0 || part->rank >= part->nranks || !part->alloc || !part->allreduce)
+            throw InvalidArgument("evaluate_partitioned: bad partition descriptor");
+        if (req.mode == PKGPU_MODE_DIRECT)
+            throw InvalidArgument("evaluate_partitioned: direct mode is not partitioned");
+    }
     const int kernel = req.kernel;
     if (kernel != PKGPU_LAPLACE && kernel != PKGPU_STOKESLET) throw InvalidArgument("unknown kernel");
     const int ks = kernel == PKGPU_LAPLACE ? 1 : 3, kt = ks;
@@ -504,19 +658,27 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         const int64_t nb = T.nboxes;
         PairGeom g{kernel, req.p, ops.n, Kp, ops.d_tmpl};
         pm = prof.begin("lists");
-        Layout Lay = build_layout(ctx, T, st);
+        Partition Part;
+        if (partitioned) Part = build_partition(ctx, T, part->rank, part->nranks, st);
+        const Partition *PP = partitioned ? &Part : nullptr;
+        Layout Lay = build_layout(ctx, T, partitioned ? Part.in : nullptr, st);
         ListSetup ls{};
         if (periodic && ell >= 1)
             for (int a = 0; a < 3; a++) ls.periodic[a] = axes[a];
         build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
-                         &ctx.launches);
+                         &ctx.launches, partitioned ? Part.in : nullptr);
         prof.end(pm);
         double *Q = ws.get<double>("Q", nb * Kp), *Tm = ws.get<double>("Tmp", nb * Kp),
-               *Pup = ws.get<double>("phi_up", nb * Kp), *Pdn = ws.get<double>("phi_dn", nb * Kp);
+               *Pdn = ws.get<double>("phi_dn", nb * Kp);
+        // phi_up lives in collective-visible memory when partitioned (summed over ranks)
+        double *Pup = partitioned ? static_cast<double *>(part->alloc(part->user, nb * Kp * sizeof(double)))
+                                  : ws.get<double>("phi_up", nb * Kp);
+        if (!Pup) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+        if (partitioned) PK_CUDA(cudaMemsetAsync(Pup, 0, nb * Kp * sizeof(double), st));
         // ---- upward pass (src/fmm.cpp:532-553) ----
         PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));
         pm = prof.begin("s2m");
-        s2m_pass(g, T, Q, st);
+        s2m_pass(g, T, Q, st, partitioned ? Part.leaves : nullptr, partitioned ? Part.nleaves : 0);
         ctx.launches += 1;
         prof.end(pm);
         for (int l = T.depth; l >= 0; l--) {
@@ -541,7 +703,16 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_up");
-            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st);
+            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st, PP);
+            prof.end(pm);
+        }
+        if (partitioned) {
+            // the upward chain is linear in the sources: the complete equivalent densities
+            // (root included, feeding the periodizing step) are the sum over ranks
+            pm = prof.begin("comm");
+            PK_CUDA(cudaStreamSynchronize(st));
+            if (part->allreduce(part->user, Pup, nb * Kp, st) != 0)
+                throw RuntimeError("evaluate_partitioned: allreduce of equivalent densities failed");
             prof.end(pm);
         }
         // ---- downward pass (src/fmm.cpp:557-601) ----
@@ -590,7 +761,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_dn");
-            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st);
+            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st, PP);
             prof.end(pm);
         }
         PK_CUDA(cudaEventRecord(ctx.ev[2], st));
@@ -616,7 +787,21 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         PK_CUDA(cudaEventRecord(ctx.ev[3], st));
         // ---- leaf pass: L2T + W + U + far ----
         pm = prof.begin("leaf");
-        leaf_pass(g, T, ctx.lists, Pdn, Pup, far, d_out, st);
+        if (partitioned) {
+            // each target is written by exactly one rank; the sum over ranks is the result
+            double *pout = static_cast<double *>(part->alloc(part->user, std::max<int64_t>(kt * nt, 1) * sizeof(double)));
+            if (!pout) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+            PK_CUDA(cudaMemsetAsync(pout, 0, kt * nt * sizeof(double), st));
+            leaf_pass(g, T, ctx.lists, Pdn, Pup, far, pout, st, Part.leaves, Part.nleaves);
+            prof.end(pm);
+            pm = prof.begin("comm");
+            PK_CUDA(cudaStreamSynchronize(st));
+            if (part->allreduce(part->user, pout, kt * nt, st) != 0)
+                throw RuntimeError("evaluate_partitioned: allreduce of potentials failed");
+            if (nt) PK_CUDA(cudaMemcpyAsync(d_out, pout, kt * nt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        } else {
+            leaf_pass(g, T, ctx.lists, Pdn, Pup, far, d_out, st);
+        }
         ctx.launches += 1;
         prof.end(pm);
         PK_CUDA(cudaEventRecord(ctx.ev[4], st));

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <tuple>
 
 #include <cudaTypedefs.h>
@@ -400,6 +401,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // tensor map over the stacked operator array, cached per (pointer, nmat, Kp, BM)
 const CUtensorMap &operator_map(const double *A, int nmat, int Kp, int BM) {
     static std::map<std::tuple<const double *, int, int, int>, CUtensorMap> cache;
+    static std::mutex mtx; // contexts may run on several host threads
+    std::lock_guard<std::mutex> lock(mtx);
     const auto key = std::make_tuple(A, nmat, Kp, BM);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;

@@ -85,6 +85,7 @@ __device__ __forceinline__ bool wrap1(int n, int size, int per, int &w, int &s) 
 struct Params {
     int per[3];
     int eval_mode; // 1: skip boxes without targets and sources without sources (src/fmm.cpp:565-625)
+    const int *mask; // optional: boxes with mask[b] == 0 get empty lists
 };
 
 __device__ __forceinline__ bool has_src(const TreeView &T, int c) { return T.srng[c].y > T.srng[c].x; }
@@ -95,6 +96,7 @@ template <class Sink> __device__ void enumerate_box(const TreeView &T, const Par
     const int l = bc.w;
     const bool eval = P.eval_mode != 0;
     if (eval && T.trng[b].y == T.trng[b].x) return; // trg_subtree == 0
+    if (P.mask && !P.mask[b]) return;
     const bool leaf = T.isleaf[b] != 0;
     // ---------------- U and W (leaf targets) ----------------
     if (leaf) {
@@ -262,6 +264,7 @@ Params make_params(const ListSetup &S, int eval) {
     Params P{};
     for (int a = 0; a < 3; a++) P.per[a] = S.periodic[a];
     P.eval_mode = eval;
+    P.mask = nullptr;
     return P;
 }
 
@@ -296,10 +299,12 @@ void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cu
 }
 
 void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, int *m2l_table, int64_t ld,
-                      const int *col_of_box, const int *slot_of_code, cudaStream_t st, int64_t *launches) {
+                      const int *col_of_box, const int *slot_of_code, cudaStream_t st, int64_t *launches,
+                      const int *mask) {
     const int nb = (int)T.nboxes;
     const TreeView tv = T.view();
-    const Params P = make_params(S, 1);
+    Params P = make_params(S, 1);
+    P.mask = mask;
     Workspace &ws = L.ws;
     int64_t *cnt[4], *off[4];
     const char *names[4] = {"u", "v", "w", "x"};

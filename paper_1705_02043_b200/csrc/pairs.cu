@@ -437,24 +437,27 @@ __global__ void split_sum_kernel(const double *part, int nsplit, int len, double
 } // namespace
 
 void leaf_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, const double *phi_dn,
-               const double *phi_up, const double *phi_far, double *out, cudaStream_t st) {
-    if (T.nleaves == 0) return;
-    LeafParams P{T.view(), g.n,         g.Kp,       g.tmpl,   T.src_pos, T.src_f, T.trg_pos, T.trg_perm, T.leaves,
+               const double *phi_up, const double *phi_far, double *out, cudaStream_t st, const int *leaves,
+               int nleaves) {
+    if (!leaves) leaves = T.leaves, nleaves = (int)T.nleaves;
+    if (nleaves == 0) return;
+    LeafParams P{T.view(), g.n,         g.Kp,       g.tmpl,   T.src_pos, T.src_f, T.trg_pos, T.trg_perm, leaves,
                  L.u.off,  L.w.off,     L.u.ent,    L.w.ent,  phi_dn,    phi_up,  phi_far,   out};
     if (g.kernel == 0)
-        leaf_kernel<0><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+        leaf_kernel<0><<<(unsigned)nleaves, NT, 0, st>>>(P);
     else
-        leaf_kernel<1><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+        leaf_kernel<1><<<(unsigned)nleaves, NT, 0, st>>>(P);
     PK_CUDA(cudaGetLastError());
 }
 
-void s2m_pass(const PairGeom &g, const DeviceTree &T, double *q, cudaStream_t st) {
-    if (T.nleaves == 0) return;
-    CheckParams P{T.view(), g.n, g.Kp, g.tmpl, T.src_pos, T.src_f, T.leaves, nullptr, nullptr, q};
+void s2m_pass(const PairGeom &g, const DeviceTree &T, double *q, cudaStream_t st, const int *leaves, int nleaves) {
+    if (!leaves) leaves = T.leaves, nleaves = (int)T.nleaves;
+    if (nleaves == 0) return;
+    CheckParams P{T.view(), g.n, g.Kp, g.tmpl, T.src_pos, T.src_f, leaves, nullptr, nullptr, q};
     if (g.kernel == 0)
-        check_kernel<0, false><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+        check_kernel<0, false><<<(unsigned)nleaves, NT, 0, st>>>(P);
     else
-        check_kernel<1, false><<<(unsigned)T.nleaves, NT, 0, st>>>(P);
+        check_kernel<1, false><<<(unsigned)nleaves, NT, 0, st>>>(P);
     PK_CUDA(cudaGetLastError());
 }
 

@@ -15,10 +15,13 @@ struct PairGeom {
 // out[kt*orig(t)] = L2T(phi_dn[b]) + sum_W M2T(phi_up[c], shift) + sum_U P2P(c, shift)
 //                   + far(phi_far on the root 2.95 surface)
 void leaf_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, const double *phi_dn,
-               const double *phi_up, const double *phi_far, double *out, cudaStream_t st);
+               const double *phi_up, const double *phi_far, double *out, cudaStream_t st,
+               const int *leaves = nullptr, int nleaves = 0);
 
 // S2M at leaves (src/fmm.cpp:539-542): q[b] = K(outer check of b, sources of b) rho
-void s2m_pass(const PairGeom &g, const DeviceTree &T, double *q, cudaStream_t st);
+// `leaves`/`nleaves` restrict the pass to a leaf subset (partitioned runs); null: all leaves
+void s2m_pass(const PairGeom &g, const DeviceTree &T, double *q, cudaStream_t st, const int *leaves = nullptr,
+              int nleaves = 0);
 
 // X list / S2L (src/fmm.cpp:580-588): q[b] += K(inner check of b - shift, sources of c) rho
 void x_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, double *q, cudaStream_t st);

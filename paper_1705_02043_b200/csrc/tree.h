@@ -90,7 +90,9 @@ void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cu
 
 // Evaluate-path lists: U/W/X as CSR; V written straight into the M2L gather table
 // table[slot * ld + col(b)] = c (slot = M2L offset slot, col from col_of_box).
+// `mask` (optional): only boxes with mask[b] != 0 get lists (partitioned runs).
 void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, int *m2l_table, int64_t ld,
-                      const int *col_of_box, const int *slot_of_code, cudaStream_t stream, int64_t *launches);
+                      const int *col_of_box, const int *slot_of_code, cudaStream_t stream, int64_t *launches,
+                      const int *mask = nullptr);
 
 } // namespace pkgpu
