@@ -449,7 +449,11 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
     // still at least 16 iterations long
     const int64_t iters = (int64_t)a.nslots * (a.Kp / BK);
-    const int64_t want = tma_path ? 8 * (int64_t)resident : 4 * (int64_t)resident;
+    static const int64_t units_per_cta = [] {
+        const char *e = std::getenv("PKGPU_GEMM_UNITS"); // tuning knob: work units per resident CTA
+        return (int64_t)(e ? std::max(1, std::atoi(e)) : 32);
+    }();
+    const int64_t want = tma_path ? units_per_cta * resident : 4 * (int64_t)resident;
     int nsplit = 1;
     if (base < want) nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / 16), 64});
     nsplit = std::max(nsplit, 1);
