@@ -268,6 +268,7 @@ __global__ void work_count_kernel(TreeView T, int n, const int64_t *__restrict__
 
 struct Layout {
     std::vector<int64_t> colbase, octbase, m2mbase; // per level (size depth + 2): m2l, oct, m2m layouts
+    int wide[kMaxLevels + 1] = {0};                // m2l layout padded to 128-column tiles
     int64_t ncols = 0, noct = 0, nm2m = 0;
     int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
     int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
@@ -307,9 +308,18 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         const int64_t nl = T.level_off[l + 1] - T.level_off[l];
         // octant grouping streams ~189 offsets over padded groups; Morton order streams
         // (nearly) all 316 over the level's boxes: pick the cheaper column count x slots
-        int64_t padded = 0;
-        for (int o = 0; o < 8; o++) padded += (count[l * 8 + o] + BN - 1) / BN * BN;
+        int64_t padded = 0, padded128 = 0;
+        for (int o = 0; o < 8; o++) {
+            padded += (count[l * 8 + o] + BN - 1) / BN * BN;
+            padded128 += (count[l * 8 + o] + 127) / 128 * 128;
+        }
         grouped[l] = padded * 189 <= (nl + BN - 1) / BN * BN * 316 ? 1 : 0;
+        // 128-column M2L tiles (one 17-warp CTA per SM, half the operator traffic) are
+        // opt-in (PKGPU_GEMM_WIDE=1): measured slower than two 64-column CTAs per SM on
+        // cfg2/3/4 (49.3 vs 46.3 ms M2L at cfg2)
+        static const bool wide_ok = std::getenv("PKGPU_GEMM_WIDE") != nullptr;
+        L.wide[l] = wide_ok && grouped[l] && padded128 * 100 <= padded * 103 ? 1 : 0;
+        const int padm = L.wide[l] ? 128 : BN;
         L.octbase[l] = co;
         L.colbase[l] = cm;
         mbase[l] = (int)cm;
@@ -320,7 +330,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             mgcol[k] = (int)cm;
             s += count[k];
             co += (count[k] + BN - 1) / BN * BN;
-            if (grouped[l]) cm += (count[k] + BN - 1) / BN * BN;
+            if (grouped[l]) cm += (count[k] + padm - 1) / padm * padm;
         }
         if (!grouped[l]) cm += (nl + BN - 1) / BN * BN;
     }
@@ -734,6 +744,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.ld_src = Lay.ncols;
                 a.A = ops.m2l;
                 a.nmat = kNumM2L;
+                a.bn = Lay.wide[l] ? 128 : 64;
                 a.X = Pup;
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573, 168-171)

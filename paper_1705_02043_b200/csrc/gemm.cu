@@ -79,12 +79,12 @@ __device__ __forceinline__ int slot_matrix(const GemmArgs &a, int slot, int colt
 }
 
 // prepass: active slots per column tile, in slot order (one block per column tile)
-__global__ void slot_scan_kernel(GemmArgs a, int *tile_slots, int *tile_nact) {
+__global__ void slot_scan_kernel(GemmArgs a, int bn, int *tile_slots, int *tile_nact) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < a.nslots; s += blockDim.x / 32) {
         bool any = false;
-        for (int j = lane; j < BN; j += 32) any |= col_src(a, s, ct * BN + j) >= 0;
+        for (int j = lane; j < bn; j += 32) any |= col_src(a, s, ct * bn + j) >= 0;
         any = __any_sync(0xffffffffu, any);
         if (lane == 0) flag[s] = any ? 1 : 0;
     }
@@ -206,21 +206,27 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
 }
 
 // ---------------------------------------------------------------------------
-// persistent TMA / mbarrier warp-specialised mainloop: 8 consumer warps + 1 producer.
+// persistent TMA / mbarrier warp-specialised mainloop: NCW consumer warps + 1 producer.
+//   BNT =  64, NCW =  8: two CTAs per SM (4-stage ring each)
+//   BNT = 128, NCW = 16: one CTA per SM (6-stage ring), each operator tile feeds 128
+//                        columns -> half the operator traffic per FLOP (big M2L levels)
 constexpr int TMA_BROW = 160; // bytes per gathered B row in shared memory (128 B data + pad)
-constexpr int NCW = 8;        // consumer warps
 
-template <int BM> constexpr int tma_stage_bytes() { return BM * BK * 8 + BN * TMA_BROW; }
+template <int BM, int BNT> constexpr int tma_stage_bytes() { return BM * BK * 8 + BNT * TMA_BROW; }
 
-template <int BM, int NSTAGE>
-__global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
-    constexpr int WARPS_M = BM / 32;       // 4 or 2
+// register cap so the intended residency fits the 64K-register file; measured with
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor (PKGPU_GEMM_VERBOSE): 96 keeps 2 x 9-warp
+// CTAs (104 drops to 1) and is the most a 17-warp CTA can launch with
+template <int BM, int NSTAGE, int BNT, int NCW>
+__global__ void __maxnreg__(96)
+    gather_gemm_tma_kernel(const __grid_constant__ TmaParams tp) {
+    constexpr int WARPS_M = BM / 32;       // 4 (BM = 128)
     constexpr int WARPS_N = NCW / WARPS_M; // 2 or 4
-    constexpr int WTN = BN / WARPS_N;      // 32 or 16
-    constexpr int NTL = WTN / 8;           // 4 or 2
+    constexpr int WTN = BNT / WARPS_N;     // 32
+    constexpr int NTL = WTN / 8;           // 4
     constexpr int A_BYTES = BM * BK * 8;
-    constexpr int STAGE = tma_stage_bytes<BM>();
-    constexpr int RPL = BN / 4; // B rows per producer lane
+    constexpr int STAGE = tma_stage_bytes<BM, BNT>();
+    constexpr int RPL = BNT / 4; // B rows per producer lane
     static_assert(STAGE % 1024 == 0, "stage must keep 1024-byte alignment for the 128B swizzle");
     const KParams &kp = tp.kp;
     const GemmArgs &a = kp.a;
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
     __shared__ int s_unit;
-    __shared__ int s_rowsrc[BN]; // producer: source box of each B row for the current slot
+    __shared__ int s_rowsrc[BNT]; // producer: source box of each B row for the current slot
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
         const int rt = unit % kp.rowtiles;
         const int rest = unit / kp.rowtiles;
         const int ct = rest % kp.coltiles, split = rest / kp.coltiles;
-        const int row0 = rt * BM, col0 = ct * BN;
+        const int row0 = rt * BM, col0 = ct * BNT;
         const int *slots = kp.tile_slots + ct * MAX_SLOTS;
         int it0, it1;
         unit_range(kp, kp.tile_nact[ct], split, it0, it1);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 2) gather_gemm_tma_kernel(cons
                     const int slot = slots[si];
                     mat = slot_matrix(a, slot, ct);
                     __syncwarp();
-                    for (int j = lane; j < BN; j += 32) s_rowsrc[j] = col_src(a, slot, col0 + j);
+                    for (int j = lane; j < BNT; j += 32) s_rowsrc[j] = col_src(a, slot, col0 + j);
                     __syncwarp();
                 }
                 tma::mbar_wait(&empty[st], ((gi / NSTAGE) & 1) ^ 1);
@@ -379,8 +385,9 @@ __global__ void gemv_kernel(const double *__restrict__ A, int rows, int cols, in
 
 template <int BM> size_t smem_bytes() { return (size_t)STAGES * (BM + BN) * PAD * sizeof(double); }
 
-constexpr int TMA_STAGES = 4; // 4 x 26 KB (BM = 128): two CTAs per SM
-template <int BM> size_t tma_smem_bytes() { return (size_t)TMA_STAGES * tma_stage_bytes<BM>() + 1024; }
+// (BNT, stages): 64 -> 4 x 26 KB, two CTAs per SM; 128 -> 6 x 36 KB, one CTA per SM
+template <int BNT> constexpr int tma_stages() { return BNT == 64 ? 4 : 6; }
+template <int BNT> size_t tma_smem_bytes() { return (size_t)tma_stages<BNT>() * tma_stage_bytes<128, BNT>() + 1024; }
 
 template <class K> void set_smem(K kernel, size_t bytes) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -442,10 +449,12 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
         const char *e = std::getenv("PKGPU_GEMM_BM"); // 64: legacy half-height tiles (comparison runs)
         return (e && std::strcmp(e, "64") == 0) ? 64 : 128;
     }();
-    const int BMsel = bm_env;
-    const int rowtiles = (a.Kp + BMsel - 1) / BMsel, coltiles = a.ncols / BN;
+    const int BMsel = tma_path ? 128 : bm_env;
+    // 128-column tiles when the caller's column layout allows (big octant-grouped levels)
+    const int bnt = (tma_path && a.bn == 128 && a.ncols % 128 == 0) ? 128 : BN;
+    const int rowtiles = (a.Kp + BMsel - 1) / BMsel, coltiles = a.ncols / bnt;
     const int64_t base = (int64_t)rowtiles * coltiles;
-    const int resident = num_sms * 2; // two CTAs per SM in both mainloops
+    const int resident = num_sms * (bnt == 128 ? 1 : 2);
     // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
     // still at least 16 iterations long
     const int64_t iters = (int64_t)a.nslots * (a.Kp / BK);
@@ -466,7 +475,7 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     if (nsplit > 1) kp.part = ws.get<double>("gemm_part", (size_t)nsplit * a.ncols * a.Kp);
     int *tslots = ws.get<int>("gemm_tile_slots", (size_t)coltiles * MAX_SLOTS);
     int *tnact = ws.get<int>("gemm_tile_nact", coltiles);
-    slot_scan_kernel<<<coltiles, 256, 0, st>>>(a, tslots, tnact);
+    slot_scan_kernel<<<coltiles, 256, 0, st>>>(a, bnt, tslots, tnact);
     kp.tile_slots = tslots;
     kp.tile_nact = tnact;
     int launches = 1;
@@ -478,14 +487,28 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
         tp.kp = kp;
         tp.tmA = operator_map(a.A, a.nmat > 0 ? a.nmat : 1, a.Kp, BMsel);
         const unsigned grid = (unsigned)std::min<int64_t>(kp.total_units, resident);
-        if (BMsel == 128) {
+        // one-time residency check (PKGPU_GEMM_VERBOSE=1): CTAs per SM actually achievable
+        auto report = [](auto kernel, int threads, size_t bytes, const char *name) {
+            if (!std::getenv("PKGPU_GEMM_VERBOSE")) return;
+            int blocks = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, bytes);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kernel);
+            std::fprintf(stderr, "[pkgpu] %s: %d CTA/SM, %d regs, %zu B dynamic smem\n", name, blocks, fa.numRegs,
+                         bytes);
+        };
+        if (bnt == 128) {
+            constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<128>(), 128, 16>;
             static bool cfg = false;
-            if (!cfg) set_smem(gather_gemm_tma_kernel<128, TMA_STAGES>, tma_smem_bytes<128>()), cfg = true;
-            gather_gemm_tma_kernel<128, TMA_STAGES><<<grid, (NCW + 1) * 32, tma_smem_bytes<128>(), st>>>(tp);
+            if (!cfg) set_smem(k, tma_smem_bytes<128>()), report(k, 17 * 32, tma_smem_bytes<128>(), "tma<128,128>"),
+                cfg = true;
+            k<<<grid, 17 * 32, tma_smem_bytes<128>(), st>>>(tp);
         } else {
+            constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<64>(), 64, 8>;
             static bool cfg = false;
-            if (!cfg) set_smem(gather_gemm_tma_kernel<64, TMA_STAGES>, tma_smem_bytes<64>()), cfg = true;
-            gather_gemm_tma_kernel<64, TMA_STAGES><<<grid, (NCW + 1) * 32, tma_smem_bytes<64>(), st>>>(tp);
+            if (!cfg) set_smem(k, tma_smem_bytes<64>()), report(k, 9 * 32, tma_smem_bytes<64>(), "tma<128,64>"),
+                cfg = true;
+            k<<<grid, 9 * 32, tma_smem_bytes<64>(), st>>>(tp);
         }
     } else {
         dim3 grid(rowtiles, coltiles, nsplit);

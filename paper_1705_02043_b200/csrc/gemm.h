@@ -29,6 +29,7 @@ struct GemmArgs {
     const int *tile_mat = nullptr;   // [ncols / 64] matrix id per column tile (overrides slot_mat)
     const double *A = nullptr;       // matrices, Kp*Kp each
     int nmat = 1;                    // number of stacked matrices at A (TMA tensor map extent)
+    int bn = 64;                     // 128: columns come in homogeneous 128-blocks (wide tiles allowed)
     const double *X = nullptr;       // input vectors [box][Kp]
     double *Y = nullptr;             // output vectors [box][Kp]
     double alpha = 1.0, beta = 0.0;  // y = beta*y + alpha*acc
