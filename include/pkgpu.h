@@ -100,6 +100,14 @@ int64_t pkgpu_context_launch_count(pkgpu_context *ctx);
  * flops = algorithmic FLOPs (2K^2 per translation, 4K^2+K per pinv, 11 / 28
  * per Laplace / Stokes pair), launches = kernel launches. Accumulated until reset. */
 pkgpu_status pkgpu_context_set_profiling(pkgpu_context *ctx, int on);
+/* M2L arithmetic path. path 0: int8 tensor pipe (exact residue GEMMs, CRT rebuild in
+ * FP64) on levels with >= min_boxes boxes, DMMA FP64 elsewhere (default; min_boxes <= 0
+ * keeps the current threshold, 2048 unless PKGPU_M2L_I8_MIN says otherwise); path 1:
+ * DMMA FP64 everywhere. nmod / beta_a / beta_b > 0 override the residue parameters
+ * (moduli count 14..20, fixed-point bits of operators / densities, beta_a + beta_b +
+ * 20 < sum log2 m_t). */
+pkgpu_status pkgpu_context_set_m2l(pkgpu_context *ctx, int path, int64_t min_boxes, int nmod, int beta_a,
+                                   int beta_b);
 pkgpu_status pkgpu_context_reset_stats(pkgpu_context *ctx);
 pkgpu_status pkgpu_context_stage_stats(pkgpu_context *ctx, const char *stage, double *seconds, double *units,
                                        double *flops, int64_t *launches);
@@ -179,6 +187,18 @@ pkgpu_status pkgpu_kernel_block_apply(pkgpu_context *ctx, int kernel, const doub
                                       size_t errlen);
 /* surface_points (src/geometry.cpp:60-71), bit-exact. */
 pkgpu_status pkgpu_surface_points(int p, const double *center, double edge, double *out);
+
+/* The integer tensor-pipe gather-GEMM behind the M2L stage (no reference counterpart:
+ * the reference applies M2L as dense FP64 GEMMs, src/fmm.cpp:560-574). Device pointers:
+ *   R[t][c][r] += sum_s sum_k A[t][s][r][k] * B[t][row(s, c)][k]   (balanced residues mod m_t)
+ * A int8 [nmod][nmat][Ki][Ki], B int8 [nmod][rows_per_mod][Ki], src int32 [nslots][ld_src]
+ * (row = src - box0, or zero_row when src < 0), R int32 [nmod][ncols][Ki]; Ki % 128 == 0,
+ * ncols % 256 == 0. Exact integer results: the test hook for the kind::i8 kernel. */
+pkgpu_status pkgpu_i8_gather_gemm(pkgpu_context *ctx, const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
+                                  int zero_row, int Ki, int nmod, const int32_t *src, int64_t ld_src, int64_t box0,
+                                  int nslots, int ncols, int32_t *R, char *err, size_t errlen);
+/* The moduli m_t (pairwise coprime, <= 256); returns how many exist. */
+int pkgpu_i8_moduli(int32_t *out, int n);
 
 /* ---- tree / lists (debug exports for the bit-exact gates) ------------------------ */
 /* FmmTree::FmmTree (src/fmm.cpp:301-356) on the device. */

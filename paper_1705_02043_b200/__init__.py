@@ -90,6 +90,10 @@ _SIGNATURES = {
     "pkgpu_context_launch_count": (I64, [P]),
     "pkgpu_context_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
     "pkgpu_context_reset_stats": (ctypes.c_int, [P]),
+    "pkgpu_context_set_m2l": (ctypes.c_int, [P, ctypes.c_int, I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "pkgpu_i8_gather_gemm": (ctypes.c_int, [P, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, P, I64, I64, ctypes.c_int, ctypes.c_int, P, ERR, SZ]),
+    "pkgpu_i8_moduli": (ctypes.c_int, [P, ctypes.c_int]),
     "pkgpu_context_stage_stats": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                                  ctypes.POINTER(I64)]),
@@ -389,6 +393,14 @@ class Context:
     def set_profiling(self, on: bool):
         lib().pkgpu_context_set_profiling(self._h, 1 if on else 0)
 
+    def set_m2l(self, path="int8", min_boxes=0, nmod=0, beta_a=0, beta_b=0):
+        """M2L arithmetic: "int8" (exact residue GEMMs on the int8 tensor pipe for levels
+        with >= min_boxes boxes, FP64 DMMA elsewhere; the default) or "dmma" (FP64 DMMA
+        everywhere). nmod / beta_a / beta_b override the residue parameters."""
+        code = {"int8": 0, "dmma": 1}[path]
+        if lib().pkgpu_context_set_m2l(self._h, code, int(min_boxes), int(nmod), int(beta_a), int(beta_b)) != 0:
+            raise ValueError(f"set_m2l: invalid settings {path, min_boxes, nmod, beta_a, beta_b}")
+
     def reset_stats(self):
         lib().pkgpu_context_reset_stats(self._h)
 
@@ -608,6 +620,28 @@ def kernel_block_apply(kernel: KernelSpec, targets, sources, shift, density, out
     if o is not out:
         out[...] = o
     return out
+
+
+def i8_moduli():
+    """The pairwise-coprime moduli of the int8 M2L residue arithmetic."""
+    out = (ctypes.c_int32 * 32)()
+    n = lib().pkgpu_i8_moduli(out, 32)
+    return [int(out[i]) for i in range(n)]
+
+
+def i8_gather_gemm(A, B, rows_per_mod, zero_row, src, box0, R, context: Optional[Context] = None):
+    """The int8 tensor-pipe gather-GEMM (test hook; device tensors with .data_ptr()):
+    R[t][c][r] += sum_s sum_k A[t][s][r][k] B[t][row(s, c)][k] as balanced residues mod
+    m_t, row = src[s][c] - box0 (zero_row when src < 0). A int8 [nmod][nmat][Ki][Ki],
+    B int8 [nmod][rows_per_mod][Ki], src int32 [nslots][ncols], R int32 [nmod][ncols][Ki]."""
+    ctx = context or default_context()
+    nmod, nmat, Ki = A.shape[0], A.shape[1], A.shape[2]
+    nslots, ncols = src.shape
+    err = _errbuf()
+    _check(lib().pkgpu_i8_gather_gemm(ctx._h, ctypes.c_void_p(A.data_ptr()), nmat, ctypes.c_void_p(B.data_ptr()),
+                                      rows_per_mod, zero_row, Ki, nmod, ctypes.c_void_p(src.data_ptr()), ncols,
+                                      box0, nslots, ncols, ctypes.c_void_p(R.data_ptr()), err, 1024), err)
+    return R
 
 
 def surface_points(p, center, edge):

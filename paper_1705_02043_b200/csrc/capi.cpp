@@ -293,6 +293,25 @@ pkgpu_status pkgpu_context_set_profiling(pkgpu_context *ctx, int on) {
     return PKGPU_OK;
 }
 
+pkgpu_status pkgpu_context_set_m2l(pkgpu_context *ctx, int path, int64_t min_boxes, int nmod, int beta_a,
+                                   int beta_b) {
+    if (path < 0 || path > 1 || (nmod > 0 && (nmod < 14 || nmod > kI8MaxModuli))) return PKGPU_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lock(ctx->mtx);
+    I8Settings &s = ctx->i8;
+    s.enabled = path == 0;
+    if (min_boxes > 0) s.min_boxes = min_boxes;
+    if (nmod > 0) s.nmod = nmod;
+    if (beta_a > 0) s.beta_a = beta_a;
+    if (beta_b > 0) s.beta_b = beta_b;
+    double logm = 0;
+    for (int t = 0; t < s.nmod; t++) logm += std::log2((double)i8_moduli()[t]);
+    if (s.beta_a + s.beta_b + 20 >= logm) {
+        s = i8_settings();
+        return PKGPU_INVALID_ARGUMENT;
+    }
+    return PKGPU_OK;
+}
+
 pkgpu_status pkgpu_context_reset_stats(pkgpu_context *ctx) {
     std::lock_guard<std::mutex> lock(ctx->mtx);
     ctx->stats.clear();
@@ -438,6 +457,24 @@ pkgpu_status pkgpu_kernel_block_apply(pkgpu_context *ctx, int kernel, const doub
         PK_CUDA(cudaSetDevice(ctx->device));
         kernel_block_apply_device(*ctx, kernel, targets, nt, sources, ns, shift, density, out, skip_coincident);
     });
+}
+
+pkgpu_status pkgpu_i8_gather_gemm(pkgpu_context *ctx, const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
+                                  int zero_row, int Ki, int nmod, const int32_t *src, int64_t ld_src, int64_t box0,
+                                  int nslots, int ncols, int32_t *R, char *err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        PK_CUDA(cudaSetDevice(ctx->device));
+        ctx->launches += i8_gather_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots,
+                                        ncols, R, ctx->ws, ctx->stream);
+        PK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int pkgpu_i8_moduli(int32_t *out, int n) {
+    const int *m = i8_moduli();
+    for (int i = 0; i < n && i < kI8MaxModuli; i++) out[i] = m[i];
+    return kI8MaxModuli;
 }
 
 pkgpu_status pkgpu_surface_points(int p, const double *center, double edge, double *out) {

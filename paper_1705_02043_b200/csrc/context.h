@@ -45,6 +45,7 @@ struct pkgpu_context {
         int64_t launches = 0;
     };
     bool profiling = false;
+    pkgpu::I8Settings i8 = pkgpu::i8_settings(); // M2L arithmetic path (pkgpu_context_set_m2l)
     std::map<std::string, StageStat> stats;
     std::vector<cudaEvent_t> evpool;
 };

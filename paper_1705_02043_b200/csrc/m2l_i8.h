@@ -1,0 +1,67 @@
+// M2L on the integer tensor pipe: tcgen05.mma kind::i8 with TMEM accumulators.
+//
+// B200 has no FP64 tcgen05 kind; DMMA (mma.sync f64) tops out at ~37 TF/s while the
+// int8 pipe runs at ~4.5 POP/s. The M2L products (src/fmm.cpp:560-574) are therefore
+// computed EXACTLY in a residue number system:
+//   A_int = rint(M_o[r,k] 2^(beta_a - e_r))      per output row r, e_r from max_o,k |M_o[r,k]|
+//   X_int = rint(phi[b,k] 2^(beta_b - E_l))      per level l, E_l from max |phi| over the level
+//   S[r,c] = sum_slot sum_k A_int X_int           (|S| < 2^(beta_a + beta_b + 19))
+// S mod m_t for pairwise-coprime moduli m_t <= 256 is an int8 x int8 -> int32 GEMM per
+// modulus (balanced residues, |x| <= 128); the Chinese remainder theorem (Garner mixed
+// radix, Horner in FP64) rebuilds S from the residues and q += 2^l 2^(e_r + E - beta_a -
+// beta_b) S. The only approximation is the two fixed-point roundings (2^-beta of the
+// row / level maxima); with beta = 56 they sit below the FP64 rounding of the operands.
+#pragma once
+
+#include <cstdint>
+
+#include "common.h"
+
+namespace pkgpu {
+
+constexpr int kI8MaxModuli = 20;
+constexpr int kI8Tile = 256; // columns per tile: level column counts are padded to this
+
+struct I8Operators {          // residues of the stacked M2L operators (built once per KifmmOps)
+    int nmod = 0, beta_a = 0, Ki = 0, nmat = 0, K = 0;
+    int8_t *res = nullptr;    // [nmod][nmat][Ki][Ki], Ki = roundup(K, 128)
+    int *rowexp = nullptr;    // [Ki] e_r
+};
+
+struct I8Settings {
+    bool enabled = false;
+    int nmod = 17, beta_a = 56, beta_b = 56;
+    int64_t min_boxes = 2048; // levels with fewer boxes stay on the DMMA gather-GEMM
+};
+// PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes
+const I8Settings &i8_settings();
+
+void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat, int K, int Kp, int nmod,
+                        int beta_a, cudaStream_t st);
+
+struct I8LevelArgs {
+    int K = 0, Kp = 0;
+    int ncols = 0;               // multiple of kI8Tile
+    const int *out_box = nullptr; // [ncols] output box per column, -1 padding
+    int nslots = 0;
+    const int *src = nullptr;     // [nslots * ld_src] global source box ids, -1 none
+    int64_t ld_src = 0;
+    int64_t box0 = 0, nbox = 0;   // sources are the level's boxes [box0, box0 + nbox)
+    const double *X = nullptr;    // [box][Kp]
+    double *Y = nullptr;          // [box][Kp]: Y += alpha * sum_slot M X
+    double alpha = 1.0;
+};
+// Returns kernel launches.
+int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st);
+
+// The integer gather-GEMM alone (tests): for t < nmod, columns c < ncols, rows r < Ki
+//   R[t][c][r] += sum over slots s with a source of sum_k A[t][s][r][k] * B[t][row(s, c)][k]
+// reduced to balanced residues mod m_t per work unit, where row(s, c) = src - box0 for a
+// source, zero_row otherwise; B has rows_per_mod rows per modulus.
+int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
+                   const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
+                   cudaStream_t st);
+
+const int *i8_moduli(); // host copy, kI8MaxModuli entries
+
+} // namespace pkgpu

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.h"
+#include "m2l_i8.h"
 
 namespace pkgpu {
 
@@ -34,6 +35,7 @@ struct KifmmOps {
     int *slot_of_code = nullptr;            // device [343]
     std::vector<int> h_slot_of_code, h_code_of_slot;
     std::map<std::pair<int, int>, double *> img; // (axes mask, ell) -> M_img Kp x Kp
+    I8Operators i8;                         // M2L residues for the int8 tensor pipe (lazy)
     bool factors_ready = false, translations_ready = false;
 };
 
