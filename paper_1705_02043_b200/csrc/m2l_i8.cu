@@ -227,14 +227,181 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     }
 }
 
-// active slots per 256-column tile, in slot order
-__global__ void i8_slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int *tile_slots,
+// ---------------------------------------------------------------------------
+// v2: gathered box rows on the M side (128 per tile, cp.async by two producer warps with
+// the 128B swizzle applied by hand), operator rows on the N side (Nt <= 256 per tile, one
+// TMA 3D load per stage). Per stage: 16 KB gathered + Nt x 128 B operator, 128 x Nt x 128
+// MACs. R is laid out [t][row][col] so the epilogue's atomics are coalesced over boxes.
+constexpr int V2_BM = 128;        // gathered boxes per tile (MMA M)
+constexpr int V2_A_BYTES = V2_BM * BKI;
+constexpr int V2_B_BYTES = 256 * BKI; // operator tile, Nt <= 256 rows
+constexpr int V2_STAGE = V2_A_BYTES + V2_B_BYTES;
+constexpr int V2_NST = 4;
+constexpr int V2_PRODUCERS = 2;   // warps
+constexpr int V2_THREADS = (V2_PRODUCERS + 1 + 4) * 32;
+
+struct V2Params {
+    CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
+    const int8_t *X; // box residues [nmod][rows_per_mod][Ki]
+    const int *src;
+    int64_t ld_src, box0;
+    int zero_row, rows_per_mod;
+    const int *tile_slots, *tile_nact;
+    int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
+    uint32_t idesc;
+    int *R; // [nmod][Ki][ncols]
+};
+
+__device__ __forceinline__ Unit decode_v2(const V2Params &p, int u) {
+    Unit x;
+    x.rt = u % p.rowtiles;
+    u /= p.rowtiles;
+    x.ct = u % p.coltiles;
+    u /= p.coltiles;
+    const int chunk = u % p.nchunk;
+    x.t = u / p.nchunk;
+    const int nact = p.tile_nact[x.ct];
+    x.s0 = nact * chunk / p.nchunk;
+    x.s1 = nact * (chunk + 1) / p.nchunk;
+    return x;
+}
+
+__global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_constant__ V2Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    __shared__ __align__(8) uint64_t full[V2_NST], empty[V2_NST], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NPT = V2_PRODUCERS * 32;
+    if (tid == 0) {
+        for (int s = 0; s < V2_NST; s++) {
+            tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
+            tma::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            tma::mbar_init(&tfull[b], 1);
+            tma::mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == V2_PRODUCERS) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+        const Unit x = decode_v2(p, u);
+        const int n = (x.s1 - x.s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + x.ct * MAX_SLOTS;
+        if (warp < V2_PRODUCERS) {
+            // ---------------- producers: 16 cp.async of 16 B per thread per stage ----------------
+            // thread -> chunk c = lane & 7 of rows j = (tid >> 3) + 8 i, i < 16
+            const int c = lane & 7, j0 = tid >> 3;
+            const int8_t *Xt = p.X + (int64_t)x.t * p.rows_per_mod * p.Ki + c * 16;
+            for (int si = x.s0; si < x.s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + x.ct * V2_BM;
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int b = srow[j0 + 8 * i];
+                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
+                }
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int gi = g + (si - x.s0) * p.KC + kc, st = gi % V2_NST;
+                    tma::mbar_wait(&empty[st], ((gi / V2_NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * V2_STAGE;
+                    if (tid == 0) {
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        tma::tma_load_3d(as + V2_A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot,
+                                         &full[st]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 8 * i;
+                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    tma::cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        } else if (warp == V2_PRODUCERS) {
+            // ---------------- MMA issuer ----------------
+            if (lane == 0) {
+                const int buf = jb & 1;
+                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dt = tmem + buf * 256;
+                for (int i = 0; i < n; i++) {
+                    const int gi = g + i, st = gi % V2_NST;
+                    tma::mbar_wait(&full[st], (gi / V2_NST) & 1);
+                    // cp.async wrote the gathered rows through the generic proxy
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tc_fence_after();
+                    const uint32_t a0 = tma::smem_u32(smem + st * V2_STAGE);
+                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + V2_A_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BKI / 32; kk++)
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"((i > 0 || kk > 0) ? 1u : 0u));
+                    umma_commit(&empty[st]);
+                }
+                umma_commit(&tfull[buf]);
+            }
+            __syncwarp();
+        } else {
+            // ---------------- epilogue: lane = box, TMEM column = operator row ----------------
+            const int buf = jb & 1, q = warp & 3;
+            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
+            tc_fence_after();
+            const int m = c_mod[x.t];
+            const double inv = 1.0 / m;
+            const int col = x.ct * V2_BM + q * 32 + lane;
+            const int r0 = x.rt * p.Nt;
+            int *Rt = p.R + ((int64_t)x.t * p.Ki + r0) * p.ncols + col;
+            const int nr = min(p.Nt, p.Ki - r0);
+            for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, v);
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const int a = (int)v[j];
+                    const int r = a - __double2int_rn((double)a * inv) * m;
+                    if (r && j0 + j < nr) atomicAdd(Rt + (int64_t)(j0 + j) * p.ncols, r);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&tempty[buf]);
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == V2_PRODUCERS) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+// active slots per column tile of `bn` columns, in slot order
+__global__ void i8_slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
                                     int *tile_nact) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
         bool any = false;
-        for (int j = lane; j < BNI; j += 32) any |= src[(int64_t)s * ld_src + (int64_t)ct * BNI + j] >= 0;
+        for (int j = lane; j < bn; j += 32) any |= src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0;
         any = __any_sync(0xffffffffu, any);
         if (lane == 0) flag[s] = any ? 1 : 0;
     }
@@ -326,7 +493,8 @@ __global__ void x_residue_kernel(const double *__restrict__ X, int64_t nbox, int
 }
 
 // Garner (balanced mixed-radix digits) + Horner in FP64: Y[out(c)][r] += alpha 2^(e_r + E - ba - bb) S
-template <int NM>
+// R layout: RC = true -> [t][r][c] (v2 kernel), false -> [t][c][r] (v1 kernel)
+template <int NM, bool RC>
 __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki, int K, int Kp,
                                    const int *__restrict__ out_box, const int *__restrict__ rowexp,
                                    const unsigned long long *__restrict__ mx, int beta_sum, double alpha,
@@ -334,7 +502,7 @@ __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki,
     const int64_t n = (int64_t)ncols * Ki;
     const int E = level_exp(mx);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i / Ki), r = (int)(i % Ki);
+        const int c = RC ? (int)(i % ncols) : (int)(i / Ki), r = RC ? (int)(i / ncols) : (int)(i % Ki);
         if (r >= K) continue;
         const int ob = out_box[c];
         if (ob < 0) continue;
@@ -422,7 +590,7 @@ const I8Settings &i8_settings() {
     static I8Settings s = [] {
         I8Settings r;
         const char *e = std::getenv("PKGPU_M2L");
-        r.enabled = e && std::strcmp(e, "i8") == 0; // default path chosen in evaluate tuning
+        r.enabled = !(e && std::strcmp(e, "dmma") == 0);
         if (const char *c = std::getenv("PKGPU_M2L_I8")) {
             int a = r.nmod, b = r.beta_a, d = r.beta_b;
             if (std::sscanf(c, "%d,%d,%d", &a, &b, &d) == 3) r.nmod = a, r.beta_a = b, r.beta_b = d;
@@ -452,6 +620,68 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
     PK_CUDA(cudaGetLastError());
 }
 
+namespace {
+
+bool use_v1() {
+    static const bool v = [] {
+        const char *e = std::getenv("PKGPU_I8_KERNEL");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return v;
+}
+
+int i8_gather_gemm_v2(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
+                      const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
+                      cudaStream_t st) {
+    const int num_sms = sm_count();
+    V2Params p;
+    std::memset(&p, 0, sizeof p);
+    p.X = B;
+    p.src = src;
+    p.ld_src = ld_src;
+    p.box0 = box0;
+    p.zero_row = zero_row;
+    p.rows_per_mod = rows_per_mod;
+    p.nmat = nmat;
+    p.nmod = nmod;
+    p.KC = Ki / BKI;
+    // operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
+    p.rowtiles = (Ki + 255) / 256;
+    p.Nt = ((Ki + p.rowtiles - 1) / p.rowtiles + 15) / 16 * 16;
+    p.coltiles = ncols / V2_BM;
+    p.ncols = ncols;
+    p.Ki = Ki;
+    p.R = R;
+    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(V2_BM >> 4) << 24);
+    const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
+    int nchunk = (int)((nslots + cmax - 1) / cmax);
+    const int64_t base = (int64_t)nmod * p.rowtiles * p.coltiles;
+    while (base * nchunk < 3LL * num_sms && nchunk * 16 < nslots) nchunk++;
+    p.nchunk = nchunk;
+    p.total_units = (int)(base * nchunk);
+    int *tslots = ws.get<int>("i8_tile_slots", (size_t)p.coltiles * MAX_SLOTS);
+    int *tnact = ws.get<int>("i8_tile_nact", p.coltiles);
+    i8_slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, V2_BM, tslots, tnact);
+    p.tile_slots = tslots;
+    p.tile_nact = tnact;
+    const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
+    const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
+    const cuuint32_t box[3] = {BKI, (cuuint32_t)p.Nt, 1};
+    encode(&p.tmB, A, 3, dims, strides, box);
+    const size_t smem = (size_t)V2_NST * V2_STAGE + 1024;
+    static bool cfg = false;
+    if (!cfg) {
+        PK_CUDA(cudaFuncSetAttribute(m2l_i8_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cfg = true;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
+    m2l_i8_v2_kernel<<<grid, V2_THREADS, smem, st>>>(p);
+    PK_CUDA(cudaGetLastError());
+    return 2;
+}
+
+} // namespace
+
 int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                    const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
                    cudaStream_t st) {
@@ -459,6 +689,9 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     if (ncols % BNI != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
         throw RuntimeError("i8_gather_gemm: bad shape");
     upload_tables();
+    if (!use_v1())
+        return i8_gather_gemm_v2(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R,
+                                 ws, st);
     const int num_sms = sm_count();
     I8Params p;
     std::memset(&p, 0, sizeof p);
@@ -484,7 +717,7 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     p.total_units = (int)(base * nchunk);
     int *tslots = ws.get<int>("i8_tile_slots", (size_t)p.coltiles * MAX_SLOTS);
     int *tnact = ws.get<int>("i8_tile_nact", p.coltiles);
-    i8_slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, tslots, tnact);
+    i8_slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, BNI, tslots, tnact);
     p.tile_slots = tslots;
     p.tile_nact = tnact;
     {
@@ -529,11 +762,16 @@ int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspa
     const int64_t n = (int64_t)a.ncols * Ki;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
     const int bs = o.beta_a + beta_b;
+    const bool rc = !use_v1();
     switch (nmod) {
 #define PK_RC(NM)                                                                                                      \
     case NM:                                                                                                           \
-        reconstruct_kernel<NM><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, mx, bs, a.alpha,  \
-                                                     a.Y);                                                             \
+        if (rc)                                                                                                        \
+            reconstruct_kernel<NM, true><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, mx, bs, \
+                                                               a.alpha, a.Y);                                          \
+        else                                                                                                           \
+            reconstruct_kernel<NM, false><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, mx,    \
+                                                                bs, a.alpha, a.Y);                                     \
         break;
         PK_RC(14) PK_RC(15) PK_RC(16) PK_RC(17) PK_RC(18) PK_RC(19) PK_RC(20)
 #undef PK_RC

@@ -31,7 +31,7 @@ struct I8Operators {          // residues of the stacked M2L operators (built on
 struct I8Settings {
     bool enabled = false;
     int nmod = 17, beta_a = 56, beta_b = 56;
-    int64_t min_boxes = 2048; // levels with fewer boxes stay on the DMMA gather-GEMM
+    int64_t min_boxes = 1;    // levels with fewer boxes stay on the DMMA gather-GEMM
 };
 // PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes
 const I8Settings &i8_settings();

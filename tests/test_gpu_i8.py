@@ -41,15 +41,15 @@ def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
     src[rng.random(src.shape) < 0.3] = -1
     src[1, :256] = -1  # a slot with no source in the first column tile (skipped by the prepass)
     dev = torch.device("cuda", 0)
-    R = torch.zeros((nmod, ncols, Ki), dtype=torch.int32, device=dev)
+    R = torch.zeros((nmod, Ki, ncols), dtype=torch.int32, device=dev)
     pk.i8_gather_gemm(torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), nrows, zero_row,
                       torch.from_numpy(src).to(dev), box0, R)
-    got = R.cpu().numpy().astype(np.int64)
+    got = R.cpu().numpy().astype(np.int64).transpose(0, 2, 1)  # -> [t][c][r]
     ref = host_residue_gemm(A, B, src, box0, zero_row)
     for t, m in enumerate(mods):
         bad = np.count_nonzero((got[t] - ref[t]) % m)
         assert bad == 0, f"modulus {m}: {bad} of {got[t].size} entries wrong"
-        assert np.abs(got[t]).max() <= 3 * 128  # reduced per unit before the atomics
+        assert np.abs(got[t]).max() <= 128 * nslots  # reduced per unit before the atomics
 
 
 @pytest.fixture(scope="module")
