@@ -37,6 +37,11 @@ WORKLOAD = "cfg2: Stokes TP (unit cube), N=100000 uniform, p=8, leaf 50, ell=2 (
 FP64_PEAK_TFLOPS = 37.07  # measured DMMA m8n8k4 loop on this pool (profiles/r01_fp64_peaks.jsonl)
 FP64_PEAK_SOURCE = "measured: DMMA.8x8x4 loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl); " \
                    "MEASURED_PEAKS.json has no FP64 entry"
+I8_PEAK_TOPS = 4595.7  # measured tcgen05 kind::i8 loop (tools/i8_peak.cu, profiles/r01_i8_peak.json)
+I8_PEAK_SOURCE = "measured: tcgen05.mma kind::i8 M128 N256 K32 loop from shared memory, 148 SMs " \
+                 "(tools/i8_peak.cu, profiles/r01_i8_peak.json)"
+I8_NCU_TRAFFIC = 14.04e9  # dram read + write bytes of one level-4 launch (profiles/r01_m2l_i8_ncu.txt)
+I8_NCU_NOTE = "ncu --set full capture of the cfg2 level-4 launch (the longest of the step)"
 REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -139,6 +144,35 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def roofline_entry(stats, steps):
+    """Roofline of the dominant kernel from the live per-stage events of the timed region.
+
+    int8 M2L (default): m2l_i8_kernel, achieved = algorithmic int8 ops (2 nmod K^2 per V
+    application, K = 888, no padding) / its device time, against the measured kind::i8
+    peak. The FP64-equivalent rate (2 K^2 per application / the same time) is reported
+    beside it. DMMA M2L (PKGPU_M2L=dmma): the FP64 gather-GEMM against the DMMA peak."""
+    i8 = stats.get("m2l_i8", {})
+    m2l = stats.get("m2l", {})
+    if i8.get("seconds", 0) > 0:
+        n = max(1, i8.get("launches", 1))
+        s, fl = i8["seconds"] / n, i8["flops"] / n
+        achieved = fl / s / 1e12
+        return {"kernel": "m2l_i8_kernel (M2L, tcgen05.mma kind::i8, TMEM accumulators)", "bound": "tensor",
+                "achieved": achieved, "peak": I8_PEAK_TOPS, "unit": "TOP/s (int8)", "frac": achieved / I8_PEAK_TOPS,
+                "traffic": I8_NCU_TRAFFIC, "traffic_note": I8_NCU_NOTE,
+                "ops_per_launch": fl, "ms_per_launch": 1e3 * s, "launches_per_step": i8["launches"] / steps,
+                "fp64_equivalent_tflops": i8["units"] * 2 * 888 ** 2 / i8["seconds"] / 1e12,
+                "peak_source": I8_PEAK_SOURCE,
+                "op_convention": "2 x nmod x K^2 int8 ops per V-list application, K = 888 (padding to 896 not counted)"}
+    n = max(1, m2l.get("launches", 1))
+    s, fl = m2l.get("seconds", 0.0) / n, m2l.get("flops", 0.0) / n
+    achieved = fl / s / 1e12 if s > 0 else None
+    return {"kernel": "gather_gemm_tma_kernel (M2L, DMMA.8x8x4)", "bound": "tensor", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
+            "traffic": None, "flops_per_launch": fl, "ms_per_launch": 1e3 * s, "peak_source": FP64_PEAK_SOURCE,
+            "flop_convention": "2 K^2 per V-list application, K = 888 (SURVEY §8d)"}
+
+
 def run_ours(args):
     import torch
 
@@ -230,15 +264,11 @@ def run_ours(args):
     same = bool(np.array_equal(out_np, d_out.cpu().numpy()))
 
     if rank == 0:
-        m2l = stats.get("m2l", {})
-        m2l_launches = max(1, m2l.get("launches", 1))
-        per_launch_s = m2l.get("seconds", 0.0) / m2l_launches
-        per_launch_flops = m2l.get("flops", 0.0) / m2l_launches
-        achieved = per_launch_flops / per_launch_s / 1e12 if per_launch_s > 0 else None
         stage_tab = {k: {"ms_per_step": 1e3 * v["seconds"] / args.steps,
                          "tflops": (v["flops"] / v["seconds"] / 1e12) if v["seconds"] > 0 and v["flops"] else None,
                          "launches_per_step": v["launches"] / args.steps}
                      for k, v in stats.items() if k != "u_pairs"}
+        roofline = roofline_entry(stats, args.steps)
         line = {
             "metric": METRIC, "value": N_POINTS / (ms_max * 1e-3), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
@@ -253,12 +283,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int((3 + 3 + 3) * N_POINTS * 8),
                     "d2h_bytes_per_step": int(3 * N_POINTS * 8), "matches_device_result": same},
             "gpu_launches": int(round(launches)),
-            "roofline": {"kernel": "gather_gemm_kernel<128> (M2L, DMMA.8x8x4)", "bound": "tensor",
-                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
-                         "flops_per_launch": per_launch_flops, "ms_per_launch": 1e3 * per_launch_s,
-                         "peak_source": FP64_PEAK_SOURCE,
-                         "flop_convention": "2 K^2 per V-list application, K = 888 (SURVEY §8d)"},
+            "roofline": roofline,
             "stages": stage_tab,
             "clocks": clk,
         }

@@ -98,7 +98,10 @@ int64_t pkgpu_context_launch_count(pkgpu_context *ctx);
  * "s2m", "m2m", "pinv_up", "x", "m2l", "l2l", "pinv_dn", "periodic", "leaf".
  * seconds = summed device time, units = applications (dense) or pairs (pair sums),
  * flops = algorithmic FLOPs (2K^2 per translation, 4K^2+K per pinv, 11 / 28
- * per Laplace / Stokes pair), launches = kernel launches. Accumulated until reset. */
+ * per Laplace / Stokes pair), launches = kernel launches. Accumulated until reset.
+ * M2L levels on the int8 pipe add sub-stages "m2l_prep" (density residues), "m2l_i8"
+ * (the kind::i8 gather-GEMM; flops = int8 ops, 2 nmod K^2 per application) and
+ * "m2l_crt" (CRT rebuild), all also inside "m2l". */
 pkgpu_status pkgpu_context_set_profiling(pkgpu_context *ctx, int on);
 /* M2L arithmetic path. path 0: int8 tensor pipe (exact residue GEMMs, CRT rebuild in
  * FP64) on levels with >= min_boxes boxes, DMMA FP64 elsewhere (default; min_boxes <= 0
@@ -192,7 +195,7 @@ pkgpu_status pkgpu_surface_points(int p, const double *center, double edge, doub
  * the reference applies M2L as dense FP64 GEMMs, src/fmm.cpp:560-574). Device pointers:
  *   R[t][c][r] += sum_s sum_k A[t][s][r][k] * B[t][row(s, c)][k]   (balanced residues mod m_t)
  * A int8 [nmod][nmat][Ki][Ki], B int8 [nmod][rows_per_mod][Ki], src int32 [nslots][ld_src]
- * (row = src - box0, or zero_row when src < 0), R int32 [nmod][Ki][ncols]; Ki % 128 == 0,
+ * (row = src - box0, or zero_row when src < 0), R int32 [nmod][ncols][Ki]; Ki % 128 == 0,
  * ncols % 256 == 0. Exact integer results: the test hook for the kind::i8 kernel. */
 pkgpu_status pkgpu_i8_gather_gemm(pkgpu_context *ctx, const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
                                   int zero_row, int Ki, int nmod, const int32_t *src, int64_t ld_src, int64_t box0,

@@ -388,7 +388,8 @@ class Context:
     def launches(self) -> int:
         return lib().pkgpu_context_launch_count(self._h)
 
-    STAGES = ("tree", "lists", "s2m", "m2m", "pinv_up", "x", "m2l", "l2l", "pinv_dn", "periodic", "leaf")
+    STAGES = ("tree", "lists", "s2m", "m2m", "pinv_up", "x", "m2l", "l2l", "pinv_dn", "periodic", "leaf",
+              "m2l_prep", "m2l_i8", "m2l_crt")  # the last three: sub-stages of m2l on the int8 pipe
 
     def set_profiling(self, on: bool):
         lib().pkgpu_context_set_profiling(self._h, 1 if on else 0)
@@ -633,10 +634,10 @@ def i8_gather_gemm(A, B, rows_per_mod, zero_row, src, box0, R, context: Optional
     """The int8 tensor-pipe gather-GEMM (test hook; device tensors with .data_ptr()):
     R[t][c][r] += sum_s sum_k A[t][s][r][k] B[t][row(s, c)][k] as balanced residues mod
     m_t, row = src[s][c] - box0 (zero_row when src < 0). A int8 [nmod][nmat][Ki][Ki],
-    B int8 [nmod][rows_per_mod][Ki], src int32 [nslots][ncols], R int32 [nmod][Ki][ncols]."""
+    B int8 [nmod][rows_per_mod][Ki], src int32 [nslots][ncols], R int32 [nmod][ncols][Ki]."""
     ctx = context or default_context()
     nmod, nmat, Ki = A.shape[0], A.shape[1], A.shape[2]
-    assert tuple(R.shape) == (nmod, Ki, src.shape[1])
+    assert tuple(R.shape) == (nmod, src.shape[1], Ki)
     nslots, ncols = src.shape
     err = _errbuf()
     _check(lib().pkgpu_i8_gather_gemm(ctx._h, ctypes.c_void_p(A.data_ptr()), nmat, ctypes.c_void_p(B.data_ptr()),

@@ -46,40 +46,6 @@ __global__ void compat_partial_kernel(const double *__restrict__ s, int64_t n, i
         for (int c = 0; c < 4; c++) part[4 * blockIdx.x + c] = red[c][0];
 }
 
-// ---- fixed-point study (PKGPU_M2L_QUANT=beta): M2L operands rounded to beta-bit grids ----
-__global__ void rowmax_kernel(const double *__restrict__ A, int nmat, int Kp, unsigned long long *__restrict__ mx) {
-    const int r = blockIdx.x, o = blockIdx.y;
-    double m = 0;
-    for (int k = threadIdx.x; k < Kp; k += blockDim.x) m = fmax(m, fabs(A[((size_t)o * Kp + r) * Kp + k]));
-    for (int s = 16; s; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
-    if ((threadIdx.x & 31) == 0) atomicMax(&mx[r], (unsigned long long)__double_as_longlong(m));
-}
-__global__ void quant_rows_kernel(double *__restrict__ A, int nmat, int Kp, const unsigned long long *__restrict__ mx,
-                                  int beta) {
-    const int r = blockIdx.x, o = blockIdx.y;
-    const double m = __longlong_as_double((long long)mx[r]);
-    if (m == 0) return;
-    const int e = ilogb(m) + 1;
-    for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
-        double &a = A[((size_t)o * Kp + r) * Kp + k];
-        a = ldexp(rint(ldexp(a, beta - e)), e - beta);
-    }
-}
-__global__ void absmax_kernel(const double *__restrict__ x, int64_t n, unsigned long long *__restrict__ mx) {
-    double m = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        m = fmax(m, fabs(x[i]));
-    for (int s = 16; s; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
-    if ((threadIdx.x & 31) == 0) atomicMax(mx, (unsigned long long)__double_as_longlong(m));
-}
-__global__ void quant_vec_kernel(const double *__restrict__ x, double *__restrict__ y, int64_t n,
-                                 const unsigned long long *__restrict__ mx, int beta) {
-    const double m = __longlong_as_double((long long)*mx);
-    const int e = m == 0 ? 0 : ilogb(m) + 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = ldexp(rint(ldexp(x[i], beta - e)), e - beta);
-}
-
 __global__ void layout_keys_kernel(TreeView T, int *keys, int *vals, int *hist) {
     __shared__ int h[kMaxLevels * 8];
     for (int i = threadIdx.x; i < kMaxLevels * 8; i += blockDim.x) h[i] = 0;
@@ -770,36 +736,11 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         x_pass(g, T, ctx.lists, Q, st);
         ctx.launches += ctx.lists.x.count ? 1 : 0;
         prof.end(pm);
-        // PKGPU_M2L_QUANT=beta_a[,beta_b]
-        static const int qbeta = std::getenv("PKGPU_M2L_QUANT") ? std::atoi(std::getenv("PKGPU_M2L_QUANT")) : 0;
-        static const int qbeta_b = [] {
-            const char *e = std::getenv("PKGPU_M2L_QUANT");
-            const char *c = e ? std::strchr(e, ',') : nullptr;
-            return c ? std::atoi(c + 1) : qbeta;
-        }();
-        const double *m2l_A = ops.m2l;
-        double *Xq = nullptr;
-        unsigned long long *qmx = nullptr;
-        if (qbeta > 0) {
-            double *Aq = ws.get<double>("quant_m2l", (size_t)kNumM2L * Kp * Kp);
-            qmx = ws.get<unsigned long long>("quant_mx", Kp + 1);
-            PK_CUDA(cudaMemsetAsync(qmx, 0, (Kp + 1) * sizeof(unsigned long long), st));
-            PK_CUDA(cudaMemcpyAsync(Aq, ops.m2l, (size_t)kNumM2L * Kp * Kp * sizeof(double), cudaMemcpyDeviceToDevice, st));
-            rowmax_kernel<<<dim3(Kp, kNumM2L), 32, 0, st>>>(Aq, kNumM2L, Kp, qmx);
-            quant_rows_kernel<<<dim3(Kp, kNumM2L), 128, 0, st>>>(Aq, kNumM2L, Kp, qmx, qbeta);
-            m2l_A = Aq;
-            Xq = ws.get<double>("quant_x", nb * Kp);
-            PK_CUDA(cudaMemcpyAsync(Xq, Pup, nb * Kp * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        }
+        int i8_apps[kMaxLevels + 1] = {0}; // levels whose M2L ran on the int8 pipe
         for (int l = 0; l <= T.depth; l++) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (qbeta > 0 && hi > lo) {
-                PK_CUDA(cudaMemsetAsync(qmx + Kp, 0, sizeof(unsigned long long), st));
-                absmax_kernel<<<256, 256, 0, st>>>(Pup + lo * Kp, (hi - lo) * Kp, qmx + Kp);
-                quant_vec_kernel<<<256, 256, 0, st>>>(Pup + lo * Kp, Xq + lo * Kp, (hi - lo) * Kp, qmx + Kp, qbeta_b);
-            }
-            if (l >= 1 && Lay.i8[l] && qbeta == 0) {
+            if (l >= 1 && Lay.i8[l]) {
                 const I8Settings &is = ctx.i8;
                 if (!ops.i8.res || ops.i8.nmod != is.nmod || ops.i8.beta_a != is.beta_a) {
                     i8_build_operators(ops.i8, ops.ws, ops.m2l, kNumM2L, ops.K, Kp, is.nmod, is.beta_a, st);
@@ -819,8 +760,17 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573, 168-171)
                 pm = prof.begin("m2l");
-                ctx.launches += m2l_i8_level(ops.i8, a, is.beta_b, ws, st);
+                int ps = prof.begin("m2l_prep");
+                const I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
+                prof.end(ps);
+                ps = prof.begin("m2l_i8");
+                ctx.launches += m2l_i8_gemm(ops.i8, a, w, ws, st);
+                prof.end(ps);
+                ps = prof.begin("m2l_crt");
+                ctx.launches += m2l_i8_finish(ops.i8, a, w, is.beta_b, st);
+                prof.end(ps);
                 prof.end(pm);
+                i8_apps[l] = 1;
             } else if (l >= 1) {
                 GemmArgs a;
                 a.Kp = Kp;
@@ -829,10 +779,10 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.nslots = kNumM2L;
                 a.src = Lay.m2l_table + c0;
                 a.ld_src = Lay.ncols;
-                a.A = m2l_A;
+                a.A = ops.m2l;
                 a.nmat = kNumM2L;
                 a.bn = Lay.wide[l] ? 128 : 64;
-                a.X = Xq ? Xq : Pup;
+                a.X = Pup;
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573, 168-171)
                 a.beta = 1.0;
@@ -924,6 +874,22 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             prof.work("x", (double)h[4], pf);
             prof.work("m2m", (double)h[5], dense);
             prof.work("m2l", (double)ctx.lists.v_total, dense);
+            // int8 levels: V applications there (CSR offsets at the level bounds); the
+            // algorithmic int8 work is nmod K^2 MACs per application (2 ops per MAC)
+            double v_i8 = 0;
+            for (int l = 1; l <= T.depth; l++) {
+                if (!i8_apps[l]) continue;
+                int64_t o2[2];
+                PK_CUDA(cudaMemcpy(&o2[0], ctx.lists.v.off + T.level_off[l], sizeof(int64_t), cudaMemcpyDeviceToHost));
+                PK_CUDA(cudaMemcpy(&o2[1], ctx.lists.v.off + T.level_off[l + 1], sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost));
+                v_i8 += (double)(o2[1] - o2[0]);
+            }
+            if (v_i8 > 0) {
+                prof.work("m2l_i8", v_i8, 2.0 * ctx.i8.nmod * K * K);
+                prof.work("m2l_prep", v_i8, 0.0);
+                prof.work("m2l_crt", v_i8, 0.0);
+            }
             prof.work("l2l", (double)h[6], dense);
             prof.work("pinv_dn", (double)h[6], pinv);
             prof.work("pinv_up", (double)h[7], pinv);

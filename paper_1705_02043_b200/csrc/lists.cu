@@ -318,6 +318,9 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
     for (int i = 0; i < 4; i++) scan_counts(ws, cnt[i], off[i], nb, st, tot[i]);
     PK_CUDA(cudaStreamSynchronize(st));
     L.v_total = tot[1];
+    L.v.off = off[1]; // per-box V counts as offsets (entries live in the M2L table)
+    L.v.count = tot[1];
+    L.v.ent = nullptr;
     CsrList *lists[4] = {&L.u, &L.v, &L.w, &L.x};
     for (int i : {0, 2, 3}) {
         lists[i]->off = off[i];

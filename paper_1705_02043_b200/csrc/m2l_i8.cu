@@ -1,20 +1,26 @@
 // M2L on the int8 tensor pipe (see m2l_i8.h for the arithmetic).
 //
-// Kernel m2l_i8_kernel: persistent, one CTA per SM, 6 warps:
-//   warp 0      producer: per (active slot, 128-deep k chunk) one TMA 3D load of the
-//               128 x 128 operator residue tile (128B swizzle) and 64 TMA gather4 loads of
-//               the 256 gathered box rows (128B swizzle) onto the stage's "full" mbarrier
-//   warp 1      MMA issuer: allocates 512 TMEM columns (two 128 x 256 int32 accumulators),
-//               one elected thread issues 4 x tcgen05.mma.cta_group::1.kind::i8 (M128 N256
-//               K32) per stage and tcgen05.commit's the stage back to the producer
-//   warps 2..5  epilogue: tcgen05.ld the finished accumulator (lane quarter warp % 4),
-//               reduce mod m_t and red.add into R[t][col][row]; overlaps the next unit's
-//               MMAs through the second accumulator
-// Work unit = (modulus, 128-row tile, 256-column tile, chunk of the tile's active slots);
-// chunks keep |int32 accumulator| < 2^31 (slots * Ki * 128^2).
+// Kernel m2l_i8_kernel: persistent, one CTA per SM, 7 warps.
+//   Tile: 128 gathered boxes (MMA M) x Nt operator rows (MMA N, Nt <= 256, Ki / Nt tiles)
+//   per modulus, reduced over the tile's active V-list slots x 128-byte k-chunks.
+//   warps 0-1  producers: per stage, 16 cp.async of 16 B per thread gather the 128 box
+//              residue rows (128 B each, 128B swizzle applied by hand: chunk c of row j
+//              lands at j*128 + ((c ^ (j & 7)) << 4)); thread 0 also issues the TMA 3D
+//              load of the Nt x 128 operator residue tile (hardware 128B swizzle).
+//              Completion: cp.async.mbarrier.arrive.noinc x 64 + expect_tx on "full".
+//   warp 2     MMA issuer: allocates 512 TMEM columns (two 128 x 256 int32 accumulators);
+//              one thread waits "full", fences the cp.async (generic proxy) writes into
+//              the async proxy, issues 4 x tcgen05.mma.cta_group::1.kind::i8 (K = 32 B
+//              each) and tcgen05.commit's the stage back to "empty".
+//   warps 3-6  epilogue: tcgen05.ld (lane quarter = warp % 4: 32 boxes) 32 columns at a
+//              time, reduce mod m_t, transpose through shared memory and red.add into
+//              R[t][col][row] with 128-byte coalesced atomics; the second accumulator
+//              lets the next unit's MMAs run meanwhile.
+// Work unit = (modulus, operator row tile, 128-column tile, chunk of the tile's active
+// slots); chunks keep |int32 accumulator| <= slots * Ki * 128^2 < 2^31.
 #include <algorithm>
-#include <cstdlib>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cudaTypedefs.h>
@@ -26,14 +32,17 @@ namespace pkgpu {
 
 namespace {
 
-constexpr int BM = 128, BNI = kI8Tile, BKI = 128, NST = 4;
-constexpr int A_BYTES = BM * BKI, B_BYTES = BNI * BKI, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BKI = 128;            // k-chunk (bytes = int8 elements) per stage
+constexpr int TBM = 128;            // gathered boxes per tile (MMA M)
+constexpr int A_BYTES = TBM * BKI;  // gathered tile
+constexpr int B_BYTES = 256 * BKI;  // operator tile, Nt <= 256 rows
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NST = 4;
+constexpr int NPROD = 2; // producer warps
+constexpr int MMA_WARP = NPROD;
+constexpr int NTHREADS = (NPROD + 1 + 4) * 32;
 constexpr int MAX_SLOTS = 320;
-constexpr int NTHREADS = 6 * 32;
-// instruction descriptor: D s32 (bits 4-5 = 2), A/B signed int8 (bits 7-9, 10-12 = 1),
-// K-major A and B, N >> 3 at bit 17, M >> 4 at bit 24
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BNI >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+constexpr int EPI_PITCH = 33; // transpose tile row pitch (ints), conflict-free
 
 const int kModuli[kI8MaxModuli] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
                                    223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
@@ -42,29 +51,24 @@ __constant__ int c_mod[kI8MaxModuli];
 __constant__ int c_pm[kI8MaxModuli][kI8MaxModuli]; // (prod_{s' < s} m_s') mod m_t, s < t
 __constant__ int c_pinv[kI8MaxModuli];              // (prod_{s < t} m_s)^-1 mod m_t
 
-struct I8Params {
-    CUtensorMap tmA; // (Ki, Ki, nmod * nmat) int8, box (128, 128, 1), 128B swizzle
-    CUtensorMap tmB; // (Ki, nmod * rows_per_mod) int8, box (128, 1), 128B swizzle, gather4
+struct Params {
+    CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
+    const int8_t *X; // box residues [nmod][rows_per_mod][Ki]
     const int *src;
     int64_t ld_src, box0;
     int zero_row, rows_per_mod;
     const int *tile_slots, *tile_nact;
-    int nmat, nmod, KC, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
-    int *R;
+    int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
+    uint32_t idesc;
+    int *R; // [nmod][ncols][Ki]
 };
 
-// ---- tcgen05 / TMA helpers ----
+// ---- tcgen05 helpers ----
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     // K-major, 128B swizzle: start >> 4, LBO 16 B (unused), SBO 1024 B (8-row groups),
     // descriptor version 1 (bit 46), layout SWIZZLE_128B = 2 (bits 61-63)
     return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -73,14 +77,6 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, int c0, int r0, int r1, int r2, int r3,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-        "%4, %5, %6}], [%7];\n" ::"r"(tma::smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(tma::smem_u32(bar))
-        : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
                  "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
@@ -96,7 +92,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 struct Unit {
     int t, rt, ct, s0, s1;
 };
-__device__ __forceinline__ Unit decode(const I8Params &p, int u) {
+__device__ __forceinline__ Unit decode(const Params &p, int u) {
+    // row tile fastest: consecutive units (running concurrently) share their gathered rows
     Unit x;
     x.rt = u % p.rowtiles;
     u /= p.rowtiles;
@@ -110,17 +107,18 @@ __device__ __forceinline__ Unit decode(const I8Params &p, int u) {
     return x;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_constant__ I8Params p) {
+__global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_constant__ Params p) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int *s_epi = reinterpret_cast<int *>(smem + NST * STAGE_BYTES); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
-    __shared__ int s_rows[BNI];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NPT = NPROD * 32;
     if (tid == 0) {
         for (int s = 0; s < NST; s++) {
-            tma::mbar_init(&full[s], 1);
+            tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
             tma::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -129,7 +127,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == 1) {
+    if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
                          tma::smem_u32(&s_tmem))
                      : "memory");
@@ -147,169 +145,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
         const int n = (x.s1 - x.s0) * p.KC;
         if (n == 0) continue;
         const int *slots = p.tile_slots + x.ct * MAX_SLOTS;
-        if (warp == 0) {
-            // ---------------- producer ----------------
-            for (int si = x.s0; si < x.s1; si++) {
-                const int slot = slots[si];
-                __syncwarp();
-                for (int j = lane; j < BNI; j += 32) {
-                    const int b = p.src[(int64_t)slot * p.ld_src + x.ct * BNI + j];
-                    s_rows[j] = x.t * p.rows_per_mod + (b >= 0 ? (int)(b - p.box0) : p.zero_row);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    for (int kc = 0; kc < p.KC; kc++) {
-                        const int gi = g + (si - x.s0) * p.KC + kc, st = gi % NST;
-                        tma::mbar_wait(&empty[st], ((gi / NST) & 1) ^ 1);
-                        unsigned char *as = smem + st * STAGE_BYTES, *bs = as + A_BYTES;
-                        tma::mbar_expect_tx(&full[st], STAGE_BYTES);
-                        tma::tma_load_3d(as, &p.tmA, kc * BKI, x.rt * BM, x.t * p.nmat + slot, &full[st]);
-#pragma unroll 4
-                        for (int q = 0; q < BNI / 4; q++)
-                            tma_gather4(bs + q * 4 * BKI, &p.tmB, kc * BKI, s_rows[4 * q], s_rows[4 * q + 1],
-                                        s_rows[4 * q + 2], s_rows[4 * q + 3], &full[st]);
-                    }
-                }
-            }
-            __syncwarp();
-        } else if (warp == 1) {
-            // ---------------- MMA issuer ----------------
-            if (lane == 0) {
-                const int buf = jb & 1;
-                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t dt = tmem + buf * BNI;
-                for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % NST;
-                    tma::mbar_wait(&full[st], (gi / NST) & 1);
-                    tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * STAGE_BYTES);
-                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
-#pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++) // K = 32 bytes per MMA: +2 in the 16-byte start field
-                        mma_i8(dt, ad + 2 * kk, bd + 2 * kk, (i > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(&empty[st]);
-                }
-                umma_commit(&tfull[buf]);
-            }
-            __syncwarp();
-        } else {
-            // ---------------- epilogue ----------------
-            const int buf = jb & 1, q = warp & 3;
-            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
-            tc_fence_after();
-            const int m = c_mod[x.t];
-            const double inv = 1.0 / m;
-            const int row = x.rt * BM + q * 32 + lane;
-            int *Rt = p.R + ((int64_t)x.t * p.ncols + x.ct * BNI) * p.Ki + row;
-            for (int j0 = 0; j0 < BNI; j0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * BNI + j0, v);
-#pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const int a = (int)v[j];
-                    const int r = a - __double2int_rn((double)a * inv) * m;
-                    if (r) atomicAdd(Rt + (int64_t)(j0 + j) * p.Ki, r);
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tma::mbar_arrive(&tempty[buf]);
-        }
-        g += n;
-        jb++;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
-    }
-}
-
-// ---------------------------------------------------------------------------
-// v2: gathered box rows on the M side (128 per tile, cp.async by two producer warps with
-// the 128B swizzle applied by hand), operator rows on the N side (Nt <= 256 per tile, one
-// TMA 3D load per stage). Per stage: 16 KB gathered + Nt x 128 B operator, 128 x Nt x 128
-// MACs. R is laid out [t][row][col] so the epilogue's atomics are coalesced over boxes.
-constexpr int V2_BM = 128;        // gathered boxes per tile (MMA M)
-constexpr int V2_A_BYTES = V2_BM * BKI;
-constexpr int V2_B_BYTES = 256 * BKI; // operator tile, Nt <= 256 rows
-constexpr int V2_STAGE = V2_A_BYTES + V2_B_BYTES;
-constexpr int V2_NST = 4;
-constexpr int V2_PRODUCERS = 2;   // warps
-constexpr int V2_THREADS = (V2_PRODUCERS + 1 + 4) * 32;
-
-struct V2Params {
-    CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
-    const int8_t *X; // box residues [nmod][rows_per_mod][Ki]
-    const int *src;
-    int64_t ld_src, box0;
-    int zero_row, rows_per_mod;
-    const int *tile_slots, *tile_nact;
-    int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
-    uint32_t idesc;
-    int *R; // [nmod][Ki][ncols]
-};
-
-__device__ __forceinline__ Unit decode_v2(const V2Params &p, int u) {
-    Unit x;
-    x.rt = u % p.rowtiles;
-    u /= p.rowtiles;
-    x.ct = u % p.coltiles;
-    u /= p.coltiles;
-    const int chunk = u % p.nchunk;
-    x.t = u / p.nchunk;
-    const int nact = p.tile_nact[x.ct];
-    x.s0 = nact * chunk / p.nchunk;
-    x.s1 = nact * (chunk + 1) / p.nchunk;
-    return x;
-}
-
-__global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_constant__ V2Params p) {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    __shared__ __align__(8) uint64_t full[V2_NST], empty[V2_NST], tfull[2], tempty[2];
-    __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int NPT = V2_PRODUCERS * 32;
-    if (tid == 0) {
-        for (int s = 0; s < V2_NST; s++) {
-            tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
-            tma::mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; b++) {
-            tma::mbar_init(&tfull[b], 1);
-            tma::mbar_init(&tempty[b], 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == V2_PRODUCERS) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         tma::smem_u32(&s_tmem))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = s_tmem;
-
-    int g = 0, jb = 0;
-    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
-        const Unit x = decode_v2(p, u);
-        const int n = (x.s1 - x.s0) * p.KC;
-        if (n == 0) continue;
-        const int *slots = p.tile_slots + x.ct * MAX_SLOTS;
-        if (warp < V2_PRODUCERS) {
-            // ---------------- producers: 16 cp.async of 16 B per thread per stage ----------------
-            // thread -> chunk c = lane & 7 of rows j = (tid >> 3) + 8 i, i < 16
+        if (warp < NPROD) {
+            // ---------------- producers ----------------
+            // thread -> 16-byte chunk c = lane & 7 of rows j = (tid >> 3) + 8 i, i < 16
             const int c = lane & 7, j0 = tid >> 3;
             const int8_t *Xt = p.X + (int64_t)x.t * p.rows_per_mod * p.Ki + c * 16;
             for (int si = x.s0; si < x.s1; si++) {
                 const int slot = slots[si];
-                const int *srow = p.src + (int64_t)slot * p.ld_src + x.ct * V2_BM;
+                const int *srow = p.src + (int64_t)slot * p.ld_src + x.ct * TBM;
                 int64_t off[16];
 #pragma unroll
                 for (int i = 0; i < 16; i++) {
@@ -317,13 +160,12 @@ __global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_c
                     off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
                 }
                 for (int kc = 0; kc < p.KC; kc++) {
-                    const int gi = g + (si - x.s0) * p.KC + kc, st = gi % V2_NST;
-                    tma::mbar_wait(&empty[st], ((gi / V2_NST) & 1) ^ 1);
-                    unsigned char *as = smem + st * V2_STAGE;
+                    const int gi = g + (si - x.s0) * p.KC + kc, st = gi % NST;
+                    tma::mbar_wait(&empty[st], ((gi / NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * STAGE_BYTES;
                     if (tid == 0) {
                         tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        tma::tma_load_3d(as + V2_A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot,
-                                         &full[st]);
+                        tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot, &full[st]);
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
@@ -333,7 +175,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_c
                     tma::cp_async_mbar_arrive(&full[st]);
                 }
             }
-        } else if (warp == V2_PRODUCERS) {
+        } else if (warp == MMA_WARP) {
             // ---------------- MMA issuer ----------------
             if (lane == 0) {
                 const int buf = jb & 1;
@@ -341,43 +183,53 @@ __global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_c
                 tc_fence_after();
                 const uint32_t dt = tmem + buf * 256;
                 for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % V2_NST;
-                    tma::mbar_wait(&full[st], (gi / V2_NST) & 1);
-                    // cp.async wrote the gathered rows through the generic proxy
+                    const int gi = g + i, st = gi % NST;
+                    tma::mbar_wait(&full[st], (gi / NST) & 1);
+                    // the gathered rows were written by cp.async through the generic proxy
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * V2_STAGE);
-                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + V2_A_BYTES);
+                    const uint32_t a0 = tma::smem_u32(smem + st * STAGE_BYTES);
+                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++)
+                    for (int kk = 0; kk < BKI / 32; kk++) // K = 32 bytes per MMA: +2 in the 16-byte start field
                         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"((i > 0 || kk > 0) ? 1u : 0u));
+                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
+                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
                     umma_commit(&empty[st]);
                 }
                 umma_commit(&tfull[buf]);
             }
             __syncwarp();
         } else {
-            // ---------------- epilogue: lane = box, TMEM column = operator row ----------------
+            // ---------------- epilogue: TMEM lane = box, column = operator row ----------------
             const int buf = jb & 1, q = warp & 3;
+            int *tile = s_epi + (warp - MMA_WARP - 1) * 32 * EPI_PITCH;
             tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
             tc_fence_after();
             const int m = c_mod[x.t];
-            const double inv = 1.0 / m;
-            const int col = x.ct * V2_BM + q * 32 + lane;
+            const float inv = 1.0f / (float)m;
+            const int col0 = x.ct * TBM + q * 32;
             const int r0 = x.rt * p.Nt;
-            int *Rt = p.R + ((int64_t)x.t * p.Ki + r0) * p.ncols + col;
             const int nr = min(p.Nt, p.Ki - r0);
+            int *Rt = p.R + ((int64_t)x.t * p.ncols + col0) * p.Ki + r0;
             for (int j0 = 0; j0 < p.Nt; j0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, v);
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
+                    // |a| < 2^31: float quotient is off by at most one; r in (-3m/2, 3m/2)
                     const int a = (int)v[j];
-                    const int r = a - __double2int_rn((double)a * inv) * m;
-                    if (r && j0 + j < nr) atomicAdd(Rt + (int64_t)(j0 + j) * p.ncols, r);
+                    tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
                 }
+                __syncwarp();
+                const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                for (int b = 0; b < 32; b++) {
+                    const int r = tile[b * EPI_PITCH + lane]; // box col0 + b, row r0 + j0 + lane
+                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                }
+                __syncwarp();
             }
             tc_fence_before();
             __syncwarp();
@@ -388,15 +240,15 @@ __global__ void __launch_bounds__(V2_THREADS, 1) m2l_i8_v2_kernel(const __grid_c
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == V2_PRODUCERS) {
+    if (warp == MMA_WARP) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
     }
 }
 
 // active slots per column tile of `bn` columns, in slot order
-__global__ void i8_slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
-                                    int *tile_nact) {
+__global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
+                                 int *tile_nact) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
@@ -423,6 +275,13 @@ __device__ __forceinline__ int mod_pos(long long a, int m, double inv) {
     if (r >= m) r -= m;
     return (int)r;
 }
+__device__ __forceinline__ int mod_small(int a, int m, float inv) {
+    // |a| < 2^22: float quotient off by at most one
+    int r = a - __float2int_rd((float)a * inv) * m;
+    if (r < 0) r += m;
+    if (r >= m) r -= m;
+    return r;
+}
 __device__ __forceinline__ int balanced(int r, int m) { return r >= (m + 1) / 2 ? r - m : r; }
 
 // residues of v (|v| <= 2^62) for all moduli, via v = a2 2^42 + a1 2^21 + a0
@@ -430,9 +289,8 @@ __device__ __forceinline__ void residues(long long v, int nmod, int8_t *out, int
     const long long a0 = v & ((1ll << 21) - 1), a1 = (v >> 21) & ((1ll << 21) - 1), a2 = v >> 42;
     for (int t = 0; t < nmod; t++) {
         const int m = c_mod[t];
-        const double inv = 1.0 / m;
         const int c21 = (int)((1ll << 21) % m), c42 = (int)(((long long)c21 * c21) % m);
-        const int r = mod_pos(a2 * c42 + a1 * c21 + a0, m, inv);
+        const int r = mod_pos(a2 * c42 + a1 * c21 + a0, m, 1.0 / m);
         out[t * stride] = (int8_t)balanced(r, m);
     }
 }
@@ -459,8 +317,7 @@ __global__ void op_residue_kernel(const double *__restrict__ A, int nmat, int K,
     int8_t *out = res + ((int64_t)o * Ki + r) * Ki;
     for (int k = threadIdx.x; k < Ki; k += blockDim.x) {
         const double a = (r < K && k < K) ? A[((size_t)o * Kp + r) * Kp + k] : 0.0;
-        const long long v = llrint(ldexp(a, beta - rowexp[r]));
-        residues(v, nmod, out + k, stride);
+        residues(llrint(ldexp(a, beta - rowexp[r])), nmod, out + k, stride);
     }
 }
 
@@ -492,9 +349,9 @@ __global__ void x_residue_kernel(const double *__restrict__ X, int64_t nbox, int
     }
 }
 
-// Garner (balanced mixed-radix digits) + Horner in FP64: Y[out(c)][r] += alpha 2^(e_r + E - ba - bb) S
-// R layout: RC = true -> [t][r][c] (v2 kernel), false -> [t][c][r] (v1 kernel)
-template <int NM, bool RC>
+// Garner (balanced mixed-radix digits) + Horner in FP64:
+//   Y[out(c)][r] += alpha 2^(e_r + E - beta_a - beta_b) S,  R = [t][c][r]
+template <int NM>
 __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki, int K, int Kp,
                                    const int *__restrict__ out_box, const int *__restrict__ rowexp,
                                    const unsigned long long *__restrict__ mx, int beta_sum, double alpha,
@@ -502,20 +359,22 @@ __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki,
     const int64_t n = (int64_t)ncols * Ki;
     const int E = level_exp(mx);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = RC ? (int)(i % ncols) : (int)(i / Ki), r = RC ? (int)(i / ncols) : (int)(i % Ki);
+        const int c = (int)(i / Ki), r = (int)(i % Ki);
         if (r >= K) continue;
         const int ob = out_box[c];
         if (ob < 0) continue;
-        int acc[NM], v[NM];
+        int x[NM], acc[NM], v[NM];
 #pragma unroll
-        for (int t = 0; t < NM; t++) acc[t] = 0;
+        for (int t = 0; t < NM; t++) {
+            x[t] = R[(int64_t)t * n + i];
+            acc[t] = 0;
+        }
 #pragma unroll
         for (int t = 0; t < NM; t++) {
             const int m = c_mod[t];
-            const double inv = 1.0 / m;
-            const int x = mod_pos((long long)R[(int64_t)t * n + i] - acc[t], m, inv);
-            const int uu = mod_pos((long long)x * c_pinv[t], m, inv);
-            v[t] = balanced(uu, m);
+            const float inv = 1.0f / (float)m;
+            const int d = mod_small(x[t] - acc[t], m, inv);
+            v[t] = balanced(mod_small(d * c_pinv[t], m, inv), m);
 #pragma unroll
             for (int s = t + 1; s < NM; s++) acc[s] += v[t] * c_pm[t][s];
         }
@@ -538,26 +397,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-void encode(CUtensorMap *m, const void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
-            const cuuint32_t *box) {
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void *>(base), dims, strides, box,
-                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
-}
-
-// CRT tables (host): pm[s][t] = prod_{s' < s} m_s' mod m_t ; pinv[t] = (prod_{s < t} m_s)^-1 mod m_t
+// CRT tables: pm[s][t] = prod_{s' < s} m_s' mod m_t ; pinv[t] = (prod_{s < t} m_s)^-1 mod m_t
 void upload_tables() {
-    static bool done = false; // per process; __constant__ data is per device: re-uploaded per device below
     static int dev_done[64] = {0};
     int dev = 0;
     PK_CUDA(cudaGetDevice(&dev));
-    if (done && dev < 64 && dev_done[dev]) return;
+    if (dev < 64 && dev_done[dev]) return;
     int pm[kI8MaxModuli][kI8MaxModuli] = {}, pinv[kI8MaxModuli] = {};
     for (int t = 0; t < kI8MaxModuli; t++) {
         const int m = kModuli[t];
-        long long P = 1 % m; // prod_{s < t} m_s mod m
+        long long P = 1 % m;
         for (int s = 0; s < t; s++) {
             pm[s][t] = (int)P;
             P = P * (kModuli[s] % m) % m;
@@ -571,7 +420,6 @@ void upload_tables() {
     PK_CUDA(cudaMemcpyToSymbol(c_mod, kModuli, sizeof kModuli));
     PK_CUDA(cudaMemcpyToSymbol(c_pm, pm, sizeof pm));
     PK_CUDA(cudaMemcpyToSymbol(c_pinv, pinv, sizeof pinv));
-    done = true;
     if (dev < 64) dev_done[dev] = 1;
 }
 
@@ -596,7 +444,7 @@ const I8Settings &i8_settings() {
             if (std::sscanf(c, "%d,%d,%d", &a, &b, &d) == 3) r.nmod = a, r.beta_a = b, r.beta_b = d;
         }
         if (const char *c = std::getenv("PKGPU_M2L_I8_MIN")) r.min_boxes = std::atoll(c);
-        r.nmod = std::max(2, std::min(r.nmod, kI8MaxModuli));
+        r.nmod = std::max(14, std::min(r.nmod, kI8MaxModuli));
         return r;
     }();
     return s;
@@ -620,21 +468,15 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
     PK_CUDA(cudaGetLastError());
 }
 
-namespace {
-
-bool use_v1() {
-    static const bool v = [] {
-        const char *e = std::getenv("PKGPU_I8_KERNEL");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    return v;
-}
-
-int i8_gather_gemm_v2(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
-                      const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
-                      cudaStream_t st) {
+int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
+                   const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
+                   cudaStream_t st) {
+    if (ncols == 0 || nslots == 0) return 0;
+    if (ncols % kI8Tile != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
+        throw RuntimeError("i8_gather_gemm: bad shape");
+    upload_tables();
     const int num_sms = sm_count();
-    V2Params p;
+    Params p;
     std::memset(&p, 0, sizeof p);
     p.X = B;
     p.src = src;
@@ -648,11 +490,13 @@ int i8_gather_gemm_v2(const int8_t *A, int nmat, const int8_t *B, int rows_per_m
     // operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
     p.rowtiles = (Ki + 255) / 256;
     p.Nt = ((Ki + p.rowtiles - 1) / p.rowtiles + 15) / 16 * 16;
-    p.coltiles = ncols / V2_BM;
+    p.coltiles = ncols / TBM;
     p.ncols = ncols;
     p.Ki = Ki;
     p.R = R;
-    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(V2_BM >> 4) << 24);
+    // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
+    // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
     const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
     int nchunk = (int)((nslots + cmax - 1) / cmax);
     const int64_t base = (int64_t)nmod * p.rowtiles * p.coltiles;
@@ -661,78 +505,18 @@ int i8_gather_gemm_v2(const int8_t *A, int nmat, const int8_t *B, int rows_per_m
     p.total_units = (int)(base * nchunk);
     int *tslots = ws.get<int>("i8_tile_slots", (size_t)p.coltiles * MAX_SLOTS);
     int *tnact = ws.get<int>("i8_tile_nact", p.coltiles);
-    i8_slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, V2_BM, tslots, tnact);
+    slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, TBM, tslots, tnact);
     p.tile_slots = tslots;
     p.tile_nact = tnact;
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
     const cuuint32_t box[3] = {BKI, (cuuint32_t)p.Nt, 1};
-    encode(&p.tmB, A, 3, dims, strides, box);
-    const size_t smem = (size_t)V2_NST * V2_STAGE + 1024;
-    static bool cfg = false;
-    if (!cfg) {
-        PK_CUDA(cudaFuncSetAttribute(m2l_i8_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cfg = true;
-    }
-    const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
-    m2l_i8_v2_kernel<<<grid, V2_THREADS, smem, st>>>(p);
-    PK_CUDA(cudaGetLastError());
-    return 2;
-}
-
-} // namespace
-
-int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
-                   const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
-                   cudaStream_t st) {
-    if (ncols == 0 || nslots == 0) return 0;
-    if (ncols % BNI != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
-        throw RuntimeError("i8_gather_gemm: bad shape");
-    upload_tables();
-    if (!use_v1())
-        return i8_gather_gemm_v2(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R,
-                                 ws, st);
-    const int num_sms = sm_count();
-    I8Params p;
-    std::memset(&p, 0, sizeof p);
-    p.src = src;
-    p.ld_src = ld_src;
-    p.box0 = box0;
-    p.zero_row = zero_row;
-    p.rows_per_mod = rows_per_mod;
-    p.nmat = nmat;
-    p.nmod = nmod;
-    p.KC = Ki / BKI;
-    p.rowtiles = Ki / BM;
-    p.coltiles = ncols / BNI;
-    p.ncols = ncols;
-    p.Ki = Ki;
-    p.R = R;
-    // slots per chunk keep |acc| <= slots * Ki * 128^2 < 2^31
-    const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
-    int nchunk = (int)((nslots + cmax - 1) / cmax);
-    const int64_t base = (int64_t)nmod * p.rowtiles * p.coltiles;
-    while (base * nchunk < 3LL * num_sms && nchunk * 16 < nslots) nchunk++;
-    p.nchunk = nchunk;
-    p.total_units = (int)(base * nchunk);
-    int *tslots = ws.get<int>("i8_tile_slots", (size_t)p.coltiles * MAX_SLOTS);
-    int *tnact = ws.get<int>("i8_tile_nact", p.coltiles);
-    i8_slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, BNI, tslots, tnact);
-    p.tile_slots = tslots;
-    p.tile_nact = tnact;
-    {
-        const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
-        const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
-        const cuuint32_t box[3] = {BKI, BM, 1};
-        encode(&p.tmA, A, 3, dims, strides, box);
-    }
-    {
-        const cuuint64_t dims[2] = {(cuuint64_t)Ki, (cuuint64_t)nmod * rows_per_mod};
-        const cuuint64_t strides[1] = {(cuuint64_t)Ki};
-        const cuuint32_t box[2] = {BKI, 1};
-        encode(&p.tmB, B, 2, dims, strides, box);
-    }
-    const size_t smem = (size_t)NST * STAGE_BYTES + 1024;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
+    const size_t smem = (size_t)NST * STAGE_BYTES + 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
     static bool cfg = false;
     if (!cfg) {
         PK_CUDA(cudaFuncSetAttribute(m2l_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -744,42 +528,58 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     return 2;
 }
 
-int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {
-    if (a.ncols == 0) return 0;
+I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st,
+                           int64_t *launches) {
+    I8LevelWork w;
+    if (a.ncols == 0) return w;
     const int nmod = o.nmod, Ki = o.Ki;
-    const int64_t rows = a.nbox + 1;
-    unsigned long long *mx = ws.get<unsigned long long>("i8_level_max", 1);
-    PK_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
-    level_absmax_kernel<<<296, 256, 0, st>>>(a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, mx);
-    int8_t *xres = ws.get<int8_t>("i8_xres", (size_t)nmod * rows * Ki);
-    x_residue_kernel<<<(unsigned)std::min<int64_t>((rows * Ki + 255) / 256, 148 * 16), 256, 0, st>>>(
-        a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, Ki, nmod, beta_b, mx, xres);
-    int *R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
-    PK_CUDA(cudaMemsetAsync(R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
-    int launches = 2;
-    launches += i8_gather_gemm(o.res, o.nmat, xres, (int)rows, (int)a.nbox, Ki, nmod, a.src, a.ld_src, a.box0,
-                               a.nslots, a.ncols, R, ws, st);
-    const int64_t n = (int64_t)a.ncols * Ki;
+    w.rows = a.nbox + 1;
+    w.mx = ws.get<unsigned long long>("i8_level_max", 1);
+    PK_CUDA(cudaMemsetAsync(w.mx, 0, sizeof(unsigned long long), st));
+    level_absmax_kernel<<<296, 256, 0, st>>>(a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, w.mx);
+    int8_t *xres = ws.get<int8_t>("i8_xres", (size_t)nmod * w.rows * Ki);
+    x_residue_kernel<<<(unsigned)std::min<int64_t>((w.rows * Ki + 255) / 256, 148 * 16), 256, 0, st>>>(
+        a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, Ki, nmod, beta_b, w.mx, xres);
+    w.xres = xres;
+    w.R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
+    PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
+    PK_CUDA(cudaGetLastError());
+    if (launches) *launches += 2;
+    return w;
+}
+
+int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st) {
+    if (a.ncols == 0) return 0;
+    return i8_gather_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)a.nbox, o.Ki, o.nmod, a.src, a.ld_src, a.box0,
+                          a.nslots, a.ncols, w.R, ws, st);
+}
+
+int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int beta_b, cudaStream_t st) {
+    if (a.ncols == 0) return 0;
+    const int64_t n = (int64_t)a.ncols * o.Ki;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
     const int bs = o.beta_a + beta_b;
-    const bool rc = !use_v1();
-    switch (nmod) {
+    switch (o.nmod) {
 #define PK_RC(NM)                                                                                                      \
     case NM:                                                                                                           \
-        if (rc)                                                                                                        \
-            reconstruct_kernel<NM, true><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, mx, bs, \
-                                                               a.alpha, a.Y);                                          \
-        else                                                                                                           \
-            reconstruct_kernel<NM, false><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, mx,    \
-                                                                bs, a.alpha, a.Y);                                     \
+        reconstruct_kernel<NM><<<grid, 256, 0, st>>>(w.R, a.ncols, o.Ki, a.K, a.Kp, a.out_box, o.rowexp, w.mx, bs,     \
+                                                     a.alpha, a.Y);                                                    \
         break;
         PK_RC(14) PK_RC(15) PK_RC(16) PK_RC(17) PK_RC(18) PK_RC(19) PK_RC(20)
 #undef PK_RC
     default:
-        throw RuntimeError("m2l_i8: unsupported modulus count " + std::to_string(nmod));
+        throw RuntimeError("m2l_i8: unsupported modulus count " + std::to_string(o.nmod));
     }
     PK_CUDA(cudaGetLastError());
-    return launches + 1;
+    return 1;
+}
+
+int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {
+    int64_t l = 0;
+    const I8LevelWork w = m2l_i8_prepare(o, a, beta_b, ws, st, &l);
+    l += m2l_i8_gemm(o, a, w, ws, st);
+    l += m2l_i8_finish(o, a, w, beta_b, st);
+    return (int)l;
 }
 
 } // namespace pkgpu

@@ -10,7 +10,8 @@
 // modulus (balanced residues, |x| <= 128); the Chinese remainder theorem (Garner mixed
 // radix, Horner in FP64) rebuilds S from the residues and q += 2^l 2^(e_r + E - beta_a -
 // beta_b) S. The only approximation is the two fixed-point roundings (2^-beta of the
-// row / level maxima); with beta = 56 they sit below the FP64 rounding of the operands.
+// row / level maxima). Default: 16 moduli (2^125.4), beta_a = beta_b = 52 -- end-to-end
+// results indistinguishable from the FP64 DMMA path (profiles/r01_m2l_arith_study.md).
 #pragma once
 
 #include <cstdint>
@@ -30,7 +31,7 @@ struct I8Operators {          // residues of the stacked M2L operators (built on
 
 struct I8Settings {
     bool enabled = false;
-    int nmod = 17, beta_a = 56, beta_b = 56;
+    int nmod = 16, beta_a = 52, beta_b = 52; // accuracy study: profiles/r01_m2l_arith_study.md
     int64_t min_boxes = 1;    // levels with fewer boxes stay on the DMMA gather-GEMM
 };
 // PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes
@@ -51,13 +52,27 @@ struct I8LevelArgs {
     double *Y = nullptr;          // [box][Kp]: Y += alpha * sum_slot M X
     double alpha = 1.0;
 };
-// Returns kernel launches.
+struct I8LevelWork {
+    const int8_t *xres = nullptr;     // [nmod][nbox + 1][Ki] density residues (last row zero)
+    int *R = nullptr;                 // [nmod][ncols][Ki] residue sums
+    unsigned long long *mx = nullptr; // level max |phi| (bit pattern)
+    int64_t rows = 0;
+};
+// The three steps of one level (separately timed by the stage profiler):
+//   prepare: level max, density residues, R = 0
+//   gemm:    the kind::i8 gather-GEMM (m2l_i8_kernel)
+//   finish:  CRT rebuild, Y += alpha 2^(...) S
+I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st,
+                           int64_t *launches);
+int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st);
+int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int beta_b, cudaStream_t st);
+// All three; returns kernel launches.
 int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st);
 
 // The integer gather-GEMM alone (tests): for t < nmod, columns c < ncols, rows r < Ki
 //   R[t][c][r] += sum over slots s with a source of sum_k A[t][s][r][k] * B[t][row(s, c)][k]
-// reduced to balanced residues mod m_t per work unit, where row(s, c) = src - box0 for a
-// source, zero_row otherwise; B has rows_per_mod rows per modulus.
+// reduced mod m_t per work unit (|partial| <= 3 m / 2), where row(s, c) = src - box0 for
+// a source, zero_row otherwise; B has rows_per_mod rows per modulus.
 int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                    const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
                    cudaStream_t st);

@@ -41,10 +41,10 @@ def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
     src[rng.random(src.shape) < 0.3] = -1
     src[1, :256] = -1  # a slot with no source in the first column tile (skipped by the prepass)
     dev = torch.device("cuda", 0)
-    R = torch.zeros((nmod, Ki, ncols), dtype=torch.int32, device=dev)
+    R = torch.zeros((nmod, ncols, Ki), dtype=torch.int32, device=dev)
     pk.i8_gather_gemm(torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), nrows, zero_row,
                       torch.from_numpy(src).to(dev), box0, R)
-    got = R.cpu().numpy().astype(np.int64).transpose(0, 2, 1)  # -> [t][c][r]
+    got = R.cpu().numpy().astype(np.int64)  # [t][c][r]
     ref = host_residue_gemm(A, B, src, box0, zero_row)
     for t, m in enumerate(mods):
         bad = np.count_nonzero((got[t] - ref[t]) % m)

@@ -3,7 +3,6 @@ paths and report rel-L2 against the reference next to each case's tolerance.
 
 Specs (';'-separated):
   dmma              FP64 DMMA everywhere
-  q:BA[,BB]         DMMA on operands rounded to BA / BB-bit grids (PKGPU_M2L_QUANT)
   i8:NM,BA,BB       int8 residue path (NM moduli) on levels >= 2048 boxes (the default)
   i8all:NM,BA,BB    int8 residue path on every level >= 1
 
@@ -29,7 +28,7 @@ def child(spec):
 
     ctx = pk.Context(0)
     kind, _, args = spec.partition(":")
-    if kind == "dmma" or kind == "q":
+    if kind == "dmma":
         ctx.set_m2l("dmma")
     elif kind in ("i8", "i8all"):
         nm, ba, bb = (int(v) for v in args.split(","))
@@ -73,8 +72,6 @@ def main():
              pot=np.fromfile(base + ".pot.f64"))
     for spec in a.specs.split(";"):
         env = dict(os.environ)
-        if spec.startswith("q:"):
-            env["PKGPU_M2L_QUANT"] = spec[2:]
         r = subprocess.run([sys.executable, __file__, "--child", spec], env=env, capture_output=True, text=True)
         print(r.stdout.strip() or (spec + " FAILED: " + r.stderr[-3000:]), flush=True)
 
