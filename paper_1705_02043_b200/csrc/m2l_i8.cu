@@ -246,6 +246,225 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256): the pair shares one
+// 256-column tile (CTA r gathers boxes [256 p + 128 r, +128)) and one operator row tile,
+// each CTA staging HALF of the operator tile (Nt / 2 rows): per CTA and stage 16 KB
+// gathered + Nt/2 x 128 B operator instead of 16 KB + Nt x 128 B, i.e. a third less L2
+// traffic per MAC, and six stages instead of four.
+//   leader (rank 0) MMA thread: waits its "full" (own 64 cp.async + own TMA + one relay
+//     arrival from the peer), issues cta_group::2 MMAs, commits "empty" / "tfull" to both
+//     CTAs (multicast); waits "tempty" (4 local + 4 remote epilogue arrivals).
+//   peer (rank 1) MMA-warp thread: relay -- waits its local "full" (its cp.async + TMA),
+//     fences the generic-proxy writes into the async proxy, arrives on the leader's "full".
+// TMEM: both CTAs allocate 512 columns (cta_group::2); each CTA's epilogue reads its own
+// 128 lanes (its boxes) of the accumulator.
+constexpr int PAIR_NST = 6;
+constexpr int PAIR_B_BYTES = 128 * BKI; // half operator tile, Nt / 2 <= 128 rows
+constexpr int PAIR_STAGE = A_BYTES + PAIR_B_BYTES;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(tma::smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    m2l_i8_pair_kernel(const __grid_constant__ Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int *s_epi = reinterpret_cast<int *>(smem + PAIR_NST * PAIR_STAGE); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t full[PAIR_NST], empty[PAIR_NST], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    constexpr int NPT = NPROD * 32;
+    const int half = p.Nt / 2;
+    if (tid == 0) {
+        for (int s = 0; s < PAIR_NST; s++) {
+            // leader's "full": one arrival per producer warp of both CTAs + the expect_tx
+            // arrival (tx = both halves of the operator tile, each CTA's TMA signals it)
+            tma::mbar_init(&full[s], 2 * NPROD + 1);
+            tma::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            tma::mbar_init(&tfull[b], 1);
+            tma::mbar_init(&tempty[b], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    const int npairs = p.coltiles / 2;
+    const int units = p.total_units; // (t, chunk, pair, rt)
+    for (int u = blockIdx.x / 2; u < units; u += gridDim.x / 2) {
+        int v = u;
+        const int rt = v % p.rowtiles;
+        v /= p.rowtiles;
+        const int pr = v % npairs;
+        v /= npairs;
+        const int chunk = v % p.nchunk;
+        const int t = v / p.nchunk;
+        const int nact = p.tile_nact[pr];
+        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        const int n = (s1 - s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + pr * MAX_SLOTS;
+        const int col0 = pr * 2 * TBM + (int)rank * TBM; // this CTA's 128 boxes
+        if (warp < NPROD) {
+            // ---------------- producers (both CTAs) ----------------
+            // cp.async groups per stage; a stage is published (proxy fence + one arrival per
+            // warp on the LEADER's "full") once this thread's copies of it have landed,
+            // PAIR_LAG stages behind the issue front
+            constexpr int PAIR_LAG = 2;
+            const int c = lane & 7, j0 = tid >> 3;
+            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
+            auto publish = [&](int gs) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) remote_arrive(map_to_rank(&full[gs % PAIR_NST], 0));
+            };
+            for (int si = s0; si < s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + col0;
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int b = srow[j0 + 8 * i];
+                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
+                }
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int i_unit = (si - s0) * p.KC + kc, gi = g + i_unit, st = gi % PAIR_NST;
+                    tma::mbar_wait(&empty[st], ((gi / PAIR_NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * PAIR_STAGE;
+                    if (tid == 0) {
+                        const uint32_t bar = map_to_rank(&full[st], 0);
+                        if (leader)
+                            asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::
+                                             "r"(bar),
+                                         "r"(p.Nt * BKI)
+                                         : "memory");
+                        asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+                                     "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tma::smem_u32(as + A_BYTES)),
+                                     "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
+                                     "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + slot), "r"(bar)
+                                     : "memory");
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 8 * i;
+                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                    if (i_unit >= PAIR_LAG) {
+                        asm volatile("cp.async.wait_group %0;\n" ::"n"(PAIR_LAG) : "memory");
+                        publish(gi - PAIR_LAG);
+                    }
+                }
+            }
+            // drain: publish the unit's last stages
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            for (int i_unit = max(0, n - PAIR_LAG); i_unit < n; i_unit++) publish(g + i_unit);
+        } else if (warp == MMA_WARP) {
+            if (lane == 0) {
+                if (leader) {
+                    // ---------------- MMA issuer (leader) ----------------
+                    const int buf = jb & 1;
+                    tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t dt = tmem + buf * 256;
+                    for (int i = 0; i < n; i++) {
+                        const int gi = g + i, st = gi % PAIR_NST;
+                        tma::mbar_wait(&full[st], (gi / PAIR_NST) & 1);
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        tc_fence_after();
+                        const uint32_t a0 = tma::smem_u32(smem + st * PAIR_STAGE);
+                        const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < BKI / 32; kk++)
+                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                         "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
+                                         "r"((i > 0 || kk > 0) ? 1u : 0u));
+                        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                                     "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&empty[st])),
+                                     "h"((uint16_t)3)
+                                     : "memory");
+                    }
+                    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                                 "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&tfull[buf])),
+                                 "h"((uint16_t)3)
+                                 : "memory");
+                }
+            }
+            __syncwarp();
+        } else {
+            // ---------------- epilogue (both CTAs: own 128 lanes = own boxes) ----------------
+            const int buf = jb & 1, q = warp & 3;
+            int *tile = s_epi + (warp - MMA_WARP - 1) * 32 * EPI_PITCH;
+            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
+            tc_fence_after();
+            const int m = c_mod[t];
+            const float inv = 1.0f / (float)m;
+            const int cw = col0 + q * 32;
+            const int r0 = rt * p.Nt;
+            const int nr = min(p.Nt, p.Ki - r0);
+            int *Rt = p.R + ((int64_t)t * p.ncols + cw) * p.Ki + r0;
+            for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                uint32_t vv[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, vv);
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const int a = (int)vv[j];
+                    tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
+                }
+                __syncwarp();
+                const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                for (int b = 0; b < 32; b++) {
+                    const int r = tile[b * EPI_PITCH + lane];
+                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) remote_arrive(map_to_rank(&tempty[buf], 0));
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
 // active slots per column tile of `bn` columns, in slot order
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
                                  int *tile_nact) {
@@ -468,14 +687,33 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
     PK_CUDA(cudaGetLastError());
 }
 
-int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
-                   const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
-                   cudaStream_t st) {
-    if (ncols == 0 || nslots == 0) return 0;
-    if (ncols % kI8Tile != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
-        throw RuntimeError("i8_gather_gemm: bad shape");
-    upload_tables();
+namespace {
+
+// PKGPU_I8_PAIR=1 selects the CTA-pair kernel (exact, currently slower: DESIGN.md §4)
+bool use_pair() {
+    static const bool v = [] {
+        const char *e = std::getenv("PKGPU_I8_PAIR");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return v;
+}
+int column_tile() { return use_pair() ? 2 * TBM : TBM; }
+
+// active-slot lists per column tile (ncols / column_tile() tiles)
+void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, Workspace &ws, cudaStream_t st, int **tslots,
+                int **tnact) {
+    const int bn = column_tile(), tiles = ncols / bn;
+    *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
+    *tnact = ws.get<int>("i8_tile_nact", tiles);
+    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact);
+    PK_CUDA(cudaGetLastError());
+}
+
+void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
+                 const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
+                 const int *tnact, cudaStream_t st) {
     const int num_sms = sm_count();
+    const bool pair = use_pair();
     Params p;
     std::memset(&p, 0, sizeof p);
     p.X = B;
@@ -495,36 +733,61 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     p.Ki = Ki;
     p.R = R;
     // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
-    // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
-    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
+    // both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the CTA pair)
+    const int M = pair ? 2 * TBM : TBM;
+    p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
     int nchunk = (int)((nslots + cmax - 1) / cmax);
-    const int64_t base = (int64_t)nmod * p.rowtiles * p.coltiles;
-    while (base * nchunk < 3LL * num_sms && nchunk * 16 < nslots) nchunk++;
+    const int64_t base = (int64_t)nmod * p.rowtiles * (pair ? p.coltiles / 2 : p.coltiles);
+    const int64_t resident = pair ? num_sms / 2 : num_sms;
+    while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
-    int *tslots = ws.get<int>("i8_tile_slots", (size_t)p.coltiles * MAX_SLOTS);
-    int *tnact = ws.get<int>("i8_tile_nact", p.coltiles);
-    slot_scan_kernel<<<p.coltiles, 256, 0, st>>>(src, ld_src, nslots, TBM, tslots, tnact);
     p.tile_slots = tslots;
     p.tile_nact = tnact;
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
-    const cuuint32_t box[3] = {BKI, (cuuint32_t)p.Nt, 1};
+    const cuuint32_t box[3] = {BKI, (cuuint32_t)(pair ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
-    const size_t smem = (size_t)NST * STAGE_BYTES + 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    static bool cfg = false;
-    if (!cfg) {
-        PK_CUDA(cudaFuncSetAttribute(m2l_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cfg = true;
+    const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
+    if (pair) {
+        const size_t smem = (size_t)PAIR_NST * PAIR_STAGE + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
+        m2l_i8_pair_kernel<<<grid, NTHREADS, smem, st>>>(p);
+    } else {
+        const size_t smem = (size_t)NST * STAGE_BYTES + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
+        m2l_i8_kernel<<<grid, NTHREADS, smem, st>>>(p);
     }
-    const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
-    m2l_i8_kernel<<<grid, NTHREADS, smem, st>>>(p);
     PK_CUDA(cudaGetLastError());
+}
+
+} // namespace
+
+int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
+                   const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, Workspace &ws,
+                   cudaStream_t st) {
+    if (ncols == 0 || nslots == 0) return 0;
+    if (ncols % kI8Tile != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
+        throw RuntimeError("i8_gather_gemm: bad shape");
+    upload_tables();
+    int *tslots = nullptr, *tnact = nullptr;
+    scan_tiles(src, ld_src, nslots, ncols, ws, st, &tslots, &tnact);
+    launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact, st);
     return 2;
 }
 
@@ -543,15 +806,19 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
     w.xres = xres;
     w.R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
+    upload_tables();
+    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, ws, st, &w.tile_slots, &w.tile_nact);
     PK_CUDA(cudaGetLastError());
-    if (launches) *launches += 2;
+    if (launches) *launches += 3;
     return w;
 }
 
 int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st) {
+    (void)ws;
     if (a.ncols == 0) return 0;
-    return i8_gather_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)a.nbox, o.Ki, o.nmod, a.src, a.ld_src, a.box0,
-                          a.nslots, a.ncols, w.R, ws, st);
+    launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)a.nbox, o.Ki, o.nmod, a.src, a.ld_src, a.box0, a.nslots,
+                a.ncols, w.R, w.tile_slots, w.tile_nact, st);
+    return 1;
 }
 
 int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int beta_b, cudaStream_t st) {

@@ -57,6 +57,7 @@ struct I8LevelWork {
     int *R = nullptr;                 // [nmod][ncols][Ki] residue sums
     unsigned long long *mx = nullptr; // level max |phi| (bit pattern)
     int64_t rows = 0;
+    int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile
 };
 // The three steps of one level (separately timed by the stage profiler):
 //   prepare: level max, density residues, R = 0
