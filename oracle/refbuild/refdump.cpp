@@ -315,6 +315,27 @@ int cmd_eval(const std::map<std::string, std::string> &a) {
     return 0;
 }
 
+// truth: the reference's own ground-truth evaluator (pairwise Ewald / direct sums,
+// oracle_system_eval, include/pkifmm/refsum.hpp:88) at a stride sample of `ntrg` source
+// points (index i * (N / ntrg)), for the SURVEY §8(c)(iii) accuracy check
+int cmd_truth(const std::map<std::string, std::string> &a) {
+    set_threads(a);
+    const KernelSpec kernel = KernelSpec::from_name(get(a, "kernel", "laplace"));
+    const auto src = to_vec3(read_f64(get(a, "src", "__required__")));
+    const auto str = read_f64(get(a, "str", "__required__"));
+    const PeriodicSetup setup = make_setup(a);
+    const int ntrg = std::stoi(get(a, "ntrg", "64"));
+    const size_t stride = std::max<size_t>(1, src.size() / ntrg);
+    std::vector<Vec3> trg;
+    for (int i = 0; i < ntrg && i * stride < src.size(); i++) trg.push_back(src[i * stride]);
+    const double t0 = now();
+    const auto spec = make_periodic_spec(kernel, setup);
+    const auto q = oracle_system_eval(spec, src, str, trg);
+    write_bin(get(a, "out", "__required__") + ".truth.f64", q);
+    std::cout << json{{"ntrg", trg.size()}, {"stride", stride}, {"seconds", now() - t0}}.dump() << "\n";
+    return 0;
+}
+
 // ---------------------------------------------------------------------------
 // operators: SVD factors and periodizing operator
 void dump_factors(const SvdFactors &f, const std::string &out) {
@@ -455,6 +476,7 @@ int main(int argc, char **argv) {
         if (cmd == "pairs") return cmd_pairs(a);
         if (cmd == "kblock") return cmd_kblock(a);
         if (cmd == "surface") return cmd_surface(a);
+        if (cmd == "truth") return cmd_truth(a);
         std::cerr << "unknown command " << cmd << "\n";
         return 1;
     } catch (const ConfigError &e) {

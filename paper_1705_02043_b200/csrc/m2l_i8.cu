@@ -38,6 +38,7 @@ constexpr int A_BYTES = TBM * BKI;  // gathered tile
 constexpr int B_BYTES = 256 * BKI;  // operator tile, Nt <= 256 rows
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NST = 4;
+constexpr int NST_MAX = 8;
 constexpr int NPROD = 2; // producer warps
 constexpr int MMA_WARP = NPROD;
 constexpr int NTHREADS = (NPROD + 1 + 4) * 32;
@@ -60,6 +61,11 @@ struct Params {
     const int *tile_slots, *tile_nact;
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
+    int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
+               // loads, 4 no epilogue atomics, 8 no MMA proxy fence
+    int nst, stage_bytes; // single-CTA kernel: stage ring depth and stride
+    int epi_transpose;    // epilogue atomics through a shared-memory transpose (coalesced)
+    int prefetch;         // stages of L2 prefetch ahead for the operator tiles (0: off)
     int *R; // [nmod][ncols][Ki]
 };
 
@@ -111,13 +117,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    int *s_epi = reinterpret_cast<int *>(smem + NST * STAGE_BYTES); // [4 warps][32][33]
-    __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[2];
+    // stage ring: p.nst stages of p.stage_bytes (16 KB gathered rows + the operator tile)
+    const int NS = p.nst, SB = p.stage_bytes;
+    int *s_epi = reinterpret_cast<int *>(smem + NS * SB); // [4 warps][32][33] when transposing
+    __shared__ __align__(8) uint64_t full[NST_MAX], empty[NST_MAX], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int NPT = NPROD * 32;
     if (tid == 0) {
-        for (int s = 0; s < NST; s++) {
+        for (int s = 0; s < NS; s++) {
             tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
             tma::mbar_init(&empty[s], 1);
         }
@@ -160,17 +168,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                     off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
                 }
                 for (int kc = 0; kc < p.KC; kc++) {
-                    const int gi = g + (si - x.s0) * p.KC + kc, st = gi % NST;
-                    tma::mbar_wait(&empty[st], ((gi / NST) & 1) ^ 1);
-                    unsigned char *as = smem + st * STAGE_BYTES;
+                    const int gi = g + (si - x.s0) * p.KC + kc, st = gi % NS;
+                    tma::mbar_wait(&empty[st], ((gi / NS) & 1) ^ 1);
+                    unsigned char *as = smem + st * SB;
                     if (tid == 0) {
-                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot, &full[st]);
+                        if (p.debug & 2) { // timing experiment: no operator loads
+                            tma::mbar_arrive(&full[st]);
+                        } else {
+                            const int mat = (p.debug & 16) ? 0 : slot; // 16: one L2-resident operator
+                            tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                            tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + mat,
+                                             &full[st]);
+                            // L2 prefetch of the operator tile p.prefetch stages ahead (same unit):
+                            // takes the DRAM latency of the operator stream off the smem ring
+                            if (p.prefetch > 0) {
+                                const int ia = (si - x.s0) * p.KC + kc + p.prefetch;
+                                const int sa = x.s0 + ia / p.KC, ka = ia % p.KC;
+                                if (sa < x.s1) {
+                                    const int ma = (p.debug & 16) ? 0 : slots[sa];
+                                    asm volatile(
+                                        "cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
+                                            reinterpret_cast<uint64_t>(&p.tmB)),
+                                        "r"(ka * BKI), "r"(x.rt * p.Nt), "r"(x.t * p.nmat + ma)
+                                        : "memory");
+                                }
+                            }
+                        }
                     }
+                    if (!(p.debug & 1)) { // (bit 0: timing experiment without the gather)
 #pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int j = j0 + 8 * i;
-                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                        for (int i = 0; i < 16; i++) {
+                            const int j = j0 + 8 * i;
+                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                        }
                     }
                     tma::cp_async_mbar_arrive(&full[st]);
                 }
@@ -183,12 +213,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                 tc_fence_after();
                 const uint32_t dt = tmem + buf * 256;
                 for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % NST;
-                    tma::mbar_wait(&full[st], (gi / NST) & 1);
+                    const int gi = g + i, st = gi % NS;
+                    tma::mbar_wait(&full[st], (gi / NS) & 1);
                     // the gathered rows were written by cp.async through the generic proxy
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    if (!(p.debug & 8)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * STAGE_BYTES);
+                    const uint32_t a0 = tma::smem_u32(smem + st * SB);
                     const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < BKI / 32; kk++) // K = 32 bytes per MMA: +2 in the 16-byte start field
@@ -216,6 +246,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
             for (int j0 = 0; j0 < p.Nt; j0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, v);
+                if (!p.epi_transpose) {
+                    // direct: thread = box, 32 consecutive rows (one 128-byte line per thread)
+                    int *Rb = Rt + (int64_t)lane * p.Ki + j0;
+#pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        const int a = (int)v[j];
+                        const int r = a - __float2int_rn((float)a * inv) * m;
+                        if (r && j0 + j < nr && !(p.debug & 4)) atomicAdd(Rb + j, r);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     // |a| < 2^31: float quotient is off by at most one; r in (-3m/2, 3m/2)
@@ -227,7 +268,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
 #pragma unroll 8
                 for (int b = 0; b < 32; b++) {
                     const int r = tile[b * EPI_PITCH + lane]; // box col0 + b, row r0 + j0 + lane
-                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    if (ok && r && !(p.debug & 4)) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
                 }
                 __syncwarp();
             }
@@ -465,6 +506,332 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multicast pair (cluster of 2, cta_group::1 MMAs): each CTA computes its own 128 boxes with
+// its own TMEM, like m2l_i8_kernel, but the two CTAs walk the same (modulus, operator row
+// tile, slot) sequence and each TMA-loads HALF of the operator tile with .multicast::cluster
+// into both CTAs' shared memory -- the operator tile is read from L2 once per pair. A stage
+// is refilled only when both CTAs' MMAs are done with it: each MMA thread commits "empty"
+// to both CTAs (multicast commit, count 2). No cross-CTA software arrivals or fences.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    m2l_i8_mc_kernel(const __grid_constant__ Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int *s_epi = reinterpret_cast<int *>(smem + NST * STAGE_BYTES); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    constexpr int NPT = NPROD * 32;
+    const int half = p.Nt / 2;
+    if (tid == 0) {
+        for (int s = 0; s < NST; s++) {
+            tma::mbar_init(&full[s], NPT + 1); // local cp.async + local expect_tx (both halves' bytes)
+            tma::mbar_init(&empty[s], 2);      // both CTAs' MMA commits
+        }
+        for (int b = 0; b < 2; b++) {
+            tma::mbar_init(&tfull[b], 1);
+            tma::mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    const int npairs = p.coltiles / 2;
+    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
+        int v = u;
+        const int rt = v % p.rowtiles;
+        v /= p.rowtiles;
+        const int pr = v % npairs;
+        v /= npairs;
+        const int chunk = v % p.nchunk;
+        const int t = v / p.nchunk;
+        const int nact = p.tile_nact[pr];
+        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        const int n = (s1 - s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + pr * MAX_SLOTS;
+        const int col0 = pr * 2 * TBM + (int)rank * TBM; // this CTA's 128 boxes
+        if (warp < NPROD) {
+            // ---------------- producers ----------------
+            const int c = lane & 7, j0 = tid >> 3;
+            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
+            for (int si = s0; si < s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + col0;
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int b = srow[j0 + 8 * i];
+                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
+                }
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int gi = g + (si - s0) * p.KC + kc, st = gi % NST;
+                    tma::mbar_wait(&empty[st], ((gi / NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * STAGE_BYTES;
+                    if (tid == 0) {
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+                            "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
+                                tma::smem_u32(as + A_BYTES + (int)rank * half * BKI)),
+                            "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI), "r"(rt * p.Nt + (int)rank * half),
+                            "r"(t * p.nmat + slot), "r"(tma::smem_u32(&full[st])), "h"((uint16_t)3)
+                            : "memory");
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 8 * i;
+                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    tma::cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        } else if (warp == MMA_WARP) {
+            // ---------------- MMA issuer (each CTA) ----------------
+            if (lane == 0) {
+                const int buf = jb & 1;
+                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dt = tmem + buf * 256;
+                for (int i = 0; i < n; i++) {
+                    const int gi = g + i, st = gi % NST;
+                    tma::mbar_wait(&full[st], (gi / NST) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tc_fence_after();
+                    const uint32_t a0 = tma::smem_u32(smem + st * STAGE_BYTES);
+                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BKI / 32; kk++)
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
+                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
+                                 "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&empty[st])),
+                                 "h"((uint16_t)3)
+                                 : "memory");
+                }
+                umma_commit(&tfull[buf]);
+            }
+            __syncwarp();
+        } else {
+            // ---------------- epilogue ----------------
+            const int buf = jb & 1, q = warp & 3;
+            int *tile = s_epi + (warp - MMA_WARP - 1) * 32 * EPI_PITCH;
+            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
+            tc_fence_after();
+            const int m = c_mod[t];
+            const float inv = 1.0f / (float)m;
+            const int cw = col0 + q * 32;
+            const int r0 = rt * p.Nt;
+            const int nr = min(p.Nt, p.Ki - r0);
+            int *Rt = p.R + ((int64_t)t * p.ncols + cw) * p.Ki + r0;
+            for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                uint32_t vv[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, vv);
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const int a = (int)vv[j];
+                    tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
+                }
+                __syncwarp();
+                const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                for (int b = 0; b < 32; b++) {
+                    const int r = tile[b * EPI_PITCH + lane];
+                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&tempty[buf]);
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Dual-tile variant (one CTA per SM): a unit covers TWO 128-box column tiles (a 256-column
+// pair tile with one slot list) and one operator row tile. Per stage: 2 x 16 KB gathered
+// rows (four producer warps) + one Nt x 128 B operator tile, consumed by two M128 x Nt MMAs
+// (one per column tile, two TMEM accumulators at columns 0 and 256). Bytes per MAC drop
+// from (128 + Nt) / (128 Nt) to (256 + Nt) / (256 Nt): 60 KB per 2 x 3.7 M MACs at Nt =
+// 224, which the per-SM L2 ingest (~69 B/clk measured) sustains at the MMA rate. The
+// accumulators fill TMEM, so the epilogue of a unit is not overlapped with the next.
+constexpr int DUAL_NPROD = 4;
+constexpr int DUAL_MMA_WARP = DUAL_NPROD;
+constexpr int DUAL_THREADS = (DUAL_NPROD + 1 + 4) * 32;
+constexpr int DUAL_A_BYTES = 2 * A_BYTES;
+constexpr int DUAL_STAGE = DUAL_A_BYTES + B_BYTES;
+constexpr int DUAL_NST = 3;
+
+__global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __grid_constant__ Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int *s_epi = reinterpret_cast<int *>(smem + DUAL_NST * DUAL_STAGE); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t full[DUAL_NST], empty[DUAL_NST], tfull, tempty;
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NPT = DUAL_NPROD * 32;
+    if (tid == 0) {
+        for (int s = 0; s < DUAL_NST; s++) {
+            tma::mbar_init(&full[s], NPT + 1);
+            tma::mbar_init(&empty[s], 1);
+        }
+        tma::mbar_init(&tfull, 1);
+        tma::mbar_init(&tempty, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == DUAL_MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    const int npairs = p.coltiles / 2;
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+        int v = u;
+        const int rt = v % p.rowtiles;
+        v /= p.rowtiles;
+        const int pr = v % npairs;
+        v /= npairs;
+        const int chunk = v % p.nchunk;
+        const int t = v / p.nchunk;
+        const int nact = p.tile_nact[pr];
+        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        const int n = (s1 - s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + pr * MAX_SLOTS;
+        const int colp = pr * 2 * TBM; // first of the 256 columns
+        if (warp < DUAL_NPROD) {
+            // ---------------- producers: 256 rows, 16 cp.async of 16 B per thread ----------------
+            const int c = lane & 7, j0 = tid >> 3; // rows j0 + 16 i, i < 16
+            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
+            for (int si = s0; si < s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + colp;
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int b = srow[j0 + 16 * i];
+                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
+                }
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int gi = g + (si - s0) * p.KC + kc, st = gi % DUAL_NST;
+                    tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * DUAL_STAGE;
+                    if (tid == 0) {
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot, &full[st]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
+                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    tma::cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        } else if (warp == DUAL_MMA_WARP) {
+            // ---------------- MMA issuer: two M128 x Nt MMAs per k-step ----------------
+            if (lane == 0) {
+                tma::mbar_wait(&tempty, (jb & 1) ^ 1);
+                tc_fence_after();
+                for (int i = 0; i < n; i++) {
+                    const int gi = g + i, st = gi % DUAL_NST;
+                    tma::mbar_wait(&full[st], (gi / DUAL_NST) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tc_fence_after();
+                    const uint32_t a0 = tma::smem_u32(smem + st * DUAL_STAGE);
+                    const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES),
+                                   bd = sw128_desc(a0 + DUAL_A_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BKI / 32; kk++) {
+                        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                                     "l"(ad0 + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"(acc));
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 256),
+                                     "l"(ad1 + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"(acc));
+                    }
+                    umma_commit(&empty[st]);
+                }
+                umma_commit(&tfull);
+            }
+            __syncwarp();
+        } else {
+            // ---------------- epilogue: both accumulators ----------------
+            const int q = warp & 3;
+            int *tile = s_epi + (warp - DUAL_MMA_WARP - 1) * 32 * EPI_PITCH;
+            tma::mbar_wait(&tfull, jb & 1);
+            tc_fence_after();
+            const int m = c_mod[t];
+            const float inv = 1.0f / (float)m;
+            const int r0 = rt * p.Nt;
+            const int nr = min(p.Nt, p.Ki - r0);
+            for (int h = 0; h < 2; h++) {
+                int *Rt = p.R + ((int64_t)t * p.ncols + colp + h * TBM + q * 32) * p.Ki + r0;
+                for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                    uint32_t vv[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + j0, vv);
+#pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        const int a = (int)vv[j];
+                        tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
+                    }
+                    __syncwarp();
+                    const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                    for (int b = 0; b < 32; b++) {
+                        const int r = tile[b * EPI_PITCH + lane];
+                        if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    }
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&tempty);
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == DUAL_MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
 // active slots per column tile of `bn` columns, in slot order
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
                                  int *tile_nact) {
@@ -555,15 +922,27 @@ __device__ __forceinline__ int level_exp(const unsigned long long *mx) {
     return m > 0 ? ilogb(m) + 1 : 0;
 }
 
-// Xres[t][i][k] for boxes i < nbox (row nbox: zeros)
+// level of an index in a run of ranges start[0] <= ... < start[n]
+__device__ __forceinline__ int level_of(const int64_t *start, int n, int64_t i) {
+    int l = 0;
+    while (l + 1 < n && i >= start[l + 1]) l++;
+    return l;
+}
+
+// Xres[t][i][k] for boxes i < nbox of the run (row nbox: zeros), scaled by the box's level
 __global__ void x_residue_kernel(const double *__restrict__ X, int64_t nbox, int K, int Kp, int Ki, int nmod,
-                                 int beta, const unsigned long long *__restrict__ mx, int8_t *__restrict__ res) {
-    const int e = level_exp(mx);
+                                 int beta, const unsigned long long *__restrict__ mx, I8Levels lv,
+                                 int8_t *__restrict__ res) {
     const int64_t rows = nbox + 1, n = rows * Ki, stride = rows * Ki;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / Ki;
         const int k = (int)(i % Ki);
-        const double x = (b < nbox && k < K) ? X[b * Kp + k] : 0.0;
+        double x = 0.0;
+        int e = 0;
+        if (b < nbox && k < K) {
+            x = X[b * Kp + k];
+            e = level_exp(mx + level_of(lv.box0, lv.n, lv.box0[0] + b));
+        }
         residues(llrint(ldexp(x, beta - e)), nmod, res + i, stride);
     }
 }
@@ -573,15 +952,17 @@ __global__ void x_residue_kernel(const double *__restrict__ X, int64_t nbox, int
 template <int NM>
 __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki, int K, int Kp,
                                    const int *__restrict__ out_box, const int *__restrict__ rowexp,
-                                   const unsigned long long *__restrict__ mx, int beta_sum, double alpha,
+                                   const unsigned long long *__restrict__ mx, int beta_sum, I8Levels lv,
                                    double *__restrict__ Y) {
     const int64_t n = (int64_t)ncols * Ki;
-    const int E = level_exp(mx);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int c = (int)(i / Ki), r = (int)(i % Ki);
         if (r >= K) continue;
         const int ob = out_box[c];
         if (ob < 0) continue;
+        const int l = level_of(lv.col0, lv.n, c);
+        const int E = level_exp(mx + l);
+        const double alpha = lv.alpha[l];
         int x[NM], acc[NM], v[NM];
 #pragma unroll
         for (int t = 0; t < NM; t++) {
@@ -689,14 +1070,17 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
 
 namespace {
 
-// PKGPU_I8_PAIR=1 selects the CTA-pair kernel (exact, currently slower: DESIGN.md §4)
-bool use_pair() {
-    static const bool v = [] {
+// kernel variant, PKGPU_I8_PAIR: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
+// (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
+// (m2l_i8_dual_kernel); see DESIGN.md §4
+int pair_mode() {
+    static const int v = [] {
         const char *e = std::getenv("PKGPU_I8_PAIR");
-        return e && std::strcmp(e, "1") == 0;
+        return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
     }();
     return v;
 }
+bool use_pair() { return pair_mode() != 0; }
 int column_tile() { return use_pair() ? 2 * TBM : TBM; }
 
 // active-slot lists per column tile (ncols / column_tile() tiles)
@@ -734,12 +1118,16 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.R = R;
     // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
     // both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the CTA pair)
-    const int M = pair ? 2 * TBM : TBM;
+    const int M = pair_mode() == 1 ? 2 * TBM : TBM;
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    static const int debug = std::getenv("PKGPU_I8_DEBUG") ? std::atoi(std::getenv("PKGPU_I8_DEBUG")) : 0;
+    p.debug = debug;
     const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
     int nchunk = (int)((nslots + cmax - 1) / cmax);
+    static const int min_chunks = std::getenv("PKGPU_I8_CHUNKS") ? std::atoi(std::getenv("PKGPU_I8_CHUNKS")) : 0;
+    nchunk = std::max(nchunk, min_chunks);
     const int64_t base = (int64_t)nmod * p.rowtiles * (pair ? p.coltiles / 2 : p.coltiles);
-    const int64_t resident = pair ? num_sms / 2 : num_sms;
+    const int64_t resident = (pair_mode() == 1 || pair_mode() == 2) ? num_sms / 2 : num_sms;
     while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
@@ -747,14 +1135,34 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.tile_nact = tnact;
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
-    const cuuint32_t box[3] = {BKI, (cuuint32_t)(pair ? p.Nt / 2 : p.Nt), 1};
+    // the CTA-pair variants stage half of the operator tile per CTA
+    const bool half_tile = pair_mode() == 1 || pair_mode() == 2;
+    const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    if (pair) {
+    if (pair_mode() == 3) {
+        const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
+        m2l_i8_dual_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
+    } else if (pair_mode() == 2) {
+        const size_t smem = (size_t)NST * STAGE_BYTES + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
+        m2l_i8_mc_kernel<<<grid, NTHREADS, smem, st>>>(p);
+    } else if (pair) {
         const size_t smem = (size_t)PAIR_NST * PAIR_STAGE + epi;
         static bool cfg = false;
         if (!cfg) {
@@ -764,11 +1172,24 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
         m2l_i8_pair_kernel<<<grid, NTHREADS, smem, st>>>(p);
     } else {
-        const size_t smem = (size_t)NST * STAGE_BYTES + epi;
-        static bool cfg = false;
-        if (!cfg) {
+        // stage = 16 KB gathered rows + the operator tile rounded to 1 KB; as many stages as
+        // the 227 KB of shared memory allow (the transposing epilogue costs 16.5 KB)
+        static const bool transpose = [] {
+            const char *e = std::getenv("PKGPU_I8_EPI");
+            return !(e && std::strcmp(e, "direct") == 0);
+        }();
+        p.epi_transpose = transpose ? 1 : 0;
+        static const int prefetch = std::getenv("PKGPU_I8_PREFETCH") ? std::atoi(std::getenv("PKGPU_I8_PREFETCH")) : 0;
+        p.prefetch = prefetch;
+        p.stage_bytes = A_BYTES + (p.Nt * BKI + 1023) / 1024 * 1024;
+        const size_t epi_bytes = transpose ? 4 * 32 * EPI_PITCH * sizeof(int) : 0;
+        const size_t avail = 227 * 1024 - 1024 - 512 - epi_bytes;
+        p.nst = (int)std::min<size_t>(NST_MAX, avail / p.stage_bytes);
+        const size_t smem = (size_t)p.nst * p.stage_bytes + epi_bytes + 1024;
+        static size_t cfg = 0;
+        if (cfg < smem) {
             PK_CUDA(cudaFuncSetAttribute(m2l_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
+            cfg = smem;
         }
         const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
         m2l_i8_kernel<<<grid, NTHREADS, smem, st>>>(p);
@@ -795,29 +1216,36 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
                            int64_t *launches) {
     I8LevelWork w;
     if (a.ncols == 0) return w;
+    if (a.lv.n < 1 || a.lv.n > kI8MaxLevels) throw RuntimeError("m2l_i8: bad level run");
     const int nmod = o.nmod, Ki = o.Ki;
-    w.rows = a.nbox + 1;
-    w.mx = ws.get<unsigned long long>("i8_level_max", 1);
-    PK_CUDA(cudaMemsetAsync(w.mx, 0, sizeof(unsigned long long), st));
-    level_absmax_kernel<<<296, 256, 0, st>>>(a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, w.mx);
+    const int64_t box0 = a.lv.box0[0], nbox = a.lv.box0[a.lv.n] - box0;
+    w.rows = nbox + 1;
+    w.mx = ws.get<unsigned long long>("i8_level_max", kI8MaxLevels);
+    PK_CUDA(cudaMemsetAsync(w.mx, 0, kI8MaxLevels * sizeof(unsigned long long), st));
+    for (int l = 0; l < a.lv.n; l++) {
+        const int64_t nb = a.lv.box0[l + 1] - a.lv.box0[l];
+        if (nb > 0)
+            level_absmax_kernel<<<(unsigned)std::min<int64_t>((nb * a.Kp + 255) / 256, 296), 256, 0, st>>>(
+                a.X + a.lv.box0[l] * a.Kp, nb, a.K, a.Kp, w.mx + l);
+    }
     int8_t *xres = ws.get<int8_t>("i8_xres", (size_t)nmod * w.rows * Ki);
     x_residue_kernel<<<(unsigned)std::min<int64_t>((w.rows * Ki + 255) / 256, 148 * 16), 256, 0, st>>>(
-        a.X + a.box0 * a.Kp, a.nbox, a.K, a.Kp, Ki, nmod, beta_b, w.mx, xres);
+        a.X + box0 * a.Kp, nbox, a.K, a.Kp, Ki, nmod, beta_b, w.mx, a.lv, xres);
     w.xres = xres;
     w.R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
     upload_tables();
     scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, ws, st, &w.tile_slots, &w.tile_nact);
     PK_CUDA(cudaGetLastError());
-    if (launches) *launches += 3;
+    if (launches) *launches += 2 + a.lv.n;
     return w;
 }
 
 int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st) {
     (void)ws;
     if (a.ncols == 0) return 0;
-    launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)a.nbox, o.Ki, o.nmod, a.src, a.ld_src, a.box0, a.nslots,
-                a.ncols, w.R, w.tile_slots, w.tile_nact, st);
+    launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src, a.ld_src, a.lv.box0[0],
+                a.nslots, a.ncols, w.R, w.tile_slots, w.tile_nact, st);
     return 1;
 }
 
@@ -830,7 +1258,7 @@ int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork 
 #define PK_RC(NM)                                                                                                      \
     case NM:                                                                                                           \
         reconstruct_kernel<NM><<<grid, 256, 0, st>>>(w.R, a.ncols, o.Ki, a.K, a.Kp, a.out_box, o.rowexp, w.mx, bs,     \
-                                                     a.alpha, a.Y);                                                    \
+                                                     a.lv, a.Y);                                                       \
         break;
         PK_RC(14) PK_RC(15) PK_RC(16) PK_RC(17) PK_RC(18) PK_RC(19) PK_RC(20)
 #undef PK_RC

@@ -40,22 +40,34 @@ const I8Settings &i8_settings();
 void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat, int K, int Kp, int nmod,
                         int beta_a, cudaStream_t st);
 
+constexpr int kI8MaxLevels = 16;
+
+// One call covers a run of consecutive levels (M2L needs only phi_up, so every level's
+// M2L can run in one launch before the downward L2L chain): their boxes are contiguous in
+// BFS order and their column ranges contiguous in the layout, each level with its own
+// fixed-point scale E_l and factor 2^l.
+struct I8Levels {
+    int n = 0;
+    int64_t box0[kI8MaxLevels + 1] = {}; // first box of each level; box0[n] = end of the run
+    int64_t col0[kI8MaxLevels + 1] = {}; // first column (relative to the call's columns); col0[n] = ncols
+    double alpha[kI8MaxLevels] = {};     // 2^l
+};
+
 struct I8LevelArgs {
     int K = 0, Kp = 0;
-    int ncols = 0;               // multiple of kI8Tile
+    int ncols = 0;               // multiple of kI8Tile (each level's range too)
     const int *out_box = nullptr; // [ncols] output box per column, -1 padding
     int nslots = 0;
     const int *src = nullptr;     // [nslots * ld_src] global source box ids, -1 none
     int64_t ld_src = 0;
-    int64_t box0 = 0, nbox = 0;   // sources are the level's boxes [box0, box0 + nbox)
+    I8Levels lv;                  // sources of a column are boxes of the column's own level
     const double *X = nullptr;    // [box][Kp]
-    double *Y = nullptr;          // [box][Kp]: Y += alpha * sum_slot M X
-    double alpha = 1.0;
+    double *Y = nullptr;          // [box][Kp]: Y += alpha_l * sum_slot M X
 };
 struct I8LevelWork {
     const int8_t *xres = nullptr;     // [nmod][nbox + 1][Ki] density residues (last row zero)
     int *R = nullptr;                 // [nmod][ncols][Ki] residue sums
-    unsigned long long *mx = nullptr; // level max |phi| (bit pattern)
+    unsigned long long *mx = nullptr; // per-level max |phi| (bit patterns)
     int64_t rows = 0;
     int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile
 };

@@ -144,3 +144,22 @@ def test_direct_mode_and_errors():
     with pytest.raises(O.ConfigError) as e:
         O.evaluate(O.LAPLACE, g["src"], [1.0, 1.0, 1.0, -1.0], g["src"], per=O.SP, p=8, op=op)
     assert str(e.value) == errs["compat"]["what"]
+
+
+@pytest.mark.parametrize("name", ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8"])
+def test_truth_fixtures_match_reference_accuracy(name):
+    """The ground-truth fixtures (tests/golden/make_truth.py: the reference's
+    oracle_system_eval at 64 sampled targets) reproduce the reference's accuracy band of
+    SURVEY §8(c): Laplace SP ~1e-7, Laplace TP ~2e-7 after the constant gauge, Stokes TP
+    ~2e-4 -- i.e. they are the truth the reference itself is measured against."""
+    g = load(f"eval_{name}.npz")
+    t = load(f"truth_{name}.npz")
+    meta = json.loads(str(g["meta"]))
+    kt = 3 if meta["kernel"] == "stokeslet" else 1
+    idx = np.arange(t["truth"].size // kt) * int(t["stride"])
+    d = np.asarray(g["pot"]).reshape(-1, kt)[idx] - t["truth"].reshape(-1, kt)
+    if meta["per"] == "tp":
+        d = d - d.mean(axis=0)
+    err = np.linalg.norm(d) / np.linalg.norm(t["truth"])
+    bound = {"lap_sp_p8": 1e-6, "lap_dp_p6": 1e-4, "lap_tp_p8": 1e-6, "sto_tp_p6": 1e-3, "sto_tp_p8": 1e-3}[name]
+    assert 0 < err <= bound, (name, err)
