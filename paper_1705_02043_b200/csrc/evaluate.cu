@@ -270,6 +270,8 @@ struct Layout {
     std::vector<int64_t> colbase, octbase, m2mbase; // per level (size depth + 2): m2l, oct, m2m layouts
     int wide[kMaxLevels + 1] = {0};                // m2l layout padded to 128-column tiles
     int i8[kMaxLevels + 1] = {0};                  // M2L on the int8 tensor pipe (256-column tiles)
+    int i8_last[kMaxLevels + 1] = {0};             // int8 run starting at this level ends at i8_last
+    int i8_big[kMaxLevels + 1] = {0};              // ... and is one big level (dual-tile kernel)
     int64_t ncols = 0, noct = 0, nm2m = 0;
     int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
     int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
@@ -305,6 +307,17 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
     L.octbase.assign(T.depth + 2, 0);
     int s = 0;
     int64_t co = 0, cm = 0;
+    // int8 runs: consecutive small levels (<= PKGPU_I8_SMALL boxes, default 1024: nearly all
+    // 316 offsets active, few columns, bound by streaming the operator residues) share one
+    // launch and are packed into as few 128-column tiles as possible; a big level runs alone
+    static const int64_t small_max =
+        std::getenv("PKGPU_I8_SMALL") ? std::atoll(std::getenv("PKGPU_I8_SMALL")) : 1024;
+    const I8Settings &is = ctx.i8;
+    auto i8_level = [&](int lv) {
+        return is.enabled && lv >= 1 && lv <= T.depth && T.level_off[lv + 1] - T.level_off[lv] >= is.min_boxes;
+    };
+    auto small_level = [&](int lv) { return T.level_off[lv + 1] - T.level_off[lv] <= small_max; };
+    int run_first = -1; // first level of the int8 run being laid out
     for (int l = 0; l <= T.depth; l++) {
         const int64_t nl = T.level_off[l + 1] - T.level_off[l];
         // octant grouping streams ~189 offsets over padded groups; Morton order streams
@@ -321,6 +334,12 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         static const bool wide_ok = std::getenv("PKGPU_GEMM_WIDE") != nullptr;
         L.wide[l] = wide_ok && grouped[l] && padded128 * 100 <= padded * 103 ? 1 : 0;
         const int padm = L.wide[l] ? 128 : BN;
+        L.i8[l] = i8_level(l) ? 1 : 0;
+        const bool in_run = L.i8[l] && run_first >= 0; // continues the current int8 run
+        if (L.i8[l] && !in_run) run_first = l;
+        // inside an int8 run an ungrouped level is packed (8-column granularity) after the
+        // previous one; grouped levels keep 64-aligned octant groups
+        if (grouped[l] || !L.i8[l]) cm = (cm + BN - 1) / BN * BN;
         L.octbase[l] = co;
         L.colbase[l] = cm;
         mbase[l] = (int)cm;
@@ -333,11 +352,17 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             co += (count[k] + BN - 1) / BN * BN;
             if (grouped[l]) cm += (count[k] + padm - 1) / padm * padm;
         }
-        if (!grouped[l]) cm += (nl + BN - 1) / BN * BN;
-        // int8-pipe levels: the column count is padded to whole 256-column tiles
-        const I8Settings &is = ctx.i8;
-        L.i8[l] = is.enabled && l >= 1 && nl >= is.min_boxes ? 1 : 0;
-        if (L.i8[l]) cm = L.colbase[l] + (cm - L.colbase[l] + kI8Tile - 1) / kI8Tile * kI8Tile;
+        if (!grouped[l]) cm += L.i8[l] ? (nl + 7) / 8 * 8 : (nl + BN - 1) / BN * BN;
+        if (L.i8[l]) {
+            // close the run unless the next level is small too (runs are whole 256-column tiles)
+            const bool cont = small_level(l) && i8_level(l + 1) && small_level(l + 1) && l + 1 - run_first < kI8MaxLevels;
+            if (!cont) {
+                cm = L.colbase[run_first] + (cm - L.colbase[run_first] + kI8Tile - 1) / kI8Tile * kI8Tile;
+                L.i8_last[run_first] = l;
+                L.i8_big[run_first] = run_first == l && !small_level(l) ? 1 : 0;
+                run_first = -1;
+            }
+        }
     }
     L.octbase[T.depth + 1] = co;
     L.colbase[T.depth + 1] = cm;
@@ -745,12 +770,9 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 l++;
                 continue;
             }
-            // small levels (<= 1024 boxes: nearly all 316 offsets active, few columns, so
-            // bound by streaming the operator residues) share one launch; big levels run
-            // alone (measured: one launch for every level is slower at cfg2, 44.8 vs 38 ms)
-            auto small = [&](int lv) { return T.level_off[lv + 1] - T.level_off[lv] <= 1024; };
-            int l1 = l;
-            while (small(l1) && l1 + 1 <= T.depth && Lay.i8[l1 + 1] && small(l1 + 1) && l1 + 1 - l < kI8MaxLevels) l1++;
+            // one launch per int8 run (build_layout): the small levels together, each big
+            // level alone (measured: one launch for every level is slower at cfg2)
+            const int l1 = Lay.i8_last[l];
             const I8Settings &is = ctx.i8;
             if (!ops.i8.res || ops.i8.nmod != is.nmod || ops.i8.beta_a != is.beta_a) {
                 i8_build_operators(ops.i8, ops.ws, ops.m2l, kNumM2L, ops.K, Kp, is.nmod, is.beta_a, st);
@@ -773,6 +795,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             }
             a.X = Pup;
             a.Y = Q;
+            a.big = Lay.i8_big[l] != 0;
             pm = prof.begin("m2l");
             int ps = prof.begin("m2l_prep");
             const I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);

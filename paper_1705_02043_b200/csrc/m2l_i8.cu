@@ -59,10 +59,13 @@ struct Params {
     int64_t ld_src, box0;
     int zero_row, rows_per_mod;
     const int *tile_slots, *tile_nact;
+    const int *tile_below; // [tile][MAX_SLOTS + 1]: active slots of the tile with index < s
+    int nslots, by_index;
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
     int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
-               // loads, 4 no epilogue atomics, 8 no MMA proxy fence
+               // loads, 4 no epilogue atomics, 8 no MMA proxy fence, 16 one operator, 32 plain
+               // per-warp "full" arrivals instead of cp.async-tracked ones
     int nst, stage_bytes; // single-CTA kernel: stage ring depth and stride
     int epi_transpose;    // epilogue atomics through a shared-memory transpose (coalesced)
     int prefetch;         // stages of L2 prefetch ahead for the operator tiles (0: off)
@@ -95,6 +98,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// warp index the compiler can prove warp-uniform (a shuffle from lane 0): branches on it
+// keep the MMA warp's loop on the uniform datapath, so descriptors live in uniform
+// registers and tcgen05.mma issues without per-instruction R2UR / waterfall loops
+__device__ __forceinline__ int warp_uniform() { return __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0); }
+// whole-warp MMA / commit, one elected lane issues (the warp must be converged)
+__device__ __forceinline__ void mma_i8_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_elect(uint64_t *bar) {
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                     tma::smem_u32(bar))
+                 : "memory");
+}
+
+// Chunk c of a column tile = its active slots with slot index in [nslots c / nchunk,
+// nslots (c + 1) / nchunk): every tile walks the SAME slot-index window at the same time,
+// so the concurrently running units of one (modulus, chunk) share each operator tile
+// through L2 instead of streaming it from DRAM once per tile.
+// Otherwise (by_index = 0) chunk c = the c-th equal share of the tile's active list: equal
+// unit sizes, which the static round-robin schedule of the big levels needs.
+__device__ __forceinline__ void chunk_range(const Params &p, int tile, int chunk, int &s0, int &s1) {
+    if (p.by_index) {
+        const int *below = p.tile_below + tile * (MAX_SLOTS + 1);
+        s0 = below[p.nslots * chunk / p.nchunk];
+        s1 = below[p.nslots * (chunk + 1) / p.nchunk];
+    } else {
+        const int nact = p.tile_nact[tile];
+        s0 = nact * chunk / p.nchunk;
+        s1 = nact * (chunk + 1) / p.nchunk;
+    }
+}
+
 struct Unit {
     int t, rt, ct, s0, s1;
 };
@@ -107,9 +145,7 @@ __device__ __forceinline__ Unit decode(const Params &p, int u) {
     u /= p.coltiles;
     const int chunk = u % p.nchunk;
     x.t = u / p.nchunk;
-    const int nact = p.tile_nact[x.ct];
-    x.s0 = nact * chunk / p.nchunk;
-    x.s1 = nact * (chunk + 1) / p.nchunk;
+    chunk_range(p, x.ct, chunk, x.s0, x.s1);
     return x;
 }
 
@@ -122,11 +158,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     int *s_epi = reinterpret_cast<int *>(smem + NS * SB); // [4 warps][32][33] when transposing
     __shared__ __align__(8) uint64_t full[NST_MAX], empty[NST_MAX], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     constexpr int NPT = NPROD * 32;
     if (tid == 0) {
         for (int s = 0; s < NS; s++) {
-            tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
+            // cp.async arrivals + the TMA expect_tx arrival (debug 32: one plain arrival per warp)
+            tma::mbar_init(&full[s], (p.debug & 32) ? NPROD + 1 : NPT + 1);
             tma::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -202,34 +239,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                             tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                         }
                     }
-                    tma::cp_async_mbar_arrive(&full[st]);
+                    if (p.debug & 32) { // timing experiment: plain per-warp arrival (no cp.async tracking)
+                        __syncwarp();
+                        if (lane == 0) tma::mbar_arrive(&full[st]);
+                    } else {
+                        tma::cp_async_mbar_arrive(&full[st]);
+                    }
                 }
             }
         } else if (warp == MMA_WARP) {
-            // ---------------- MMA issuer ----------------
-            if (lane == 0) {
-                const int buf = jb & 1;
-                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+            // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform), one
+            // elected lane issues each tcgen05.mma / commit ----------------
+            const int buf = jb & 1;
+            tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dt = tmem + buf * 256;
+            int st = g % NS;
+            uint32_t ph = (g / NS) & 1;
+            const uint32_t sbase = tma::smem_u32(smem);
+            for (int i = 0; i < n; i++) {
+                tma::mbar_wait(&full[st], ph);
+                // the gathered rows were written by cp.async through the generic proxy
+                if (!(p.debug & 8)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 tc_fence_after();
-                const uint32_t dt = tmem + buf * 256;
-                for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % NS;
-                    tma::mbar_wait(&full[st], (gi / NS) & 1);
-                    // the gathered rows were written by cp.async through the generic proxy
-                    if (!(p.debug & 8)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * SB);
-                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
+                const uint32_t a0 = sbase + st * SB;
+                const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++) // K = 32 bytes per MMA: +2 in the 16-byte start field
-                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
-                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
-                    umma_commit(&empty[st]);
-                }
-                umma_commit(&tfull[buf]);
+                for (int kk = 0; kk < BKI / 32; kk++) // K = 32 bytes per MMA: +2 in the 16-byte start field
+                    mma_i8_elect(dt, ad + 2 * kk, bd + 2 * kk, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                commit_elect(&empty[st]);
+                if (++st == NS) st = 0, ph ^= 1;
             }
+            commit_elect(&tfull[buf]);
             __syncwarp();
         } else {
             // ---------------- epilogue: TMEM lane = box, column = operator row ----------------
@@ -329,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     int *s_epi = reinterpret_cast<int *>(smem + PAIR_NST * PAIR_STAGE); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t full[PAIR_NST], empty[PAIR_NST], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     constexpr int NPT = NPROD * 32;
@@ -369,8 +410,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         v /= npairs;
         const int chunk = v % p.nchunk;
         const int t = v / p.nchunk;
-        const int nact = p.tile_nact[pr];
-        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        int s0, s1;
+        chunk_range(p, pr, chunk, s0, s1);
         const int n = (s1 - s0) * p.KC;
         if (n == 0) continue;
         const int *slots = p.tile_slots + pr * MAX_SLOTS;
@@ -521,7 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     int *s_epi = reinterpret_cast<int *>(smem + NST * STAGE_BYTES); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const uint32_t rank = cluster_rank();
     constexpr int NPT = NPROD * 32;
     const int half = p.Nt / 2;
@@ -557,8 +598,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         v /= npairs;
         const int chunk = v % p.nchunk;
         const int t = v / p.nchunk;
-        const int nact = p.tile_nact[pr];
-        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        int s0, s1;
+        chunk_range(p, pr, chunk, s0, s1);
         const int n = (s1 - s0) * p.KC;
         if (n == 0) continue;
         const int *slots = p.tile_slots + pr * MAX_SLOTS;
@@ -599,32 +640,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 }
             }
         } else if (warp == MMA_WARP) {
-            // ---------------- MMA issuer (each CTA) ----------------
-            if (lane == 0) {
-                const int buf = jb & 1;
-                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+            // ---------------- MMA issuer (each CTA; whole warp, elected lane issues) ----------------
+            const int buf = jb & 1;
+            tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dt = tmem + buf * 256;
+            int st = g % NST;
+            uint32_t ph = (g / NST) & 1;
+            const uint32_t sbase = tma::smem_u32(smem);
+            for (int i = 0; i < n; i++) {
+                tma::mbar_wait(&full[st], ph);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 tc_fence_after();
-                const uint32_t dt = tmem + buf * 256;
-                for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % NST;
-                    tma::mbar_wait(&full[st], (gi / NST) & 1);
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * STAGE_BYTES);
-                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
+                const uint32_t a0 = sbase + st * STAGE_BYTES;
+                const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++)
-                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
-                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
-                                 "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&empty[st])),
-                                 "h"((uint16_t)3)
-                                 : "memory");
-                }
-                umma_commit(&tfull[buf]);
+                for (int kk = 0; kk < BKI / 32; kk++)
+                    mma_i8_elect(dt, ad + 2 * kk, bd + 2 * kk, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
+                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
+                             "h"((uint16_t)3)
+                             : "memory");
+                if (++st == NST) st = 0, ph ^= 1;
             }
+            commit_elect(&tfull[buf]);
             __syncwarp();
         } else {
             // ---------------- epilogue ----------------
@@ -692,7 +732,7 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
     int *s_epi = reinterpret_cast<int *>(smem + DUAL_NST * DUAL_STAGE); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t full[DUAL_NST], empty[DUAL_NST], tfull, tempty;
     __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     constexpr int NPT = DUAL_NPROD * 32;
     if (tid == 0) {
         for (int s = 0; s < DUAL_NST; s++) {
@@ -724,8 +764,8 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
         v /= npairs;
         const int chunk = v % p.nchunk;
         const int t = v / p.nchunk;
-        const int nact = p.tile_nact[pr];
-        const int s0 = nact * chunk / p.nchunk, s1 = nact * (chunk + 1) / p.nchunk;
+        int s0, s1;
+        chunk_range(p, pr, chunk, s0, s1);
         const int n = (s1 - s0) * p.KC;
         if (n == 0) continue;
         const int *slots = p.tile_slots + pr * MAX_SLOTS;
@@ -760,32 +800,29 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
                 }
             }
         } else if (warp == DUAL_MMA_WARP) {
-            // ---------------- MMA issuer: two M128 x Nt MMAs per k-step ----------------
-            if (lane == 0) {
-                tma::mbar_wait(&tempty, (jb & 1) ^ 1);
+            // ---------------- MMA issuer: two M128 x Nt MMAs per k-step (whole warp,
+            // elected lane issues) ----------------
+            tma::mbar_wait(&tempty, (jb & 1) ^ 1);
+            tc_fence_after();
+            int st = g % DUAL_NST;
+            uint32_t ph = (g / DUAL_NST) & 1;
+            const uint32_t sbase = tma::smem_u32(smem);
+            for (int i = 0; i < n; i++) {
+                tma::mbar_wait(&full[st], ph);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 tc_fence_after();
-                for (int i = 0; i < n; i++) {
-                    const int gi = g + i, st = gi % DUAL_NST;
-                    tma::mbar_wait(&full[st], (gi / DUAL_NST) & 1);
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    tc_fence_after();
-                    const uint32_t a0 = tma::smem_u32(smem + st * DUAL_STAGE);
-                    const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES),
-                                   bd = sw128_desc(a0 + DUAL_A_BYTES);
+                const uint32_t a0 = sbase + st * DUAL_STAGE;
+                const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES), bd = sw128_desc(a0 + DUAL_A_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++) {
-                        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                                     "l"(ad0 + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"(acc));
-                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + 256),
-                                     "l"(ad1 + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc), "r"(acc));
-                    }
-                    umma_commit(&empty[st]);
+                for (int kk = 0; kk < BKI / 32; kk++) {
+                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                    mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                    mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, acc);
                 }
-                umma_commit(&tfull);
+                commit_elect(&empty[st]);
+                if (++st == DUAL_NST) st = 0, ph ^= 1;
             }
+            commit_elect(&tfull);
             __syncwarp();
         } else {
             // ---------------- epilogue: both accumulators ----------------
@@ -834,7 +871,7 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
 
 // active slots per column tile of `bn` columns, in slot order
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
-                                 int *tile_nact) {
+                                 int *tile_nact, int *tile_below) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
@@ -846,8 +883,12 @@ __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, in
     __syncthreads();
     if (threadIdx.x == 0) {
         int n = 0;
-        for (int s = 0; s < nslots; s++)
+        int *below = tile_below + ct * (MAX_SLOTS + 1);
+        for (int s = 0; s < nslots; s++) {
+            below[s] = n;
             if (flag[s]) tile_slots[ct * MAX_SLOTS + n++] = s;
+        }
+        below[nslots] = n;
         tile_nact[ct] = n;
     }
 }
@@ -1070,34 +1111,36 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
 
 namespace {
 
-// kernel variant, PKGPU_I8_PAIR: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
+// kernel variant per launch: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
 // (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
-// (m2l_i8_dual_kernel); see DESIGN.md §4
-int pair_mode() {
-    static const int v = [] {
+// (m2l_i8_dual_kernel). Default: dual for big levels (octant groups fill 256-column pair
+// tiles; 8 MMAs per pipeline stage and half the operator bytes per MAC), single for the
+// small-level run. PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
+int select_mode(bool big) {
+    static const int forced = [] {
         const char *e = std::getenv("PKGPU_I8_PAIR");
-        return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
+        return e ? std::max(0, std::min(3, std::atoi(e))) : -1;
     }();
-    return v;
+    return forced >= 0 ? forced : (big ? 3 : 0);
 }
-bool use_pair() { return pair_mode() != 0; }
-int column_tile() { return use_pair() ? 2 * TBM : TBM; }
+int column_tile(int mode) { return mode != 0 ? 2 * TBM : TBM; }
 
-// active-slot lists per column tile (ncols / column_tile() tiles)
-void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, Workspace &ws, cudaStream_t st, int **tslots,
-                int **tnact) {
-    const int bn = column_tile(), tiles = ncols / bn;
+// active-slot lists per column tile (ncols / column_tile(mode) tiles)
+void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode, Workspace &ws, cudaStream_t st,
+                int **tslots, int **tnact, int **tbelow) {
+    const int bn = column_tile(mode), tiles = ncols / bn;
     *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
     *tnact = ws.get<int>("i8_tile_nact", tiles);
-    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact);
+    *tbelow = ws.get<int>("i8_tile_below", (size_t)tiles * (MAX_SLOTS + 1));
+    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow);
     PK_CUDA(cudaGetLastError());
 }
 
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
-                 const int *tnact, cudaStream_t st) {
+                 const int *tnact, const int *tbelow, int mode, cudaStream_t st) {
     const int num_sms = sm_count();
-    const bool pair = use_pair();
+    const bool pair = mode != 0;
     Params p;
     std::memset(&p, 0, sizeof p);
     p.X = B;
@@ -1118,7 +1161,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.R = R;
     // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
     // both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the CTA pair)
-    const int M = pair_mode() == 1 ? 2 * TBM : TBM;
+    const int M = mode == 1 ? 2 * TBM : TBM;
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     static const int debug = std::getenv("PKGPU_I8_DEBUG") ? std::atoi(std::getenv("PKGPU_I8_DEBUG")) : 0;
     p.debug = debug;
@@ -1127,16 +1170,22 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     static const int min_chunks = std::getenv("PKGPU_I8_CHUNKS") ? std::atoi(std::getenv("PKGPU_I8_CHUNKS")) : 0;
     nchunk = std::max(nchunk, min_chunks);
     const int64_t base = (int64_t)nmod * p.rowtiles * (pair ? p.coltiles / 2 : p.coltiles);
-    const int64_t resident = (pair_mode() == 1 || pair_mode() == 2) ? num_sms / 2 : num_sms;
+    const int64_t resident = (mode == 1 || mode == 2) ? num_sms / 2 : num_sms;
     while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
     p.tile_slots = tslots;
     p.tile_nact = tnact;
+    p.tile_below = tbelow;
+    p.nslots = nslots;
+    // slot-index windows for the small-level run (operator reuse through L2 across its
+    // tiles); equal list shares for the dual-tile big levels (balanced static schedule)
+    static const int by_index_env = std::getenv("PKGPU_I8_BYINDEX") ? std::atoi(std::getenv("PKGPU_I8_BYINDEX")) : -1;
+    p.by_index = by_index_env >= 0 ? by_index_env : (mode == 3 ? 0 : 1);
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
     // the CTA-pair variants stage half of the operator tile per CTA
-    const bool half_tile = pair_mode() == 1 || pair_mode() == 2;
+    const bool half_tile = mode == 1 || mode == 2;
     const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
@@ -1144,7 +1193,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    if (pair_mode() == 3) {
+    if (mode == 3) {
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
         static bool cfg = false;
         if (!cfg) {
@@ -1153,7 +1202,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         }
         const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
         m2l_i8_dual_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
-    } else if (pair_mode() == 2) {
+    } else if (mode == 2) {
         const size_t smem = (size_t)NST * STAGE_BYTES + epi;
         static bool cfg = false;
         if (!cfg) {
@@ -1206,9 +1255,11 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     if (ncols % kI8Tile != 0 || Ki % BKI != 0 || nslots > MAX_SLOTS || nmod < 1 || nmod > kI8MaxModuli)
         throw RuntimeError("i8_gather_gemm: bad shape");
     upload_tables();
-    int *tslots = nullptr, *tnact = nullptr;
-    scan_tiles(src, ld_src, nslots, ncols, ws, st, &tslots, &tnact);
-    launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact, st);
+    int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
+    const int mode = select_mode(ncols >= 2048);
+    scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow);
+    launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
+                tbelow, mode, st);
     return 2;
 }
 
@@ -1235,7 +1286,8 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
     w.R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
     upload_tables();
-    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, ws, st, &w.tile_slots, &w.tile_nact);
+    w.mode = select_mode(a.big);
+    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below);
     PK_CUDA(cudaGetLastError());
     if (launches) *launches += 2 + a.lv.n;
     return w;
@@ -1245,7 +1297,7 @@ int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w
     (void)ws;
     if (a.ncols == 0) return 0;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src, a.ld_src, a.lv.box0[0],
-                a.nslots, a.ncols, w.R, w.tile_slots, w.tile_nact, st);
+                a.nslots, a.ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st);
     return 1;
 }
 

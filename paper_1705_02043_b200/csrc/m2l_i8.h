@@ -63,6 +63,7 @@ struct I8LevelArgs {
     I8Levels lv;                  // sources of a column are boxes of the column's own level
     const double *X = nullptr;    // [box][Kp]
     double *Y = nullptr;          // [box][Kp]: Y += alpha_l * sum_slot M X
+    bool big = false;             // one large level: the dual-tile kernel (see select_mode)
 };
 struct I8LevelWork {
     const int8_t *xres = nullptr;     // [nmod][nbox + 1][Ki] density residues (last row zero)
@@ -70,6 +71,8 @@ struct I8LevelWork {
     unsigned long long *mx = nullptr; // per-level max |phi| (bit patterns)
     int64_t rows = 0;
     int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile
+    int *tile_below = nullptr;                       // per tile: active slots below each slot index
+    int mode = 0;                                    // kernel variant (select_mode)
 };
 // The three steps of one level (separately timed by the stage profiler):
 //   prepare: level max, density residues, R = 0
