@@ -106,7 +106,9 @@ pkgpu_status pkgpu_context_set_profiling(pkgpu_context *ctx, int on);
 /* M2L arithmetic path. path 0: int8 tensor pipe (exact residue GEMMs, CRT rebuild in
  * FP64) on levels with >= min_boxes boxes, DMMA FP64 elsewhere (default; min_boxes <= 0
  * keeps the current threshold, 1 unless PKGPU_M2L_I8_MIN says otherwise); path 1:
- * DMMA FP64 everywhere. nmod / beta_a / beta_b > 0 override the residue parameters
+ * DMMA FP64 everywhere; path 2: as 0, plus M2M / L2L / pseudo-inverses on the int8 pipe
+ * (per-column fixed-point scale; opt-in, slower than DMMA at cfg2). nmod / beta_a / beta_b
+ * > 0 override the residue parameters
  * (moduli count 14..20, fixed-point bits of operators / densities, beta_a + beta_b +
  * 20 < sum log2 m_t). */
 pkgpu_status pkgpu_context_set_m2l(pkgpu_context *ctx, int path, int64_t min_boxes, int nmod, int beta_a,

@@ -397,8 +397,9 @@ class Context:
     def set_m2l(self, path="int8", min_boxes=0, nmod=0, beta_a=0, beta_b=0):
         """M2L arithmetic: "int8" (exact residue GEMMs on the int8 tensor pipe for levels
         with >= min_boxes boxes, FP64 DMMA elsewhere; the default) or "dmma" (FP64 DMMA
-        everywhere). nmod / beta_a / beta_b override the residue parameters."""
-        code = {"int8": 0, "dmma": 1}[path]
+        everywhere) or "int8_all" (as "int8", plus M2M / L2L / pseudo-inverses on the int8
+        pipe). nmod / beta_a / beta_b override the residue parameters."""
+        code = {"int8": 0, "dmma": 1, "int8_all": 2}[path]
         if lib().pkgpu_context_set_m2l(self._h, code, int(min_boxes), int(nmod), int(beta_a), int(beta_b)) != 0:
             raise ValueError(f"set_m2l: invalid settings {path, min_boxes, nmod, beta_a, beta_b}")
 

@@ -275,7 +275,24 @@ struct Layout {
     int64_t ncols = 0, noct = 0, nm2m = 0;
     int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
     int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
+    int *l2l_src8 = nullptr;          // [8][noct]: parent per (octant slot, column) for i8_translate
+    std::vector<int64_t> lvbase;      // per-level columns of lvcol (levels padded to kI8Tile)
+    int *lvcol = nullptr;             // box per column, -1 padding (pseudo-inverse columns)
 };
+
+__global__ void lvcol_fill_kernel(TreeView T, const int *__restrict__ lvbase, int *lvcol) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int l = T.cell[b].w;
+    lvcol[lvbase[l] + (b - T.level_off[l])] = b;
+}
+__global__ void l2l_src8_kernel(const int *__restrict__ l2l_src, const int *__restrict__ tile_oct, int64_t noct,
+                                int *src8) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= noct) return;
+    const int b = l2l_src[c];
+    if (b >= 0) src8[(int64_t)tile_oct[c / BN] * noct + c] = b;
+}
 
 // Columns of the gather-GEMMs. Octant grouping makes every 64-column M2L tile share
 // one offset set (~189 of 316 slots active, no zero columns) at the price of padding
@@ -340,6 +357,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         // inside an int8 run an ungrouped level is packed (8-column granularity) after the
         // previous one; grouped levels keep 64-aligned octant groups
         if (grouped[l] || !L.i8[l]) cm = (cm + BN - 1) / BN * BN;
+        co = (co + kI8Tile - 1) / kI8Tile * kI8Tile; // levels in whole int8 tiles (i8_translate L2L)
         L.octbase[l] = co;
         L.colbase[l] = cm;
         mbase[l] = (int)cm;
@@ -364,6 +382,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             }
         }
     }
+    co = (co + kI8Tile - 1) / kI8Tile * kI8Tile;
     L.octbase[T.depth + 1] = co;
     L.colbase[T.depth + 1] = cm;
     L.noct = co;
@@ -383,6 +402,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
     L.out_oct = ws.get<int>("out_oct", CO);
     L.l2l_src = ws.get<int>("l2l_src", CO);
     L.tile_oct = ws.get<int>("tile_oct", CO / BN + 1);
+    PK_CUDA(cudaMemsetAsync(L.tile_oct, 0, (CO / BN + 1) * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.out_box, 0xff, C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.m2l_table, 0xff, (size_t)kNumM2L * C * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.out_oct, 0xff, CO * sizeof(int), st));
@@ -391,11 +411,33 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         tv, skeys, svals, d_small, d_small + NK, d_small + 2 * NK, d_small + 3 * NK, d_small + 3 * NK + kMaxLevels + 1,
         L.col_of_box, L.out_box, L.out_oct, L.l2l_src, L.tile_oct);
     PK_CUDA(cudaGetLastError());
+    if (ctx.i8.trans) {
+        if (mask) {
+            mask_oct_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(mask, CO, L.out_oct, L.l2l_src);
+            ctx.launches += 1;
+        }
+        L.l2l_src8 = ws.get<int>("l2l_src8", (size_t)8 * CO);
+        PK_CUDA(cudaMemsetAsync(L.l2l_src8, 0xff, (size_t)8 * CO * sizeof(int), st));
+        l2l_src8_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(L.l2l_src, L.tile_oct, CO, L.l2l_src8);
+        // pseudo-inverse columns: each level's boxes, padded to whole int8 tiles
+        L.lvbase.assign(T.depth + 2, 0);
+        for (int l = 0; l <= T.depth; l++)
+            L.lvbase[l + 1] = L.lvbase[l] + (T.level_off[l + 1] - T.level_off[l] + kI8Tile - 1) / kI8Tile * kI8Tile;
+        std::vector<int> hb(L.lvbase.begin(), L.lvbase.end());
+        int *d_lvbase = ws.get<int>("lvbase", hb.size());
+        PK_CUDA(cudaMemcpyAsync(d_lvbase, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        L.lvcol = ws.get<int>("lvcol", std::max<int64_t>(L.lvbase[T.depth + 1], 1));
+        PK_CUDA(cudaMemsetAsync(L.lvcol, 0xff, std::max<int64_t>(L.lvbase[T.depth + 1], 1) * sizeof(int), st));
+        lvcol_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, d_lvbase, L.lvcol);
+        PK_CUDA(cudaGetLastError());
+        ctx.launches += 2;
+        PK_CUDA(cudaStreamSynchronize(st)); // hb is read by the async copy
+    }
     // ---- M2M layout: internal boxes with sources, compacted in BFS order ----
     int *flags = ws.get<int>("m2m_flags", nb), *list = ws.get<int>("m2m_list", nb);
     int *lcount = ws.get<int>("m2m_lcount", kMaxLevels + 1), *nsel = ws.get<int>("m2m_nsel", 1);
     PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
-    if (mask) {
+    if (mask && !ctx.i8.trans) {
         mask_oct_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(mask, CO, L.out_oct, L.l2l_src);
         ctx.launches += 1;
     }
@@ -416,7 +458,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         cbase[l] = (int)cmm;
         L.m2mbase[l] = cmm;
         nint += lc[l];
-        cmm += (lc[l] + BN - 1) / BN * BN;
+        cmm += (lc[l] + kI8Tile - 1) / kI8Tile * kI8Tile; // whole int8 tiles (i8_translate)
     }
     L.m2mbase[T.depth + 1] = cmm;
     L.nm2m = cmm;
@@ -499,7 +541,7 @@ Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int
     for (int l = 0; l <= T.depth; l++) {
         start[l] = s, base[l] = (int)c, P.actbase[l] = c;
         s += lc[l];
-        c += (lc[l] + BN - 1) / BN * BN;
+        c += (lc[l] + kI8Tile - 1) / kI8Tile * kI8Tile;
     }
     P.actbase[T.depth + 1] = c;
     P.act = ws.get<int>("pt_act", std::max<int64_t>(c, 1));
@@ -516,8 +558,54 @@ Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int
     return P;
 }
 
+// int8 operator sets for i8_translate, built on first use
+I8Operators &i8_ops(pkgpu_context &ctx, KifmmOps &ops, I8Operators &o, const double *A, int nmat, const char *tag,
+                    cudaStream_t st) {
+    const I8Settings &is = ctx.i8;
+    if (!o.res || o.nmod != is.nmod || o.beta_a != is.beta_a) {
+        i8_build_operators(o, ops.ws, A, nmat, ops.K, ops.Kp, is.nmod, is.beta_a, st, tag);
+        ctx.launches += 3;
+    }
+    return o;
+}
+
 void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t hi, int level, double *Q, double *Tmp,
-                double *Phi, cudaStream_t st, const Partition *P = nullptr) {
+                double *Phi, cudaStream_t st, const Partition *P, const Layout &Lay) {
+    if (ctx.i8.trans) {
+        // x = V (S+ (U^T b)) as two int8-pipe translations (nested order kept)
+        I8TransArgs a;
+        a.K = ops.K;
+        a.Kp = ops.Kp;
+        if (P && P->on) {
+            a.out_box = P->act + P->actbase[level];
+            a.ncols = (int)(P->actbase[level + 1] - P->actbase[level]);
+        } else {
+            a.out_box = Lay.lvcol + Lay.lvbase[level];
+            a.ncols = (int)(Lay.lvbase[level + 1] - Lay.lvbase[level]);
+        }
+        if (a.ncols <= 0) return;
+        a.nslots = 1;
+        a.src = a.out_box;
+        a.ld_src = a.ncols;
+        a.src_lo = lo;
+        a.src_hi = hi;
+        a.X = Q;
+        a.Y = Tmp;
+        a.rdiv = up ? ops.s_up : ops.s_dn;
+        a.rdiv_eps = up ? ops.up.eps : ops.dn.eps;
+        I8Operators &u = up ? i8_ops(ctx, ops, ops.i8_ut_up, ops.Ut_up, 1, "ut_up", st)
+                            : i8_ops(ctx, ops, ops.i8_ut_dn, ops.Ut_dn, 1, "ut_dn", st);
+        ctx.launches += i8_translate(u, a, ctx.i8.beta_b, ctx.ws, st);
+        a.X = Tmp;
+        a.Y = Phi;
+        a.rdiv = nullptr;
+        a.alpha = std::ldexp(1.0, -level); // phi /= 2^l (src/fmm.cpp:550-551, 595-596)
+        a.beta = 0.0;
+        I8Operators &v = up ? i8_ops(ctx, ops, ops.i8_v_up, ops.V_up, 1, "v_up", st)
+                            : i8_ops(ctx, ops, ops.i8_v_dn, ops.V_dn, 1, "v_dn", st);
+        ctx.launches += i8_translate(v, a, ctx.i8.beta_b, ctx.ws, st);
+        return;
+    }
     GemmArgs a;
     a.Kp = ops.Kp;
     if (P && P->on) { // only the boxes meeting this rank's leaves
@@ -724,7 +812,25 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         for (int l = T.depth; l >= 0; l--) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.m2mbase[l], c1 = Lay.m2mbase[l + 1];
-            if (c1 > c0) {
+            if (c1 > c0 && ctx.i8.trans) {
+                I8TransArgs a;
+                a.K = ops.K;
+                a.Kp = Kp;
+                a.ncols = (int)(c1 - c0);
+                a.out_box = Lay.out_m2m + c0;
+                a.nslots = 8;
+                a.src = Lay.m2m_src + c0;
+                a.ld_src = Lay.nm2m;
+                a.src_lo = T.level_off[l + 1]; // children
+                a.src_hi = T.level_off[l + 2];
+                a.X = Pup;
+                a.Y = Q;
+                a.alpha = std::ldexp(1.0, l); // q += 2^l M2M_o phi_child (src/fmm.cpp:547)
+                a.beta = 0.0;
+                pm = prof.begin("m2m");
+                ctx.launches += i8_translate(i8_ops(ctx, ops, ops.i8_m2m, ops.m2m, 8, "m2m", st), a, ctx.i8.beta_b, ws, st);
+                prof.end(pm);
+            } else if (c1 > c0) {
                 GemmArgs a;
                 a.Kp = Kp;
                 a.ncols = (int)(c1 - c0);
@@ -743,7 +849,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_up");
-            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st, PP);
+            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st, PP, Lay);
             prof.end(pm);
         }
         if (partitioned) {
@@ -834,7 +940,26 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
                 prof.end(pm);
             }
-            if (l >= 1) {
+            if (l >= 1 && ctx.i8.trans) {
+                const int64_t o0 = Lay.octbase[l], o1 = Lay.octbase[l + 1];
+                I8TransArgs b;
+                b.K = ops.K;
+                b.Kp = Kp;
+                b.ncols = (int)(o1 - o0);
+                b.out_box = Lay.out_oct + o0;
+                b.nslots = 8;
+                b.src = Lay.l2l_src8 + o0;
+                b.ld_src = Lay.noct;
+                b.src_lo = T.level_off[l - 1]; // parents
+                b.src_hi = T.level_off[l];
+                b.X = Pdn;
+                b.Y = Q;
+                b.alpha = std::ldexp(1.0, l) * 0.5; // q += (2^l / 2) L2L_o phi_parent (src/fmm.cpp:590-591)
+                b.beta = 1.0;
+                pm = prof.begin("l2l");
+                ctx.launches += i8_translate(i8_ops(ctx, ops, ops.i8_l2l, ops.l2l, 8, "l2l", st), b, ctx.i8.beta_b, ws, st);
+                prof.end(pm);
+            } else if (l >= 1) {
                 const int64_t o0 = Lay.octbase[l], o1 = Lay.octbase[l + 1];
                 GemmArgs b;
                 b.Kp = Kp;
@@ -855,7 +980,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_dn");
-            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st, PP);
+            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st, PP, Lay);
             prof.end(pm);
         }
         PK_CUDA(cudaEventRecord(ctx.ev[2], st));

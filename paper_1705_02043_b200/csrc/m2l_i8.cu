@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include <cudaTypedefs.h>
 
@@ -51,6 +52,8 @@ const int kModuli[kI8MaxModuli] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 
 __constant__ int c_mod[kI8MaxModuli];
 __constant__ int c_pm[kI8MaxModuli][kI8MaxModuli]; // (prod_{s' < s} m_s') mod m_t, s < t
 __constant__ int c_pinv[kI8MaxModuli];              // (prod_{s < t} m_s)^-1 mod m_t
+__constant__ int c_c21[kI8MaxModuli], c_c42[kI8MaxModuli]; // 2^21 mod m_t, 2^42 mod m_t
+__constant__ float c_finv[kI8MaxModuli];            // 1 / m_t
 
 struct Params {
     CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
@@ -61,6 +64,7 @@ struct Params {
     const int *tile_slots, *tile_nact;
     const int *tile_below; // [tile][MAX_SLOTS + 1]: active slots of the tile with index < s
     int nslots, by_index;
+    int direct; // single-kernel epilogue stores the partial residues (one unit per output tile)
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
     int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
@@ -309,7 +313,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
 #pragma unroll 8
                 for (int b = 0; b < 32; b++) {
                     const int r = tile[b * EPI_PITCH + lane]; // box col0 + b, row r0 + j0 + lane
-                    if (ok && r && !(p.debug & 4)) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    if (ok && !(p.debug & 4)) {
+                        if (p.direct)
+                            Rt[(int64_t)b * p.Ki + j0 + lane] = r;
+                        else if (r)
+                            atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    }
                 }
                 __syncwarp();
             }
@@ -911,13 +920,19 @@ __device__ __forceinline__ int mod_small(int a, int m, float inv) {
 }
 __device__ __forceinline__ int balanced(int r, int m) { return r >= (m + 1) / 2 ? r - m : r; }
 
-// residues of v (|v| <= 2^62) for all moduli, via v = a2 2^42 + a1 2^21 + a0
+// residues of v (|v| <= 2^62) for all moduli, via v = a2 2^42 + a1 2^21 + a0: the folded
+// value a2 (2^42 mod m) + a1 (2^21 mod m) + a0 has |.| < 2^30, reduced with a float quotient
+// (off by at most one or two) and corrections -- 32-bit integer work only
 __device__ __forceinline__ void residues(long long v, int nmod, int8_t *out, int64_t stride) {
-    const long long a0 = v & ((1ll << 21) - 1), a1 = (v >> 21) & ((1ll << 21) - 1), a2 = v >> 42;
+    const int a0 = (int)(v & ((1ll << 21) - 1)), a1 = (int)((v >> 21) & ((1ll << 21) - 1)), a2 = (int)(v >> 42);
     for (int t = 0; t < nmod; t++) {
         const int m = c_mod[t];
-        const int c21 = (int)((1ll << 21) % m), c42 = (int)(((long long)c21 * c21) % m);
-        const int r = mod_pos(a2 * c42 + a1 * c21 + a0, m, 1.0 / m);
+        const int f = a2 * c_c42[t] + a1 * c_c21[t] + a0;
+        int r = f - __float2int_rd(__int2float_rn(f) * c_finv[t]) * m;
+        if (r < 0) r += m;
+        if (r < 0) r += m;
+        if (r >= m) r -= m;
+        if (r >= m) r -= m;
         out[t * stride] = (int8_t)balanced(r, m);
     }
 }
@@ -1013,7 +1028,7 @@ __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki,
 #pragma unroll
         for (int t = 0; t < NM; t++) {
             const int m = c_mod[t];
-            const float inv = 1.0f / (float)m;
+            const float inv = c_finv[t];
             const int d = mod_small(x[t] - acc[t], m, inv);
             v[t] = balanced(mod_small(d * c_pinv[t], m, inv), m);
 #pragma unroll
@@ -1023,6 +1038,99 @@ __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki,
 #pragma unroll
         for (int t = NM - 2; t >= 0; t--) h = fma(h, (double)c_mod[t], (double)v[t]);
         Y[(int64_t)ob * Kp + r] += alpha * ldexp(h, rowexp[r] + E - beta_sum);
+    }
+}
+
+// ---- i8_translate: per-column fixed-point scale ----
+// Block per column c: E_c from max |X| over the column's sources, then the residues of those
+// source rows at scale 2^(beta - E_c) (a source shared by several columns is written with
+// the same E by each of them), and R[.][c][.] = 0. Block 0 also zeroes the zero row.
+__global__ void tr_prepare_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int64_t src_lo,
+                                  int64_t nsrc, const double *__restrict__ X, int K, int Kp, int Ki, int nmod, int beta,
+                                  int ncols, int8_t *__restrict__ xres, int *__restrict__ ecol, int *__restrict__ R,
+                                  int zero_r) {
+    __shared__ double red[32];
+    __shared__ int sb[8];
+    const int c = blockIdx.x, tid = threadIdx.x;
+    const int64_t stride = (nsrc + 1) * Ki;
+    if (tid < nslots) sb[tid] = src[(int64_t)tid * ld_src + c];
+    __syncthreads();
+    double m = 0.0;
+    for (int s = 0; s < nslots; s++) {
+        const int b = sb[s];
+        if (b < 0) continue;
+        for (int k = tid; k < K; k += blockDim.x) m = fmax(m, fabs(X[(int64_t)b * Kp + k]));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    if (tid < 32) {
+        m = tid < (int)(blockDim.x >> 5) ? red[tid] : 0.0;
+        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (tid == 0) red[0] = m;
+    }
+    __syncthreads();
+    m = red[0];
+    const int E = m > 0 ? ilogb(m) + 1 : 0;
+    if (tid == 0) ecol[c] = E;
+    for (int s = 0; s < nslots; s++) {
+        const int b = sb[s];
+        if (b < 0) continue;
+        int8_t *row = xres + (int64_t)(b - src_lo) * Ki;
+        for (int k = tid; k < Ki; k += blockDim.x) {
+            const double x = k < K ? X[(int64_t)b * Kp + k] : 0.0;
+            residues(llrint(ldexp(x, beta - E)), nmod, row + k, stride);
+        }
+    }
+    if (zero_r)
+        for (int t = 0; t < nmod; t++)
+            for (int k = tid; k < Ki; k += blockDim.x) R[((int64_t)t * ncols + c) * Ki + k] = 0;
+    if (c == 0)
+        for (int i = tid; i < nmod * Ki; i += blockDim.x) xres[(int64_t)(i / Ki) * stride + nsrc * Ki + i % Ki] = 0;
+}
+
+// CRT rebuild of one residue vector (Garner balanced mixed radix, Horner in FP64)
+template <int NM> __device__ __forceinline__ double crt_value(const int *__restrict__ R, int64_t i, int64_t n) {
+    int x[NM], acc[NM], v[NM];
+#pragma unroll
+    for (int t = 0; t < NM; t++) {
+        x[t] = R[(int64_t)t * n + i];
+        acc[t] = 0;
+    }
+#pragma unroll
+    for (int t = 0; t < NM; t++) {
+        const int m = c_mod[t];
+        const float inv = c_finv[t];
+        const int d = mod_small(x[t] - acc[t], m, inv);
+        v[t] = balanced(mod_small(d * c_pinv[t], m, inv), m);
+#pragma unroll
+        for (int s = t + 1; s < NM; s++) acc[s] += v[t] * c_pm[t][s];
+    }
+    double h = v[NM - 1];
+#pragma unroll
+    for (int t = NM - 2; t >= 0; t--) h = fma(h, (double)c_mod[t], (double)v[t]);
+    return h;
+}
+
+template <int NM>
+__global__ void tr_finish_kernel(const int *__restrict__ R, int ncols, int Ki, int K, int Kp,
+                                 const int *__restrict__ out_box, const int *__restrict__ rowexp,
+                                 const int *__restrict__ ecol, int beta_sum, double alpha, double beta,
+                                 const double *__restrict__ rdiv, double rdiv_eps, double *__restrict__ Y) {
+    const int64_t n = (int64_t)ncols * Ki;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i / Ki), r = (int)(i % Ki);
+        if (r >= K) continue;
+        const int ob = out_box[c];
+        if (ob < 0) continue;
+        const double v = ldexp(crt_value<NM>(R, i, n), rowexp[r] + ecol[c] - beta_sum);
+        double *y = Y + (int64_t)ob * Kp + r;
+        if (rdiv) {
+            const double d = rdiv[r];
+            *y = d > rdiv_eps ? v / d : 0.0;
+        } else {
+            *y = (beta != 0.0 ? beta * *y : 0.0) + alpha * v;
+        }
     }
 }
 
@@ -1061,6 +1169,17 @@ void upload_tables() {
     PK_CUDA(cudaMemcpyToSymbol(c_mod, kModuli, sizeof kModuli));
     PK_CUDA(cudaMemcpyToSymbol(c_pm, pm, sizeof pm));
     PK_CUDA(cudaMemcpyToSymbol(c_pinv, pinv, sizeof pinv));
+    int c21[kI8MaxModuli], c42[kI8MaxModuli];
+    float finv[kI8MaxModuli];
+    for (int t = 0; t < kI8MaxModuli; t++) {
+        const int m = kModuli[t];
+        c21[t] = (int)((1ll << 21) % m);
+        c42[t] = (int)((long long)c21[t] * c21[t] % m);
+        finv[t] = 1.0f / (float)m;
+    }
+    PK_CUDA(cudaMemcpyToSymbol(c_c21, c21, sizeof c21));
+    PK_CUDA(cudaMemcpyToSymbol(c_c42, c42, sizeof c42));
+    PK_CUDA(cudaMemcpyToSymbol(c_finv, finv, sizeof finv));
     if (dev < 64) dev_done[dev] = 1;
 }
 
@@ -1080,6 +1199,10 @@ const I8Settings &i8_settings() {
         I8Settings r;
         const char *e = std::getenv("PKGPU_M2L");
         r.enabled = !(e && std::strcmp(e, "dmma") == 0);
+        // measured at cfg2: the int8 translations lose to the DMMA gather-GEMM (the per-column
+        // residue / CRT traffic outweighs the GEMM for 1-8 slots), so they are opt-in
+        const char *t = std::getenv("PKGPU_TRANS");
+        r.trans = r.enabled && t && std::strcmp(t, "i8") == 0;
         if (const char *c = std::getenv("PKGPU_M2L_I8")) {
             int a = r.nmod, b = r.beta_a, d = r.beta_b;
             if (std::sscanf(c, "%d,%d,%d", &a, &b, &d) == 3) r.nmod = a, r.beta_a = b, r.beta_b = d;
@@ -1092,19 +1215,20 @@ const I8Settings &i8_settings() {
 }
 
 void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat, int K, int Kp, int nmod,
-                        int beta_a, cudaStream_t st) {
+                        int beta_a, cudaStream_t st, const char *tag) {
+    const std::string pre = std::string("i8_") + tag + "_";
     upload_tables();
     o.nmod = nmod;
     o.beta_a = beta_a;
     o.K = K;
     o.Ki = (K + BKI - 1) / BKI * BKI;
     o.nmat = nmat;
-    unsigned long long *mx = ws.get<unsigned long long>("i8_rowmax", o.Ki);
+    unsigned long long *mx = ws.get<unsigned long long>(pre + "rowmax", o.Ki);
     PK_CUDA(cudaMemsetAsync(mx, 0, o.Ki * sizeof(unsigned long long), st));
     rowmax_kernel<<<dim3(K, nmat), 32, 0, st>>>(A, nmat, K, Kp, mx);
-    o.rowexp = ws.get<int>("i8_rowexp", o.Ki);
+    o.rowexp = ws.get<int>(pre + "rowexp", o.Ki);
     rowexp_kernel<<<(o.Ki + 127) / 128, 128, 0, st>>>(mx, K, o.Ki, o.rowexp);
-    o.res = ws.get<int8_t>("i8_res", (size_t)nmod * nmat * o.Ki * o.Ki);
+    o.res = ws.get<int8_t>(pre + "res", (size_t)nmod * nmat * o.Ki * o.Ki);
     op_residue_kernel<<<dim3(o.Ki, nmat), 128, 0, st>>>(A, nmat, K, Kp, o.Ki, nmod, beta_a, o.rowexp, o.res);
     PK_CUDA(cudaGetLastError());
 }
@@ -1138,7 +1262,7 @@ void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode,
 
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
-                 const int *tnact, const int *tbelow, int mode, cudaStream_t st) {
+                 const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false) {
     const int num_sms = sm_count();
     const bool pair = mode != 0;
     Params p;
@@ -1174,6 +1298,8 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
+    if (direct && (nchunk != 1 || mode != 0)) throw RuntimeError("i8 gemm: direct stores need one unit per tile");
+    p.direct = direct ? 1 : 0;
     p.tile_slots = tslots;
     p.tile_nact = tnact;
     p.tile_below = tbelow;
@@ -1227,7 +1353,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
             const char *e = std::getenv("PKGPU_I8_EPI");
             return !(e && std::strcmp(e, "direct") == 0);
         }();
-        p.epi_transpose = transpose ? 1 : 0;
+        p.epi_transpose = (transpose || direct) ? 1 : 0;
         static const int prefetch = std::getenv("PKGPU_I8_PREFETCH") ? std::atoi(std::getenv("PKGPU_I8_PREFETCH")) : 0;
         p.prefetch = prefetch;
         p.stage_bytes = A_BYTES + (p.Nt * BKI + 1023) / 1024 * 1024;
@@ -1319,6 +1445,45 @@ int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork 
     }
     PK_CUDA(cudaGetLastError());
     return 1;
+}
+
+int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {
+    if (a.ncols == 0) return 0;
+    if (a.ncols % kI8Tile != 0 || a.nslots < 1 || a.nslots > 8 || a.nslots > o.nmat || a.src_hi < a.src_lo)
+        throw RuntimeError("i8_translate: bad shape");
+    upload_tables();
+    const int nmod = o.nmod, Ki = o.Ki;
+    const int64_t nsrc = a.src_hi - a.src_lo;
+    int8_t *xres = ws.get<int8_t>("tr_xres", (size_t)nmod * (nsrc + 1) * Ki);
+    int *ecol = ws.get<int>("tr_ecol", a.ncols);
+    int *R = ws.get<int>("tr_R", (size_t)nmod * a.ncols * Ki);
+    // <= 16 slots: one work unit per output tile (launch_gemm), whose epilogue stores the
+    // partial residues directly -- no R zeroing, no atomics
+    static const bool chunks_forced = std::getenv("PKGPU_I8_CHUNKS") != nullptr;
+    const bool direct = a.nslots <= 16 && !chunks_forced;
+    tr_prepare_kernel<<<a.ncols, 256, 0, st>>>(a.src, a.ld_src, a.nslots, a.src_lo, nsrc, a.X, a.K, a.Kp, Ki, nmod,
+                                                beta_b, a.ncols, xres, ecol, R, direct ? 0 : 1);
+    PK_CUDA(cudaGetLastError());
+    int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
+    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, 0, ws, st, &tslots, &tnact, &tbelow);
+    launch_gemm(o.res, o.nmat, xres, (int)(nsrc + 1), (int)nsrc, Ki, nmod, a.src, a.ld_src, a.src_lo, a.nslots,
+                a.ncols, R, tslots, tnact, tbelow, 0, st, direct);
+    const int64_t n = (int64_t)a.ncols * Ki;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    const int bs = o.beta_a + beta_b;
+    switch (nmod) {
+#define PK_TF(NM)                                                                                                      \
+    case NM:                                                                                                           \
+        tr_finish_kernel<NM><<<grid, 256, 0, st>>>(R, a.ncols, Ki, a.K, a.Kp, a.out_box, o.rowexp, ecol, bs, a.alpha,  \
+                                                   a.beta, a.rdiv, a.rdiv_eps, a.Y);                                   \
+        break;
+        PK_TF(14) PK_TF(15) PK_TF(16) PK_TF(17) PK_TF(18) PK_TF(19) PK_TF(20)
+#undef PK_TF
+    default:
+        throw RuntimeError("i8_translate: unsupported modulus count " + std::to_string(nmod));
+    }
+    PK_CUDA(cudaGetLastError());
+    return 4;
 }
 
 int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {

@@ -31,14 +31,41 @@ struct I8Operators {          // residues of the stacked M2L operators (built on
 
 struct I8Settings {
     bool enabled = false;
+    bool trans = false;       // M2M / L2L / pseudo-inverses on the int8 pipe too (i8_translate)
     int nmod = 16, beta_a = 52, beta_b = 52; // accuracy study: profiles/r01_m2l_arith_study.md
     int64_t min_boxes = 1;    // levels with fewer boxes stay on the DMMA gather-GEMM
 };
-// PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes
+// PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes,
+// PKGPU_TRANS = i8 | dmma (default dmma; i8 requires PKGPU_M2L = i8)
 const I8Settings &i8_settings();
 
+// `tag` names the operator set's workspace buffers (one I8Operators per matrix stack)
 void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat, int K, int Kp, int nmod,
-                        int beta_a, cudaStream_t st);
+                        int beta_a, cudaStream_t st, const char *tag = "m2l");
+
+// The other dense translations on the int8 pipe, same residue arithmetic with a fixed-point
+// scale PER OUTPUT COLUMN (E_c from the column's own sources): valid when every source box
+// of the call feeds columns of one exponent, i.e. each source feeds one column (M2M:
+// children -> parent; pinv: identity) or each column has one source (L2L: parent -> child).
+//   Y[out(c)][r] = rdiv ? (rdiv[r] > eps ? S / rdiv[r] : 0) : beta Y + alpha S,
+//   S = sum_slot A[slot] X[src(slot, c)]
+// Replaces gather_gemm for M2M (src/fmm.cpp:544-548), L2L (:589-592) and pinv_apply
+// (src/linalg.cpp:78-87, two calls: U^T then V).
+struct I8TransArgs {
+    int K = 0, Kp = 0;
+    int ncols = 0;                   // multiple of kI8Tile
+    const int *out_box = nullptr;    // [ncols] output box, -1 padding
+    int nslots = 1;                  // = operator stack size (slot s uses matrix s)
+    const int *src = nullptr;        // [nslots * ld_src] source box, -1 none
+    int64_t ld_src = 0;
+    int64_t src_lo = 0, src_hi = 0;  // every source box lies in [src_lo, src_hi)
+    const double *X = nullptr;       // [box][Kp]
+    double *Y = nullptr;             // [box][Kp]
+    double alpha = 1.0, beta = 0.0;
+    const double *rdiv = nullptr;
+    double rdiv_eps = 0.0;
+};
+int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspace &ws, cudaStream_t st);
 
 constexpr int kI8MaxLevels = 16;
 

@@ -234,6 +234,8 @@ void OperatorCache::upload_factors(KifmmOps &ops, cudaStream_t st) {
     };
     build(ops.up, "up", ops.Ut_up, ops.V_up, ops.s_up);
     build(ops.dn, "dn", ops.Ut_dn, ops.V_dn, ops.s_dn);
+    // int8 residues of the factors are rebuilt from the new matrices on next use
+    ops.i8_ut_up.res = ops.i8_v_up.res = ops.i8_ut_dn.res = ops.i8_v_dn.res = nullptr;
     ops.factors_ready = true;
 }
 

@@ -36,6 +36,8 @@ struct KifmmOps {
     std::vector<int> h_slot_of_code, h_code_of_slot;
     std::map<std::pair<int, int>, double *> img; // (axes mask, ell) -> M_img Kp x Kp
     I8Operators i8;                         // M2L residues for the int8 tensor pipe (lazy)
+    I8Operators i8_m2m, i8_l2l;             // M2M / L2L residues (lazy, i8_translate)
+    I8Operators i8_ut_up, i8_v_up, i8_ut_dn, i8_v_dn; // pseudo-inverse factors (reset on upload)
     bool factors_ready = false, translations_ready = false;
 };
 

@@ -27,8 +27,9 @@ def host_residue_gemm(A, B, src, box0, zero_row):
     return R.astype(np.int64)
 
 
+# ncols >= 2048 runs the dual-tile kernel (two 128-box accumulators per operator tile)
 @pytest.mark.parametrize("Ki,nslots,ncols,nmod", [(128, 3, 256, 2), (384, 7, 512, 3), (896, 12, 256, 2),
-                                                  (1536, 5, 512, 1)])
+                                                  (1536, 5, 512, 1), (896, 9, 2048, 1), (384, 4, 2304, 2)])
 def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
     rng = np.random.default_rng(Ki * 31 + nslots)
     mods = pk.i8_moduli()[:nmod]
@@ -85,3 +86,23 @@ def test_int8_and_dmma_paths_agree_and_are_deterministic():
     assert rel_l2(r1, r3) <= 10 * float(g["self_spread"])
     with pytest.raises(ValueError):
         a.set_m2l("int8", nmod=14, beta_a=60, beta_b=60)  # range of the moduli exceeded
+
+
+@pytest.fixture(scope="module")
+def i8_all():
+    ctx = pk.Context(0)
+    ctx.set_m2l("int8_all", min_boxes=1)
+    yield ctx
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", EVAL_ALL)
+def test_evaluate_int8_translations_vs_reference(name, i8_all):
+    """M2M / L2L / pseudo-inverses on the int8 pipe too (i8_translate): same bar."""
+    g = load(f"eval_{name}.npz")
+    req, meta = golden_request(g)
+    res = pk.evaluate(req, context=i8_all)
+    rel = rel_l2(res.potentials, g["pot"])
+    tol = max(1e-10, 10 * float(g["self_spread"]))
+    print(f"{name} [int8 M2L + translations]: rel-L2 {rel:.3e} (tol {tol:.1e})")
+    assert rel <= tol

@@ -1,0 +1,4 @@
+R=r61
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 2>&1 | tail -15
+timeout 300 python tools/run_cfg2.py --evals 6 --warm 2 --stats > gpurun_out/${R}_stats.log 2>&1; grep -E "^m2m|^l2l|^pinv|timings" gpurun_out/${R}_stats.log | cut -c1-100
+PKGPU_TRANS=dmma timeout 300 python tools/run_cfg2.py --evals 6 --warm 2 --stats > gpurun_out/${R}_stats_dmma.log 2>&1; grep -E "^m2m|^l2l|^pinv|timings" gpurun_out/${R}_stats_dmma.log | cut -c1-100
