@@ -796,7 +796,10 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
                          &ctx.launches, partitioned ? Part.in : nullptr);
         prof.end(pm);
-        double *Q = ws.get<double>("Q", nb * Kp), *Tm = ws.get<double>("Tmp", nb * Kp),
+        // pseudo-inverse scratch: one level at a time (indexed by box id through a level offset)
+        int64_t maxlev = 1;
+        for (int l = 0; l <= T.depth; l++) maxlev = std::max<int64_t>(maxlev, T.level_off[l + 1] - T.level_off[l]);
+        double *Q = ws.get<double>("Q", nb * Kp), *Tm = ws.get<double>("Tmp", maxlev * Kp),
                *Pdn = ws.get<double>("phi_dn", nb * Kp);
         // phi_up lives in collective-visible memory when partitioned (summed over ranks)
         double *Pup = partitioned ? static_cast<double *>(part->alloc(part->user, nb * Kp * sizeof(double)))
@@ -849,7 +852,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_up");
-            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm, Pup, st, PP, Lay);
+            pinv_level(ctx, ops, true, lo, hi, l, Q, Tm - lo * Kp, Pup, st, PP, Lay);
             prof.end(pm);
         }
         if (partitioned) {
@@ -904,14 +907,20 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             a.big = Lay.i8_big[l] != 0;
             pm = prof.begin("m2l");
             int ps = prof.begin("m2l_prep");
-            const I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
+            I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
             prof.end(ps);
-            ps = prof.begin("m2l_i8");
-            ctx.launches += m2l_i8_gemm(ops.i8, a, w, ws, st);
-            prof.end(ps);
-            ps = prof.begin("m2l_crt");
-            ctx.launches += m2l_i8_finish(ops.i8, a, w, is.beta_b, st);
-            prof.end(ps);
+            for (int64_t w0 = 0; w0 < a.ncols; w0 += kI8Window) { // column windows bound the residue sums
+                const int64_t w1 = std::min<int64_t>(a.ncols, w0 + kI8Window);
+                ps = prof.begin("m2l_prep");
+                ctx.launches += m2l_i8_window(ops.i8, a, w, w0, w1, ws, st);
+                prof.end(ps);
+                ps = prof.begin("m2l_i8");
+                ctx.launches += m2l_i8_gemm(ops.i8, a, w, w0, w1, ws, st);
+                prof.end(ps);
+                ps = prof.begin("m2l_crt");
+                ctx.launches += m2l_i8_finish(ops.i8, a, w, w0, w1, is.beta_b, st);
+                prof.end(ps);
+            }
             prof.end(pm);
             for (int j = l; j <= l1; j++) i8_apps[j] = 1;
             l = l1 + 1;
@@ -980,7 +989,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 prof.end(pm);
             }
             pm = prof.begin("pinv_dn");
-            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm, Pdn, st, PP, Lay);
+            pinv_level(ctx, ops, false, lo, hi, l, Q, Tm - lo * Kp, Pdn, st, PP, Lay);
             prof.end(pm);
         }
         PK_CUDA(cudaEventRecord(ctx.ev[2], st));

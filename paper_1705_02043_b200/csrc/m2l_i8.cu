@@ -57,6 +57,7 @@ __constant__ float c_finv[kI8MaxModuli];            // 1 / m_t
 
 struct Params {
     CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
+    CUtensorMap tmX; // box residues (Ki, nmod * rows_per_mod) int8, box (128, 1), 128B swizzle (gather4)
     const int8_t *X; // box residues [nmod][rows_per_mod][Ki]
     const int *src;
     int64_t ld_src, box0;
@@ -338,21 +339,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
-// CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256): the pair shares one
-// 256-column tile (CTA r gathers boxes [256 p + 128 r, +128)) and one operator row tile,
-// each CTA staging HALF of the operator tile (Nt / 2 rows): per CTA and stage 16 KB
-// gathered + Nt/2 x 128 B operator instead of 16 KB + Nt x 128 B, i.e. a third less L2
-// traffic per MAC, and six stages instead of four.
-//   leader (rank 0) MMA thread: waits its "full" (own 64 cp.async + own TMA + one relay
-//     arrival from the peer), issues cta_group::2 MMAs, commits "empty" / "tfull" to both
-//     CTAs (multicast); waits "tempty" (4 local + 4 remote epilogue arrivals).
-//   peer (rank 1) MMA-warp thread: relay -- waits its local "full" (its cp.async + TMA),
-//     fences the generic-proxy writes into the async proxy, arrives on the leader's "full".
-// TMEM: both CTAs allocate 512 columns (cta_group::2); each CTA's epilogue reads its own
-// 128 lanes (its boxes) of the accumulator.
-constexpr int PAIR_NST = 6;
-constexpr int PAIR_B_BYTES = 128 * BKI; // half operator tile, Nt / 2 <= 128 rows
-constexpr int PAIR_STAGE = A_BYTES + PAIR_B_BYTES;
+// CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256), all loads by TMA:
+// the pair shares one 256-column tile (CTA r owns boxes [256 p + 128 r, +128)) and one
+// operator row tile. Per stage each CTA stages its 128 gathered box rows (32 TMA gather4
+// loads of 4 rows, hardware 128B swizzle) and HALF of the operator tile (Nt / 2 rows, one
+// TMA 3D load): 16 KB + Nt/2 x 128 B per CTA, i.e. 2/3 of the single-CTA bytes per MAC,
+// and up to eight stages deep (runtime ring). Every load signals the LEADER's "full" barrier (.cta_group::2
+// TMA, complete_tx across the pair), so no thread relays arrivals and no generic-proxy
+// writes need fencing.
+//   warp 0      producer (both CTAs): lane i issues the gather4 of rows 4i..4i+3, lane 0
+//               the operator half; the leader's lane 0 posts expect_tx for both CTAs
+//   warp 1      MMA issuer (leader, whole warp, elected lane): tcgen05.mma.cta_group::2
+//               M256 x Nt x K32 kind::i8, commits "empty" / "tfull" to both CTAs
+//   warps 2-5   epilogue (both CTAs, own 128 TMEM lanes = own boxes) as in m2l_i8_kernel;
+//               releases the accumulator on the leader's "tempty" (4 local + 4 remote)
+constexpr int PAIR_THREADS = 6 * 32;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -370,34 +371,41 @@ __device__ __forceinline__ uint32_t map_to_rank(const void *p, uint32_t rank) {
 __device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
+// TMA gather4 of four 128-byte rows into consecutive (swizzled) rows at dst, completing on
+// the pair leader's barrier `bar` (a shared::cluster address)
+__device__ __forceinline__ void gather4_pair(uint32_t dst, const CUtensorMap *map, int c0, int r0, int r1, int r2,
+                                             int r3, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::"
+                 "bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+                 : "memory");
+}
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     m2l_i8_pair_kernel(const __grid_constant__ Params p) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    int *s_epi = reinterpret_cast<int *>(smem + PAIR_NST * PAIR_STAGE); // [4 warps][32][33]
-    __shared__ __align__(8) uint64_t full[PAIR_NST], empty[PAIR_NST], tfull[2], tempty[2];
+    const int NS = p.nst, SB = p.stage_bytes; // runtime ring: 16 KB gathered rows + half operator tile
+    int *s_epi = reinterpret_cast<int *>(smem + NS * SB); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t full[NST_MAX], empty[NST_MAX], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
     const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    constexpr int NPT = NPROD * 32;
     const int half = p.Nt / 2;
     if (tid == 0) {
-        for (int s = 0; s < PAIR_NST; s++) {
-            // leader's "full": one arrival per producer warp of both CTAs + the expect_tx
-            // arrival (tx = both halves of the operator tile, each CTA's TMA signals it)
-            tma::mbar_init(&full[s], 2 * NPROD + 1);
-            tma::mbar_init(&empty[s], 1);
+        for (int s = 0; s < NS; s++) {
+            tma::mbar_init(&full[s], 1);  // leader: its expect_tx arrival (+ 60 KB of transactions)
+            tma::mbar_init(&empty[s], 1); // the leader's multicast MMA commit
         }
         for (int b = 0; b < 2; b++) {
             tma::mbar_init(&tfull[b], 1);
-            tma::mbar_init(&tempty[b], 8);
+            tma::mbar_init(&tempty[b], 8); // leader: 4 local + 4 remote epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == MMA_WARP) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
                          tma::smem_u32(&s_tmem))
                      : "memory");
@@ -410,8 +418,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
     int g = 0, jb = 0;
     const int npairs = p.coltiles / 2;
-    const int units = p.total_units; // (t, chunk, pair, rt)
-    for (int u = blockIdx.x / 2; u < units; u += gridDim.x / 2) {
+    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
         int v = u;
         const int rt = v % p.rowtiles;
         v /= p.rowtiles;
@@ -425,101 +432,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (n == 0) continue;
         const int *slots = p.tile_slots + pr * MAX_SLOTS;
         const int col0 = pr * 2 * TBM + (int)rank * TBM; // this CTA's 128 boxes
-        if (warp < NPROD) {
-            // ---------------- producers (both CTAs) ----------------
-            // cp.async groups per stage; a stage is published (proxy fence + one arrival per
-            // warp on the LEADER's "full") once this thread's copies of it have landed,
-            // PAIR_LAG stages behind the issue front
-            constexpr int PAIR_LAG = 2;
-            const int c = lane & 7, j0 = tid >> 3;
-            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
-            auto publish = [&](int gs) {
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                __syncwarp();
-                if (lane == 0) remote_arrive(map_to_rank(&full[gs % PAIR_NST], 0));
-            };
+        if (warp == 0) {
+            // ---------------- producer (both CTAs) ----------------
+            const uint32_t sbase = tma::smem_u32(smem);
+            int st = g % NS;
+            uint32_t ph = (g / NS) & 1;
+            const int rowbase = t * p.rows_per_mod;
             for (int si = s0; si < s1; si++) {
                 const int slot = slots[si];
-                const int *srow = p.src + (int64_t)slot * p.ld_src + col0;
-                int64_t off[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    const int b = srow[j0 + 8 * i];
-                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
-                }
+                const int4 b4 = *reinterpret_cast<const int4 *>(p.src + (int64_t)slot * p.ld_src + col0 + 4 * lane);
+                const int r0 = rowbase + (b4.x >= 0 ? (int)(b4.x - p.box0) : p.zero_row);
+                const int r1 = rowbase + (b4.y >= 0 ? (int)(b4.y - p.box0) : p.zero_row);
+                const int r2 = rowbase + (b4.z >= 0 ? (int)(b4.z - p.box0) : p.zero_row);
+                const int r3 = rowbase + (b4.w >= 0 ? (int)(b4.w - p.box0) : p.zero_row);
                 for (int kc = 0; kc < p.KC; kc++) {
-                    const int i_unit = (si - s0) * p.KC + kc, gi = g + i_unit, st = gi % PAIR_NST;
-                    tma::mbar_wait(&empty[st], ((gi / PAIR_NST) & 1) ^ 1);
-                    unsigned char *as = smem + st * PAIR_STAGE;
-                    if (tid == 0) {
-                        const uint32_t bar = map_to_rank(&full[st], 0);
+                    tma::mbar_wait(&empty[st], ph ^ 1);
+                    const uint32_t as = sbase + st * SB;
+                    const uint32_t bar = map_to_rank(&full[st], 0);
+                    if (lane == 0) {
                         if (leader)
                             asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::
                                              "r"(bar),
-                                         "r"(p.Nt * BKI)
+                                         "r"(2 * (A_BYTES + half * BKI))
                                          : "memory");
                         asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
-                                     "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tma::smem_u32(as + A_BYTES)),
+                                     "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(as + A_BYTES),
                                      "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
                                      "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + slot), "r"(bar)
                                      : "memory");
                     }
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int j = j0 + 8 * i;
-                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
-                    }
-                    asm volatile("cp.async.commit_group;\n" ::: "memory");
-                    if (i_unit >= PAIR_LAG) {
-                        asm volatile("cp.async.wait_group %0;\n" ::"n"(PAIR_LAG) : "memory");
-                        publish(gi - PAIR_LAG);
-                    }
+                    gather4_pair(as + lane * 4 * BKI, &p.tmX, kc * BKI, r0, r1, r2, r3, bar);
+                    if (++st == NS) st = 0, ph ^= 1;
                 }
             }
-            // drain: publish the unit's last stages
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-            for (int i_unit = max(0, n - PAIR_LAG); i_unit < n; i_unit++) publish(g + i_unit);
-        } else if (warp == MMA_WARP) {
-            if (lane == 0) {
-                if (leader) {
-                    // ---------------- MMA issuer (leader) ----------------
-                    const int buf = jb & 1;
-                    tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+        } else if (warp == 1) {
+            if (leader) {
+                // ---------------- MMA issuer (leader; whole warp, elected lane) ----------------
+                const int buf = jb & 1;
+                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dt = tmem + buf * 256;
+                int st = g % NS;
+                uint32_t ph = (g / NS) & 1;
+                const uint32_t sbase = tma::smem_u32(smem);
+                for (int i = 0; i < n; i++) {
+                    tma::mbar_wait(&full[st], ph);
                     tc_fence_after();
-                    const uint32_t dt = tmem + buf * 256;
-                    for (int i = 0; i < n; i++) {
-                        const int gi = g + i, st = gi % PAIR_NST;
-                        tma::mbar_wait(&full[st], (gi / PAIR_NST) & 1);
-                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                        tc_fence_after();
-                        const uint32_t a0 = tma::smem_u32(smem + st * PAIR_STAGE);
-                        const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
+                    const uint32_t a0 = sbase + st * SB;
+                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
 #pragma unroll
-                        for (int kk = 0; kk < BKI / 32; kk++)
-                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                                         "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
-                                         "r"((i > 0 || kk > 0) ? 1u : 0u));
-                        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
-                                     "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&empty[st])),
-                                     "h"((uint16_t)3)
-                                     : "memory");
-                    }
-                    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
-                                 "cluster.b64 [%0], %1;\n" ::"r"(tma::smem_u32(&tfull[buf])),
+                    for (int kk = 0; kk < BKI / 32; kk++)
+                        asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+                                     "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
+                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
+                    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                                 "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
                                  "h"((uint16_t)3)
                                  : "memory");
+                    if (++st == NS) st = 0, ph ^= 1;
                 }
+                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                             "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&tfull[buf])),
+                             "h"((uint16_t)3)
+                             : "memory");
             }
             __syncwarp();
         } else {
             // ---------------- epilogue (both CTAs: own 128 lanes = own boxes) ----------------
             const int buf = jb & 1, q = warp & 3;
-            int *tile = s_epi + (warp - MMA_WARP - 1) * 32 * EPI_PITCH;
+            int *tile = s_epi + (warp - 2) * 32 * EPI_PITCH;
             tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
             tc_fence_after();
             const int m = c_mod[t];
-            const float inv = 1.0f / (float)m;
+            const float inv = c_finv[t];
             const int cw = col0 + q * 32;
             const int r0 = rt * p.Nt;
             const int nr = min(p.Nt, p.Ki - r0);
@@ -550,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     tc_fence_before();
     cluster_sync();
-    if (warp == MMA_WARP) {
+    if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
     }
@@ -1007,7 +995,7 @@ __global__ void x_residue_kernel(const double *__restrict__ X, int64_t nbox, int
 //   Y[out(c)][r] += alpha 2^(e_r + E - beta_a - beta_b) S,  R = [t][c][r]
 template <int NM>
 __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki, int K, int Kp,
-                                   const int *__restrict__ out_box, const int *__restrict__ rowexp,
+                                   const int *__restrict__ out_box, int64_t col_off, const int *__restrict__ rowexp,
                                    const unsigned long long *__restrict__ mx, int beta_sum, I8Levels lv,
                                    double *__restrict__ Y) {
     const int64_t n = (int64_t)ncols * Ki;
@@ -1016,7 +1004,7 @@ __global__ void reconstruct_kernel(const int *__restrict__ R, int ncols, int Ki,
         if (r >= K) continue;
         const int ob = out_box[c];
         if (ob < 0) continue;
-        const int l = level_of(lv.col0, lv.n, c);
+        const int l = level_of(lv.col0, lv.n, c + col_off);
         const int E = level_exp(mx + l);
         const double alpha = lv.alpha[l];
         int x[NM], acc[NM], v[NM];
@@ -1318,6 +1306,18 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
+    if (mode == 1) {
+        if (p.Nt % 32 != 0) throw RuntimeError("i8 pair kernel: Nt / 2 must be a multiple of 16");
+        const cuuint64_t xd[2] = {(cuuint64_t)Ki, (cuuint64_t)nmod * rows_per_mod};
+        const cuuint64_t xs[1] = {(cuuint64_t)Ki};
+        const cuuint32_t xb[2] = {BKI, 1};
+        const cuuint32_t xe[2] = {1, 1};
+        const CUresult rx = encode_fn()(&p.tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t *>(B), xd, xs, xb, xe,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (rx != CUDA_SUCCESS)
+            throw CudaError("cuTensorMapEncodeTiled (int8 gather) failed (" + std::to_string((int)rx) + ")");
+    }
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
     if (mode == 3) {
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
@@ -1338,14 +1338,16 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
         m2l_i8_mc_kernel<<<grid, NTHREADS, smem, st>>>(p);
     } else if (pair) {
-        const size_t smem = (size_t)PAIR_NST * PAIR_STAGE + epi;
-        static bool cfg = false;
-        if (!cfg) {
+        p.stage_bytes = A_BYTES + (p.Nt / 2 * BKI + 1023) / 1024 * 1024;
+        p.nst = (int)std::min<size_t>(NST_MAX, (227 * 1024 - epi) / p.stage_bytes);
+        const size_t smem = (size_t)p.nst * p.stage_bytes + epi;
+        static size_t cfg = 0;
+        if (cfg < smem) {
             PK_CUDA(cudaFuncSetAttribute(m2l_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
+            cfg = smem;
         }
         const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
-        m2l_i8_pair_kernel<<<grid, NTHREADS, smem, st>>>(p);
+        m2l_i8_pair_kernel<<<grid, PAIR_THREADS, smem, st>>>(p);
     } else {
         // stage = 16 KB gathered rows + the operator tile rounded to 1 KB; as many stages as
         // the 227 KB of shared memory allow (the transposing epilogue costs 16.5 KB)
@@ -1409,34 +1411,47 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
     x_residue_kernel<<<(unsigned)std::min<int64_t>((w.rows * Ki + 255) / 256, 148 * 16), 256, 0, st>>>(
         a.X + box0 * a.Kp, nbox, a.K, a.Kp, Ki, nmod, beta_b, w.mx, a.lv, xres);
     w.xres = xres;
-    w.R = ws.get<int>("i8_R", (size_t)nmod * a.ncols * Ki);
-    PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)nmod * a.ncols * Ki * sizeof(int), st));
     upload_tables();
     w.mode = select_mode(a.big);
-    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below);
     PK_CUDA(cudaGetLastError());
-    if (launches) *launches += 2 + a.lv.n;
+    if (launches) *launches += 1 + a.lv.n;
     return w;
 }
 
-int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st) {
-    (void)ws;
-    if (a.ncols == 0) return 0;
-    launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src, a.ld_src, a.lv.box0[0],
-                a.nslots, a.ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st);
+int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
+                  cudaStream_t st) {
+    const int ncols = (int)(c1 - c0);
+    if (ncols <= 0) return 0;
+    if (c0 % kI8Tile != 0 || ncols % kI8Tile != 0) throw RuntimeError("m2l_i8: column window not tile aligned");
+    // residue sums of this column window only (the window bounds R: 4 nmod Ki bytes per column)
+    w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
+    PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
+    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below);
     return 1;
 }
 
-int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int beta_b, cudaStream_t st) {
-    if (a.ncols == 0) return 0;
-    const int64_t n = (int64_t)a.ncols * o.Ki;
+int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
+                cudaStream_t st) {
+    (void)ws;
+    const int ncols = (int)(c1 - c0);
+    if (ncols <= 0) return 0;
+    launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
+                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st);
+    return 1;
+}
+
+int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int64_t c0, int64_t c1,
+                  int beta_b, cudaStream_t st) {
+    const int ncols = (int)(c1 - c0);
+    if (ncols <= 0) return 0;
+    const int64_t n = (int64_t)ncols * o.Ki;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
     const int bs = o.beta_a + beta_b;
     switch (o.nmod) {
 #define PK_RC(NM)                                                                                                      \
     case NM:                                                                                                           \
-        reconstruct_kernel<NM><<<grid, 256, 0, st>>>(w.R, a.ncols, o.Ki, a.K, a.Kp, a.out_box, o.rowexp, w.mx, bs,     \
-                                                     a.lv, a.Y);                                                       \
+        reconstruct_kernel<NM><<<grid, 256, 0, st>>>(w.R, ncols, o.Ki, a.K, a.Kp, a.out_box + c0, c0, o.rowexp, w.mx, \
+                                                     bs, a.lv, a.Y);                                                   \
         break;
         PK_RC(14) PK_RC(15) PK_RC(16) PK_RC(17) PK_RC(18) PK_RC(19) PK_RC(20)
 #undef PK_RC
@@ -1488,9 +1503,13 @@ int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspa
 
 int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {
     int64_t l = 0;
-    const I8LevelWork w = m2l_i8_prepare(o, a, beta_b, ws, st, &l);
-    l += m2l_i8_gemm(o, a, w, ws, st);
-    l += m2l_i8_finish(o, a, w, beta_b, st);
+    I8LevelWork w = m2l_i8_prepare(o, a, beta_b, ws, st, &l);
+    for (int64_t c0 = 0; c0 < a.ncols; c0 += kI8Window) {
+        const int64_t c1 = std::min<int64_t>(a.ncols, c0 + kI8Window);
+        l += m2l_i8_window(o, a, w, c0, c1, ws, st);
+        l += m2l_i8_gemm(o, a, w, c0, c1, ws, st);
+        l += m2l_i8_finish(o, a, w, c0, c1, beta_b, st);
+    }
     return (int)l;
 }
 

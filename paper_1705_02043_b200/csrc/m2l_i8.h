@@ -22,6 +22,7 @@ namespace pkgpu {
 
 constexpr int kI8MaxModuli = 20;
 constexpr int kI8Tile = 256; // columns per tile: level column counts are padded to this
+constexpr int64_t kI8Window = 65536; // columns per M2L gemm/finish window (bounds the int32 residue sums)
 
 struct I8Operators {          // residues of the stacked M2L operators (built once per KifmmOps)
     int nmod = 0, beta_a = 0, Ki = 0, nmat = 0, K = 0;
@@ -102,13 +103,20 @@ struct I8LevelWork {
     int mode = 0;                                    // kernel variant (select_mode)
 };
 // The three steps of one level (separately timed by the stage profiler):
-//   prepare: level max, density residues, R = 0
-//   gemm:    the kind::i8 gather-GEMM (m2l_i8_kernel)
-//   finish:  CRT rebuild, Y += alpha 2^(...) S
+//   prepare: level max, density residues
+//   window:  R = 0, active-slot scan (column window)
+//   gemm:    the kind::i8 gather-GEMM (column window)
+//   finish:  CRT rebuild, Y += alpha 2^(...) S (column window)
 I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st,
                            int64_t *launches);
-int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, Workspace &ws, cudaStream_t st);
-int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int beta_b, cudaStream_t st);
+// gemm / finish act on the column window [c0, c1) (multiples of kI8Tile): R holds only the
+// window's residue sums, so big levels run in windows of at most kI8Window columns
+int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
+                  cudaStream_t st); // R = 0, active-slot scan of the window
+int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
+                cudaStream_t st);
+int m2l_i8_finish(const I8Operators &o, const I8LevelArgs &a, const I8LevelWork &w, int64_t c0, int64_t c1,
+                  int beta_b, cudaStream_t st);
 // All three; returns kernel launches.
 int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st);
 

@@ -1,0 +1,4 @@
+R=r68
+source tools/gpu_run45_fn.sh
+PKGPU_I8_PAIR=1 timeout 300 python -m pytest tests/test_gpu_i8.py -q -x -k "exact or all_levels" 2>&1 | tail -3
+PKGPU_I8_PAIR=1 ll pair

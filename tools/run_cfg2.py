@@ -36,9 +36,13 @@ def main():
     for _ in range(a.warm):
         pk.evaluate(req, context=ctx, out=out)
     ctx.set_profiling(a.stats)
+    # under `ncu --profile-from-start off` only the timed evaluates are captured
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
     for _ in range(a.evals):
         r = pk.evaluate(req, context=ctx, out=out)
     torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
     print("timings", r.timings, "launches", ctx.launches)
     if a.stats:
         for k, v in ctx.stage_stats().items():

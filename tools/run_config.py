@@ -88,6 +88,7 @@ def main():
     ctx.set_profiling(a.stats)
     ctx.reset_stats()
     ev = []
+    torch.cuda.cudart().cudaProfilerStart()  # `ncu --profile-from-start off` captures the timed evaluates
     for _ in range(a.evals):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -95,6 +96,7 @@ def main():
         e.record()
         torch.cuda.synchronize()
         ev.append(s.elapsed_time(e))
+    torch.cuda.cudart().cudaProfilerStop()
     info.update(ms_per_eval=float(np.mean(ev)), evals_per_s=len(pts) / (np.mean(ev) * 1e-3),
                 timings=r.timings.__dict__, free_gb=torch.cuda.mem_get_info()[0] / 1e9,
                 peak_alloc_gb=torch.cuda.max_memory_allocated() / 1e9)
