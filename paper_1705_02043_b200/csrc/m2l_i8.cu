@@ -66,6 +66,7 @@ struct Params {
     const int *tile_below; // [tile][MAX_SLOTS + 1]: active slots of the tile with index < s
     int nslots, by_index;
     int direct; // single-kernel epilogue stores the partial residues (one unit per output tile)
+    const uint8_t *half_mask; // dual kernel: [pair tile][slot] bit h = half h has a source
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
     int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
@@ -774,12 +775,15 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
             for (int si = s0; si < s1; si++) {
                 const int slot = slots[si];
                 const int *srow = p.src + (int64_t)slot * p.ld_src + colp;
+                // halves without a source for this slot are neither gathered nor multiplied
+                const int hm = p.half_mask[pr * MAX_SLOTS + slot]; // loaded alongside the rows (no extra latency)
+                int bx[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) bx[i] = srow[j0 + 16 * i];
                 int64_t off[16];
 #pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    const int b = srow[j0 + 16 * i];
-                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
-                }
+                for (int i = 0; i < 16; i++)
+                    off[i] = (int64_t)(bx[i] >= 0 ? (int)(bx[i] - p.box0) : p.zero_row) * p.Ki;
                 for (int kc = 0; kc < p.KC; kc++) {
                     const int gi = g + (si - s0) * p.KC + kc, st = gi % DUAL_NST;
                     tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
@@ -791,7 +795,8 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
-                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                        if ((hm >> (i >> 3)) & 1)
+                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                     }
                     tma::cp_async_mbar_arrive(&full[st]);
                 }
@@ -804,20 +809,35 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
             int st = g % DUAL_NST;
             uint32_t ph = (g / DUAL_NST) & 1;
             const uint32_t sbase = tma::smem_u32(smem);
-            for (int i = 0; i < n; i++) {
+            bool started0 = false, started1 = false; // first MMA of a half overwrites its accumulator
+            const uint8_t *hmt = p.half_mask + pr * MAX_SLOTS;
+            int hm = hmt[slots[s0]];
+            int hm_next = s0 + 1 < s1 ? hmt[slots[s0 + 1]] : 0;
+            for (int i = 0, kc = 0, si = s0; i < n; i++) {
                 tma::mbar_wait(&full[st], ph);
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 tc_fence_after();
                 const uint32_t a0 = sbase + st * DUAL_STAGE;
                 const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES), bd = sw128_desc(a0 + DUAL_A_BYTES);
+                // REDUX writes a uniform register: the conditional MMAs stay on the uniform datapath
+                // (a branch on a loaded value would bring back the per-MMA R2UR waterfall)
+                const unsigned hu = __reduce_or_sync(0xffffffffu, (unsigned)hm);
+                const bool on0 = (hu & 1u) != 0, on1 = (hu & 2u) != 0;
 #pragma unroll
                 for (int kk = 0; kk < BKI / 32; kk++) {
-                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                    mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, acc);
-                    mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                    if (on0) mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, (started0 || kk > 0) ? 1u : 0u);
+                    if (on1) mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, (started1 || kk > 0) ? 1u : 0u);
                 }
+                started0 |= on0;
+                started1 |= on1;
                 commit_elect(&empty[st]);
                 if (++st == DUAL_NST) st = 0, ph ^= 1;
+                if (++kc == p.KC) { // next slot: its mask was loaded a slot ahead
+                    kc = 0;
+                    si++;
+                    hm = hm_next;
+                    hm_next = si + 1 < s1 ? hmt[slots[si + 1]] : 0;
+                }
             }
             commit_elect(&tfull);
             __syncwarp();
@@ -831,7 +851,11 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
             const float inv = 1.0f / (float)m;
             const int r0 = rt * p.Nt;
             const int nr = min(p.Nt, p.Ki - r0);
+            int used = 0; // halves that received an MMA in this unit (others hold stale TMEM)
+            for (int si = s0 + lane; si < s1; si += 32) used |= p.half_mask[pr * MAX_SLOTS + slots[si]];
+            for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
             for (int h = 0; h < 2; h++) {
+                if (!((used >> h) & 1)) continue;
                 int *Rt = p.R + ((int64_t)t * p.ncols + colp + h * TBM + q * 32) * p.Ki + r0;
                 for (int j0 = 0; j0 < p.Nt; j0 += 32) {
                     uint32_t vv[32];
@@ -867,15 +891,24 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
 }
 
 // active slots per column tile of `bn` columns, in slot order
+// half_mask (bn = 256, pair tiles): bit h set when the 128-column half h has a source
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
-                                 int *tile_nact, int *tile_below) {
+                                 int *tile_nact, int *tile_below, uint8_t *half_mask) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
-        bool any = false;
-        for (int j = lane; j < bn; j += 32) any |= src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0;
-        any = __any_sync(0xffffffffu, any);
-        if (lane == 0) flag[s] = any ? 1 : 0;
+        bool h0 = false, h1 = false;
+        for (int j = lane; j < bn; j += 32) {
+            const bool a = src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0;
+            if (j < TBM) h0 |= a;
+            else h1 |= a;
+        }
+        h0 = __any_sync(0xffffffffu, h0);
+        h1 = __any_sync(0xffffffffu, h1);
+        if (lane == 0) {
+            flag[s] = (h0 || h1) ? 1 : 0;
+            if (half_mask) half_mask[ct * MAX_SLOTS + s] = (uint8_t)((h0 ? 1 : 0) | (h1 ? 2 : 0));
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1225,32 +1258,38 @@ namespace {
 
 // kernel variant per launch: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
 // (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
-// (m2l_i8_dual_kernel). Default: dual for big levels (octant groups fill 256-column pair
-// tiles; 8 MMAs per pipeline stage and half the operator bytes per MAC), single for the
-// small-level run. PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
+// (m2l_i8_dual_kernel). Default: dual everywhere (8 MMAs per pipeline stage, half the
+// operator bytes per MAC; a pair tile's halves with no source for a slot skip its gather
+// and MMA). i8_gather_gemm (tests) keeps the single kernel below 2048 columns so both stay
+// covered. PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
 int select_mode(bool big) {
     static const int forced = [] {
         const char *e = std::getenv("PKGPU_I8_PAIR");
         return e ? std::max(0, std::min(3, std::atoi(e))) : -1;
     }();
-    return forced >= 0 ? forced : (big ? 3 : 0);
+    (void)big; // measured: with per-half slot masks the dual kernel also wins on the small-level run
+    return forced >= 0 ? forced : 3;
 }
 int column_tile(int mode) { return mode != 0 ? 2 * TBM : TBM; }
 
 // active-slot lists per column tile (ncols / column_tile(mode) tiles)
 void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode, Workspace &ws, cudaStream_t st,
-                int **tslots, int **tnact, int **tbelow) {
+                int **tslots, int **tnact, int **tbelow, uint8_t **thmask = nullptr) {
     const int bn = column_tile(mode), tiles = ncols / bn;
     *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
     *tnact = ws.get<int>("i8_tile_nact", tiles);
     *tbelow = ws.get<int>("i8_tile_below", (size_t)tiles * (MAX_SLOTS + 1));
-    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow);
+    uint8_t *hmask = mode == 3 ? ws.get<uint8_t>("i8_tile_hmask", (size_t)tiles * MAX_SLOTS) : nullptr;
+    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask);
+    if (thmask) *thmask = hmask;
     PK_CUDA(cudaGetLastError());
 }
 
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
-                 const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false) {
+                 const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false,
+                 const uint8_t *thmask = nullptr) {
+    if (mode == 3 && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernel needs the half masks");
     const int num_sms = sm_count();
     const bool pair = mode != 0;
     Params p;
@@ -1292,6 +1331,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.tile_nact = tnact;
     p.tile_below = tbelow;
     p.nslots = nslots;
+    p.half_mask = thmask;
     // slot-index windows for the small-level run (operator reuse through L2 across its
     // tiles); equal list shares for the dual-tile big levels (balanced static schedule)
     static const int by_index_env = std::getenv("PKGPU_I8_BYINDEX") ? std::atoi(std::getenv("PKGPU_I8_BYINDEX")) : -1;
@@ -1384,10 +1424,11 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
         throw RuntimeError("i8_gather_gemm: bad shape");
     upload_tables();
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
-    const int mode = select_mode(ncols >= 2048);
-    scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow);
+    const int mode = ncols >= 2048 ? select_mode(true) : 0;
+    uint8_t *thmask = nullptr;
+    scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
-                tbelow, mode, st);
+                tbelow, mode, st, false, thmask);
     return 2;
 }
 
@@ -1426,7 +1467,8 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     // residue sums of this column window only (the window bounds R: 4 nmod Ki bytes per column)
     w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
-    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below);
+    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below,
+               &w.tile_hmask);
     return 1;
 }
 
@@ -1436,7 +1478,8 @@ int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int6
     const int ncols = (int)(c1 - c0);
     if (ncols <= 0) return 0;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
-                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st);
+                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st, false,
+                w.tile_hmask);
     return 1;
 }
 

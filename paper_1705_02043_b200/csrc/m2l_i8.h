@@ -100,6 +100,7 @@ struct I8LevelWork {
     int64_t rows = 0;
     int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile
     int *tile_below = nullptr;                       // per tile: active slots below each slot index
+    uint8_t *tile_hmask = nullptr;                   // dual kernel: per (pair tile, slot) active halves
     int mode = 0;                                    // kernel variant (select_mode)
 };
 // The three steps of one level (separately timed by the stage profiler):
