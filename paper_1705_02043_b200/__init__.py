@@ -409,7 +409,7 @@ class Context:
     def stage_stats(self):
         """{stage: dict(seconds, units, flops, launches)} accumulated while profiling."""
         out = {}
-        for st in self.STAGES + ("u_pairs",):
+        for st in self.STAGES + ("u_pairs", "m2l_mma_rows"):
             sec, un, fl, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
             if lib().pkgpu_context_stage_stats(self._h, st.encode(), ctypes.byref(sec), ctypes.byref(un),
                                                ctypes.byref(fl), ctypes.byref(ln)) == 0:

@@ -871,6 +871,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         ctx.launches += ctx.lists.x.count ? 1 : 0;
         prof.end(pm);
         int i8_apps[kMaxLevels + 1] = {0}; // levels whose M2L ran on the int8 pipe
+        bool mma_rows_zeroed = false;
         // ---- M2L on the int8 pipe: every int8 level in ONE launch (M2L reads only phi_up,
         // so it can precede the L2L chain; one pass streams each operator tile once for all
         // levels), in runs of consecutive int8 levels ----
@@ -905,6 +906,11 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             a.X = Pup;
             a.Y = Q;
             a.big = Lay.i8_big[l] != 0;
+            if (ctx.profiling) {
+                a.mma_rows = ws.get<unsigned long long>("i8_mma_rows", 1);
+                if (!mma_rows_zeroed) PK_CUDA(cudaMemsetAsync(a.mma_rows, 0, sizeof(unsigned long long), st));
+                mma_rows_zeroed = true;
+            }
             pm = prof.begin("m2l");
             int ps = prof.begin("m2l_prep");
             I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
@@ -1065,6 +1071,13 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             }
             if (v_i8 > 0) {
                 prof.work("m2l_i8", v_i8, 2.0 * ctx.i8.nmod * K * K);
+                if (mma_rows_zeroed) { // MMA rows issued vs V applications (tile padding / union waste)
+                    unsigned long long rows = 0;
+                    PK_CUDA(cudaMemcpyAsync(&rows, ws.get<unsigned long long>("i8_mma_rows", 1), sizeof rows,
+                                            cudaMemcpyDeviceToHost, st));
+                    PK_CUDA(cudaStreamSynchronize(st));
+                    prof.work("m2l_mma_rows", (double)rows, 0.0);
+                }
                 prof.work("m2l_prep", v_i8, 0.0);
                 prof.work("m2l_crt", v_i8, 0.0);
             }

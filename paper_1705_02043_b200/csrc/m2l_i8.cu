@@ -1459,6 +1459,15 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
     return w;
 }
 
+// profiling: MMA rows issued (128 per active half per slot) -- padding and union waste show
+// against the V-list applications
+__global__ void mma_rows_kernel(const uint8_t *__restrict__ hmask, int nslots, unsigned long long *rows) {
+    int c = 0;
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) c += __popc(hmask[blockIdx.x * MAX_SLOTS + s]);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(rows, 128ull * c);
+}
+
 int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
                   cudaStream_t st) {
     const int ncols = (int)(c1 - c0);
@@ -1469,6 +1478,11 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
     scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below,
                &w.tile_hmask);
+    if (a.mma_rows && w.tile_hmask) {
+        mma_rows_kernel<<<ncols / (2 * TBM), 32, 0, st>>>(w.tile_hmask, a.nslots, a.mma_rows);
+        PK_CUDA(cudaGetLastError());
+        return 2;
+    }
     return 1;
 }
 

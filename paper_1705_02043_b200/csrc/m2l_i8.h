@@ -92,6 +92,7 @@ struct I8LevelArgs {
     const double *X = nullptr;    // [box][Kp]
     double *Y = nullptr;          // [box][Kp]: Y += alpha_l * sum_slot M X
     bool big = false;             // one large level: the dual-tile kernel (see select_mode)
+    unsigned long long *mma_rows = nullptr; // profiling: += 128 x active (pair tile, slot, half) triples
 };
 struct I8LevelWork {
     const int8_t *xres = nullptr;     // [nmod][nbox + 1][Ki] density residues (last row zero)
