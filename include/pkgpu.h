@@ -166,6 +166,37 @@ pkgpu_status pkgpu_operator_matrix(const pkgpu_operator *op, double *out);
 /* CRC-64/XZ (src/periodize.cpp:40-55). */
 uint64_t pkgpu_crc64(const void *data, size_t len);
 
+/* Ewald / image-sum parameters (EwaldParams, include/pkifmm/refsum.hpp:21-27). */
+typedef struct {
+    double xi;           /* 8.0 */
+    int real_shells;     /* 2 */
+    int wave_cutoff;     /* 64 */
+    long long n_images;  /* 1000000 (direct singly periodic sums) */
+} pkgpu_ewald;
+/* solve_m2l (include/pkifmm/periodize.hpp:42; src/periodize.cpp:57-158) on the GPU: K^{P,F}
+ * on the inner root surface by per-pair Ewald / image sums, T = pinv(a_dn) K^{P,F} with
+ * the context's downward factors, backward residual gate 1e-11 (gated = 0 skips the gate
+ * and records residual_max = -1, the ungated operator of SURVEY §8c cfg 4). Singly
+ * periodic along x (cfg 1) is built along z and permuted like the reference's SP-x recipe.
+ * Errors: ConfigError for unsupported (kernel, periodicity); RuntimeError past the gate. */
+pkgpu_status pkgpu_operator_solve(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup, int p,
+                                  const pkgpu_ewald *params, int gated, pkgpu_operator **op, char *err,
+                                  size_t errlen);
+/* save_operator (include/pkifmm/periodize.hpp:61; src/periodize.cpp:189-229): PKM2L file,
+ * same header keys and payload CRC as the reference writes. */
+pkgpu_status pkgpu_operator_save(const pkgpu_operator *op, const char *path, char *err, size_t errlen);
+/* periodic_block / kpf_block (include/pkifmm/refsum.hpp:68-72): out[(kt i + a)(ks ns) + ks j
+ * + b] = K^P(t_i, s_j) (far_only: K^{P,F}); host arrays, xyz interleaved. */
+pkgpu_status pkgpu_periodic_block(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup, const pkgpu_ewald *params,
+                                  int far_only, const double *targets, int64_t nt, const double *sources, int64_t ns,
+                                  double *out, char *err, size_t errlen);
+/* oracle_system_eval (include/pkifmm/refsum.hpp:88; src/refsum.cpp:757-770): q_t = sum_s
+ * K^P(x_t, y_s) phi_s on the GPU, compatibility checked first (ConfigError). */
+pkgpu_status pkgpu_oracle_system_eval(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup,
+                                      const pkgpu_ewald *params, const double *sources, int64_t ns,
+                                      const double *strengths, const double *targets, int64_t nt, double *out,
+                                      char *err, size_t errlen);
+
 /* ---- KIFMM operators (src/fmm.cpp:180-236) --------------------------------------- */
 /* Parity mode: inject SVD factors in the reference's layout (SvdFactors,
  * include/pkifmm/linalg.hpp:45-53: u m x k row-major, sigma k, vt k x n row-major) for

@@ -71,6 +71,11 @@ class _Timings(ctypes.Structure):
                 ("far", ctypes.c_double)]
 
 
+class _Ewald(ctypes.Structure):
+    _fields_ = [("xi", ctypes.c_double), ("real_shells", ctypes.c_int), ("wave_cutoff", ctypes.c_int),
+                ("n_images", ctypes.c_longlong)]
+
+
 class _Compat(ctypes.Structure):
     _fields_ = [("ok", ctypes.c_int), ("residual", ctypes.c_double), ("violated", ctypes.c_char * 96)]
 
@@ -111,6 +116,13 @@ _SIGNATURES = {
     "pkgpu_operator_relabel": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(_Setup)]),
     "pkgpu_operator_matrix": (ctypes.c_int, [P, P]),
     "pkgpu_crc64": (ctypes.c_uint64, [P, SZ]),
+    "pkgpu_operator_solve": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(_Setup), ctypes.c_int,
+                                            ctypes.POINTER(_Ewald), ctypes.c_int, ctypes.POINTER(P), ERR, SZ]),
+    "pkgpu_operator_save": (ctypes.c_int, [P, ctypes.c_char_p, ERR, SZ]),
+    "pkgpu_periodic_block": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(_Setup), ctypes.POINTER(_Ewald),
+                                            ctypes.c_int, P, I64, P, I64, P, ERR, SZ]),
+    "pkgpu_oracle_system_eval": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(_Setup), ctypes.POINTER(_Ewald), P,
+                                                I64, P, P, I64, P, ERR, SZ]),
     "pkgpu_set_kifmm_factors": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, ERR, SZ]),
     "pkgpu_get_kifmm_factors": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P, ERR, SZ]),
     "pkgpu_kifmm_matrix": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -339,6 +351,63 @@ class PeriodizingOperator:
         _check(lib().pkgpu_operator_create(int(kernel.type), ctypes.byref(s), p, _ptr(m), m.shape[0],
                                            ctypes.byref(h), err, 1024), err)
         return PeriodizingOperator(h.value)
+
+
+class EwaldParams:
+    """EwaldParams (include/pkifmm/refsum.hpp:21-27)."""
+
+    def __init__(self, xi=8.0, real_shells=2, wave_cutoff=64, n_images=1_000_000):
+        self.xi, self.real_shells, self.wave_cutoff, self.n_images = xi, real_shells, wave_cutoff, n_images
+
+    def _c(self):
+        return _Ewald(float(self.xi), int(self.real_shells), int(self.wave_cutoff), int(self.n_images))
+
+
+def solve_m2l(kernel: KernelSpec, setup: PeriodicSetup, p: int, params: Optional[EwaldParams] = None,
+              gated: bool = True, context: Optional["Context"] = None) -> PeriodizingOperator:
+    """solve_m2l (include/pkifmm/periodize.hpp:42) on the GPU: K^{P,F} on the inner root
+    surface, T = pinv(a_dn) K^{P,F}, backward-residual gate 1e-11 (gated=False: the ungated
+    operator, residual_max = -1). ConfigError for unsupported (kernel, periodicity)."""
+    ctx = context or default_context()
+    h, err, s, e = ctypes.c_void_p(), _errbuf(), setup._c(), (params or EwaldParams())._c()
+    _check(lib().pkgpu_operator_solve(ctx._h, int(kernel.type), ctypes.byref(s), int(p), ctypes.byref(e),
+                                      1 if gated else 0, ctypes.byref(h), err, 1024), err)
+    return PeriodizingOperator(h.value)
+
+
+def save_operator(op: PeriodizingOperator, path) -> None:
+    """save_operator (include/pkifmm/periodize.hpp:61): PKM2L with the reference's header."""
+    err = _errbuf()
+    _check(lib().pkgpu_operator_save(op._h, str(path).encode(), err, 1024), err)
+
+
+def periodic_block(kernel: KernelSpec, setup: PeriodicSetup, targets, sources, far_only=False,
+                   params: Optional[EwaldParams] = None, context: Optional["Context"] = None):
+    """periodic_block / kpf_block (include/pkifmm/refsum.hpp:68-72) on the GPU."""
+    ctx = context or default_context()
+    t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+    sr = np.ascontiguousarray(sources, dtype=np.float64).reshape(-1, 3)
+    k = kernel.ks
+    out = np.empty((k * len(t), k * len(sr)))
+    err, s, e = _errbuf(), setup._c(), (params or EwaldParams())._c()
+    _check(lib().pkgpu_periodic_block(ctx._h, int(kernel.type), ctypes.byref(s), ctypes.byref(e),
+                                      1 if far_only else 0, _ptr(t), len(t), _ptr(sr), len(sr), _ptr(out), err,
+                                      1024), err)
+    return out
+
+
+def oracle_system_eval(kernel: KernelSpec, setup: PeriodicSetup, sources, strengths, targets,
+                       params: Optional[EwaldParams] = None, context: Optional["Context"] = None):
+    """oracle_system_eval (include/pkifmm/refsum.hpp:88): q_t = sum_s K^P(x_t, y_s) phi_s."""
+    ctx = context or default_context()
+    sr = np.ascontiguousarray(sources, dtype=np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(strengths, dtype=np.float64).reshape(-1)
+    t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(kernel.kt * len(t))
+    err, s, e = _errbuf(), setup._c(), (params or EwaldParams())._c()
+    _check(lib().pkgpu_oracle_system_eval(ctx._h, int(kernel.type), ctypes.byref(s), ctypes.byref(e), _ptr(sr),
+                                          len(sr), _ptr(q), _ptr(t), len(t), _ptr(out), err, 1024), err)
+    return out
 
 
 def load_operator(path) -> PeriodizingOperator:

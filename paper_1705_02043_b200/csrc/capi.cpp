@@ -1,6 +1,8 @@
 // extern "C" boundary of libpkgpu (include/pkgpu.h). Translates C++ exceptions into
 // status codes + messages, owns the PKM2L operator reader, and hosts the synthetic
 // workload generator.
+#include <array>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -9,6 +11,8 @@
 #include <sstream>
 
 #include "context.h"
+#include "gemm.h"
+#include "periodize.h"
 
 using namespace pkgpu;
 
@@ -207,6 +211,14 @@ pkgpu_operator *load_pkm2l(const std::string &path) {
     op->p = std::stoi(at(h, "p").text);
     op->method = method_from(at(h, "method").text);
     op->residual_max = std::stod(at(h, "residual_max").text);
+    if (h.obj.count("params")) {
+        const JVal &pa = at(h, "params");
+        if (pa.obj.count("xi")) op->xi = std::stod(at(pa, "xi").text);
+        if (pa.obj.count("real_shells")) op->real_shells = std::stoi(at(pa, "real_shells").text);
+        if (pa.obj.count("wave_cutoff")) op->wave_cutoff = std::stoi(at(pa, "wave_cutoff").text);
+        if (pa.obj.count("n_images")) op->n_images = std::stoll(at(pa, "n_images").text);
+    }
+    if (h.obj.count("created")) op->created = at(h, "created").text;
     const int rows = std::stoi(at(h, "rows").text), cols = std::stoi(at(h, "cols").text);
     const int ks = op->kernel == PKGPU_LAPLACE ? 1 : 3;
     const int n = surface_point_count(op->p);
@@ -401,6 +413,200 @@ pkgpu_status pkgpu_operator_matrix(const pkgpu_operator *op, double *out) {
 }
 
 uint64_t pkgpu_crc64(const void *data, size_t len) { return crc64_xz(data, len); }
+
+namespace {
+
+EwaldSettings ewald_from(const pkgpu_ewald *e) {
+    EwaldSettings s;
+    if (e) {
+        s.xi = e->xi;
+        s.real_shells = e->real_shells;
+        s.wave_cutoff = e->wave_cutoff;
+        s.n_images = e->n_images;
+    }
+    if (!(s.xi > 0.0) || s.real_shells < 0 || s.wave_cutoff < 1 || s.n_images < 1)
+        throw InvalidArgument("EwaldParams: xi > 0, real_shells >= 0, wave_cutoff >= 1, n_images >= 1 required");
+    return s;
+}
+
+// shortest round-trip decimal, with a ".0" on integral values (nlohmann's number format)
+std::string json_double(double v) {
+    char buf[40];
+    for (int prec = 1; prec <= 17; prec++) {
+        std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string s(buf);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+
+std::string json_str(const std::string &v) { return "\"" + v + "\""; }
+
+const char *kernel_label(int k) { return k == PKGPU_LAPLACE ? "laplace" : "stokeslet"; }
+const char *periodicity_label(int p) {
+    switch (p) {
+    case PKGPU_SP: return "sp";
+    case PKGPU_DP: return "dp";
+    case PKGPU_TP: return "tp";
+    }
+    return "none";
+}
+
+} // namespace
+
+pkgpu_status pkgpu_operator_solve(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup, int p,
+                                  const pkgpu_ewald *params, int gated, pkgpu_operator **op, char *err,
+                                  size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        PK_CUDA(cudaSetDevice(ctx->device));
+        if (kernel != PKGPU_LAPLACE && kernel != PKGPU_STOKESLET) throw InvalidArgument("unknown kernel");
+        if (p < 2) throw InvalidArgument("surface grid requires p >= 2");
+        const EwaldSettings e = ewald_from(params);
+        pkgpu_setup s = *setup;
+        // singly periodic along x: build along z (the reference's SP sum) and permute the
+        // surface indices by the axis rotation (x, y, z) -> (y, z, x) (cfg 1)
+        const bool spx = s.periodicity == PKGPU_SP && s.axes[0] && !s.axes[1] && !s.axes[2];
+        if (s.periodicity == PKGPU_SP && !spx && !(s.axes[2] && !s.axes[0] && !s.axes[1]))
+            throw InvalidArgument("solve_m2l: singly periodic operators are built along z or x");
+        if (spx) {
+            if (kernel != PKGPU_LAPLACE) throw InvalidArgument("spx permutation implemented for scalar kernels only");
+            s.axes[0] = 0, s.axes[2] = 1;
+        }
+        PeriodicSolve r = solve_periodizing_operator(*ctx, kernel, s, p, e, gated != 0);
+        auto o = std::make_unique<pkgpu_operator>();
+        o->kernel = kernel;
+        o->setup = *setup;
+        o->p = p;
+        o->dim = r.dim;
+        if (spx) {
+            const auto g = surface_grid(p);
+            const int n = (int)g.size() / 3;
+            std::map<std::array<int, 3>, int> at;
+            for (int i = 0; i < n; i++) at[{g[3 * i], g[3 * i + 1], g[3 * i + 2]}] = i;
+            std::vector<int> pi(n);
+            for (int i = 0; i < n; i++) pi[i] = at.at({g[3 * i + 1], g[3 * i + 2], g[3 * i]});
+            o->matrix.resize(r.matrix.size());
+            for (int i = 0; i < n; i++)
+                for (int j = 0; j < n; j++) o->matrix[(size_t)i * n + j] = r.matrix[(size_t)pi[i] * n + pi[j]];
+        } else {
+            o->matrix = std::move(r.matrix);
+        }
+        o->method = r.method;
+        o->residual_max = r.residual_max;
+        o->xi = e.xi;
+        o->real_shells = e.real_shells;
+        o->wave_cutoff = e.wave_cutoff;
+        o->n_images = e.n_images;
+        o->created = iso_now();
+        o->crc = crc64_xz(o->matrix.data(), o->matrix.size() * sizeof(double));
+        *op = o.release();
+    });
+}
+
+pkgpu_status pkgpu_operator_save(const pkgpu_operator *op, const char *path, char *err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!op) throw InvalidArgument("save_operator: null operator");
+        const int ks = op->kernel == PKGPU_LAPLACE ? 1 : 3;
+        std::string axes;
+        for (int a = 0; a < 3; a++)
+            if (op->setup.axes[a]) axes += "xyz"[a];
+        const uint64_t crc = crc64_xz(op->matrix.data(), op->matrix.size() * sizeof(double));
+        // keys in the order the reference's (sorted) JSON object writes them
+        std::ostringstream h;
+        h << "{\"cols\":" << op->dim << ",\"created\":" << json_str(op->created) << ",\"ell\":" << op->setup.ell
+          << ",\"format\":\"pkm2l\",\"inner_scale\":" << json_double(1.05) << ",\"kernel\":"
+          << json_str(kernel_label(op->kernel)) << ",\"ks\":" << ks << ",\"kt\":" << ks
+          << ",\"method\":" << json_str(method_label(op->method)) << ",\"n\":" << surface_point_count(op->p)
+          << ",\"outer_scale\":" << json_double(2.95) << ",\"p\":" << op->p << ",\"params\":{\"n_images\":"
+          << op->n_images << ",\"real_shells\":" << op->real_shells << ",\"wave_cutoff\":" << op->wave_cutoff
+          << ",\"xi\":" << json_double(op->xi) << "},\"payload_crc64\":" << crc
+          << ",\"periodic_axes\":" << json_str(axes) << ",\"periodicity\":"
+          << json_str(periodicity_label(op->setup.periodicity)) << ",\"residual_max\":"
+          << json_double(op->residual_max) << ",\"rows\":" << op->dim << ",\"version\":1}";
+        const std::string hs = h.str();
+        std::ofstream f(path, std::ios::binary | std::ios::trunc);
+        if (!f) throw RuntimeError(std::string("save_operator: cannot open ") + path);
+        static const char kMagic[6] = {'P', 'K', 'M', '2', 'L', '\x01'};
+        f.write(kMagic, 6);
+        char lenbuf[8];
+        for (int i = 0; i < 8; i++) lenbuf[i] = static_cast<char>((hs.size() >> (8 * i)) & 0xff);
+        f.write(lenbuf, 8);
+        f.write(hs.data(), static_cast<std::streamsize>(hs.size()));
+        f.write(reinterpret_cast<const char *>(op->matrix.data()),
+                static_cast<std::streamsize>(op->matrix.size() * sizeof(double)));
+        if (!f) throw RuntimeError(std::string("save_operator: write failed for ") + path);
+    });
+}
+
+pkgpu_status pkgpu_periodic_block(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup, const pkgpu_ewald *params,
+                                  int far_only, const double *targets, int64_t nt, const double *sources, int64_t ns,
+                                  double *out, char *err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        PK_CUDA(cudaSetDevice(ctx->device));
+        const EwaldSettings e = ewald_from(params);
+        const int k = kernel == PKGPU_LAPLACE ? 1 : 3;
+        cudaStream_t st = ctx->stream;
+        double *t = ctx->ws.get<double>("pb_t", 3 * nt + 1), *s = ctx->ws.get<double>("pb_s", 3 * ns + 1);
+        double *o = ctx->ws.get<double>("pb_o", (size_t)k * nt * k * ns + 1);
+        PK_CUDA(cudaMemcpyAsync(t, targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaMemcpyAsync(s, sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        periodic_block_device(kernel, *setup, e, far_only != 0, t, (int)nt, s, (int)ns, o, k * ns, st);
+        PK_CUDA(cudaMemcpyAsync(out, o, (size_t)k * nt * k * ns * sizeof(double), cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        ctx->launches += 1;
+    });
+}
+
+pkgpu_status pkgpu_oracle_system_eval(pkgpu_context *ctx, int kernel, const pkgpu_setup *setup,
+                                      const pkgpu_ewald *params, const double *sources, int64_t ns,
+                                      const double *strengths, const double *targets, int64_t nt, double *out,
+                                      char *err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::lock_guard<std::mutex> lock(ctx->mtx);
+        PK_CUDA(cudaSetDevice(ctx->device));
+        const EwaldSettings e = ewald_from(params);
+        periodic_method(kernel, *setup); // ConfigError for unsupported combinations first
+        const int k = kernel == PKGPU_LAPLACE ? 1 : 3;
+        // check_compatibility (src/refsum.cpp:733-756)
+        if (!(kernel == PKGPU_STOKESLET && setup->periodicity == PKGPU_TP)) {
+            double abs_total = 0.0, worst = 0.0;
+            for (int64_t i = 0; i < k * ns; i++) abs_total += std::fabs(strengths[i]);
+            for (int a = 0; a < k; a++) {
+                double sum = 0.0;
+                for (int64_t i = 0; i < ns; i++) sum += strengths[i * k + a];
+                worst = std::max(worst, std::fabs(sum));
+            }
+            if (worst > 1e-12 * abs_total) {
+                char msg[256];
+                std::snprintf(msg, sizeof msg, "oracle_system_eval: compatibility violation (%s, residual=%f)",
+                              kernel == PKGPU_LAPLACE ? "neutrality: net charge must vanish"
+                                                      : "neutrality: net force must vanish",
+                              worst);
+                throw ConfigError(msg);
+            }
+        }
+        cudaStream_t st = ctx->stream;
+        double *s = ctx->ws.get<double>("os_s", 3 * ns + 1), *q = ctx->ws.get<double>("os_q", k * ns + 1);
+        PK_CUDA(cudaMemcpyAsync(s, sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaMemcpyAsync(q, strengths, k * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        // targets in chunks: K^P block (chunk x ns) then a gemv
+        const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)(1 << 27) / (k * k * ns + 1)));
+        double *t = ctx->ws.get<double>("os_t", 3 * chunk + 1), *B = ctx->ws.get<double>("os_B", k * chunk * k * ns + 1);
+        double *y = ctx->ws.get<double>("os_y", k * chunk + 1);
+        for (int64_t t0 = 0; t0 < nt; t0 += chunk) {
+            const int64_t m = std::min(chunk, nt - t0);
+            PK_CUDA(cudaMemcpyAsync(t, targets + 3 * t0, 3 * m * sizeof(double), cudaMemcpyHostToDevice, st));
+            periodic_block_device(kernel, *setup, e, false, t, (int)m, s, (int)ns, B, k * ns, st);
+            gemv(B, (int)(k * m), (int)(k * ns), (int)(k * ns), q, y, 1.0, 0.0, nullptr, 0.0, st);
+            PK_CUDA(cudaMemcpyAsync(out + k * t0, y, k * m * sizeof(double), cudaMemcpyDeviceToHost, st));
+            ctx->launches += 2;
+        }
+        PK_CUDA(cudaStreamSynchronize(st));
+    });
+}
 
 pkgpu_status pkgpu_set_kifmm_factors(pkgpu_context *ctx, int kernel, int p, const double *u_up, const double *s_up,
                                      const double *vt_up, const double *u_dn, const double *s_dn,

@@ -19,6 +19,10 @@ struct pkgpu_operator {
     int method = 0;
     double residual_max = 0.0;
     uint64_t crc = 0;
+    double xi = 8.0;             // EwaldParams of the provenance (save_operator header)
+    int real_shells = 2, wave_cutoff = 64;
+    long long n_images = 1000000;
+    std::string created;
     // device copy, uploaded lazily per device
     mutable std::mutex mtx;
     mutable double *d_matrix = nullptr;
