@@ -57,7 +57,8 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed region: NVML
+    every ~5 ms, or nvidia-smi every ~0.2 s where NVML is unavailable."""
 
     def __init__(self, index):
         self.index = index
@@ -66,6 +67,29 @@ class ClockSampler:
         self._t = None
 
     def start(self):
+        try:  # NVML: a sample every ~5 ms, so short timed regions still get many
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+            def run_nvml():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        reasons = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(sm), float(smax), int(reasons)))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.005)
+
+            self._t = threading.Thread(target=run_nvml, daemon=True)
+            self._t.start()
+            return
+        except Exception:
+            pass
+
         def run():
             while not self._stop.is_set():
                 try:

@@ -789,13 +789,18 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
                     tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
                     unsigned char *as = smem + st * DUAL_STAGE;
                     if (tid == 0) {
-                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot, &full[st]);
+                        if (p.debug & 2) { // timing experiment: no operator loads (results invalid)
+                            tma::mbar_arrive(&full[st]);
+                        } else {
+                            tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                            tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot,
+                                             &full[st]);
+                        }
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
-                        if ((hm >> (i >> 3)) & 1)
+                        if (((hm >> (i >> 3)) & 1) && !(p.debug & 1))
                             tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                     }
                     tma::cp_async_mbar_arrive(&full[st]);
@@ -890,24 +895,211 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Dual tile + operator multicast (cluster of 2): each CTA runs the dual-tile pipeline on its
+// own 256-column pair tile; the two pair tiles of a 512-column quad share one offset list,
+// and each CTA TMA-loads HALF of the operator tile with .multicast::cluster into both CTAs'
+// shared memory -- half the operator bytes per CTA from L2 (the dual kernel's dominant load,
+// profiles/r01_i8_pipe_probe.md). A stage is refilled only when both CTAs' MMAs are done with
+// it (each MMA commit is multicast to both "empty" barriers).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
+    m2l_i8_dualmc_kernel(const __grid_constant__ Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int *s_epi = reinterpret_cast<int *>(smem + DUAL_NST * DUAL_STAGE); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t full[DUAL_NST], empty[DUAL_NST], tfull, tempty;
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
+    constexpr int NPT = DUAL_NPROD * 32;
+    if (tid == 0) {
+        for (int s = 0; s < DUAL_NST; s++) {
+            tma::mbar_init(&full[s], NPT + 1); // local cp.async + local expect_tx (both B halves' bytes)
+            tma::mbar_init(&empty[s], 2);      // both CTAs' MMA commits (the peer writes our B half)
+        }
+        tma::mbar_init(&tfull, 1);
+        tma::mbar_init(&tempty, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == DUAL_MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    const uint32_t rank = cluster_rank();
+    const int half = p.Nt / 2;
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    const int nquads = p.coltiles / 4;
+    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
+        int v = u;
+        const int rt = v % p.rowtiles;
+        v /= p.rowtiles;
+        const int qd = v % nquads; // 512-column quad: this CTA owns pair tile 2 qd + rank
+        v /= nquads;
+        const int chunk = v % p.nchunk;
+        const int t = v / p.nchunk;
+        int s0, s1;
+        chunk_range(p, qd, chunk, s0, s1);
+        const int n = (s1 - s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + qd * MAX_SLOTS;
+        const int colp = (2 * qd + (int)rank) * 2 * TBM; // first of this CTA's 256 columns
+        const int hsh = 2 * (int)rank;                      // this CTA's bits of the quad's quarter masks
+        if (warp < DUAL_NPROD) {
+            // ---------------- producers: 256 rows, 16 cp.async of 16 B per thread ----------------
+            const int c = lane & 7, j0 = tid >> 3; // rows j0 + 16 i, i < 16
+            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
+            for (int si = s0; si < s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + colp;
+                // halves without a source for this slot are neither gathered nor multiplied
+                const int hm = p.half_mask[qd * MAX_SLOTS + slot] >> hsh; // loaded alongside the rows
+                int bx[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) bx[i] = srow[j0 + 16 * i];
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    off[i] = (int64_t)(bx[i] >= 0 ? (int)(bx[i] - p.box0) : p.zero_row) * p.Ki;
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int gi = g + (si - s0) * p.KC + kc, st = gi % DUAL_NST;
+                    tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
+                    unsigned char *as = smem + st * DUAL_STAGE;
+                    if (tid == 0) {
+                        // this CTA's half of the operator tile, multicast into both CTAs; the
+                        // local barrier expects both halves
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+                            "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
+                                tma::smem_u32(as + DUAL_A_BYTES + (int)rank * half * BKI)),
+                            "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI), "r"(rt * p.Nt + (int)rank * half),
+                            "r"(t * p.nmat + slot), "r"(tma::smem_u32(&full[st])), "h"((uint16_t)3)
+                            : "memory");
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
+                        if (((hm >> (i >> 3)) & 1) && !(p.debug & 1))
+                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    tma::cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        } else if (warp == DUAL_MMA_WARP) {
+            // ---------------- MMA issuer: two M128 x Nt MMAs per k-step (whole warp,
+            // elected lane issues) ----------------
+            tma::mbar_wait(&tempty, (jb & 1) ^ 1);
+            tc_fence_after();
+            int st = g % DUAL_NST;
+            uint32_t ph = (g / DUAL_NST) & 1;
+            const uint32_t sbase = tma::smem_u32(smem);
+            bool started0 = false, started1 = false; // first MMA of a half overwrites its accumulator
+            const uint8_t *hmt = p.half_mask + qd * MAX_SLOTS;
+            int hm = hmt[slots[s0]] >> hsh;
+            int hm_next = s0 + 1 < s1 ? hmt[slots[s0 + 1]] >> hsh : 0;
+            for (int i = 0, kc = 0, si = s0; i < n; i++) {
+                tma::mbar_wait(&full[st], ph);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                tc_fence_after();
+                const uint32_t a0 = sbase + st * DUAL_STAGE;
+                const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES), bd = sw128_desc(a0 + DUAL_A_BYTES);
+                // REDUX writes a uniform register: the conditional MMAs stay on the uniform datapath
+                // (a branch on a loaded value would bring back the per-MMA R2UR waterfall)
+                const unsigned hu = __reduce_or_sync(0xffffffffu, (unsigned)hm);
+                const bool on0 = (hu & 1u) != 0, on1 = (hu & 2u) != 0;
+#pragma unroll
+                for (int kk = 0; kk < BKI / 32; kk++) {
+                    if (on0) mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, (started0 || kk > 0) ? 1u : 0u);
+                    if (on1) mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, (started1 || kk > 0) ? 1u : 0u);
+                }
+                started0 |= on0;
+                started1 |= on1;
+                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
+                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
+                             "h"((uint16_t)3)
+                             : "memory");
+                if (++st == DUAL_NST) st = 0, ph ^= 1;
+                if (++kc == p.KC) { // next slot: its mask was loaded a slot ahead
+                    kc = 0;
+                    si++;
+                    hm = hm_next;
+                    hm_next = si + 1 < s1 ? hmt[slots[si + 1]] >> hsh : 0;
+                }
+            }
+            commit_elect(&tfull);
+            __syncwarp();
+        } else {
+            // ---------------- epilogue: both accumulators ----------------
+            const int q = warp & 3;
+            int *tile = s_epi + (warp - DUAL_MMA_WARP - 1) * 32 * EPI_PITCH;
+            tma::mbar_wait(&tfull, jb & 1);
+            tc_fence_after();
+            const int m = c_mod[t];
+            const float inv = 1.0f / (float)m;
+            const int r0 = rt * p.Nt;
+            const int nr = min(p.Nt, p.Ki - r0);
+            int used = 0; // halves that received an MMA in this unit (others hold stale TMEM)
+            for (int si = s0 + lane; si < s1; si += 32) used |= p.half_mask[qd * MAX_SLOTS + slots[si]] >> hsh;
+            for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+            for (int h = 0; h < 2; h++) {
+                if (!((used >> h) & 1)) continue;
+                int *Rt = p.R + ((int64_t)t * p.ncols + colp + h * TBM + q * 32) * p.Ki + r0;
+                for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                    uint32_t vv[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + j0, vv);
+#pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        const int a = (int)vv[j];
+                        tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
+                    }
+                    __syncwarp();
+                    const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                    for (int b = 0; b < 32; b++) {
+                        const int r = tile[b * EPI_PITCH + lane];
+                        if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    }
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tma::mbar_arrive(&tempty);
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    cluster_sync(); // no CTA leaves while the peer may still multicast into it
+    if (warp == DUAL_MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+
 // active slots per column tile of `bn` columns, in slot order
-// half_mask (bn = 256, pair tiles): bit h set when the 128-column half h has a source
+// half_mask (bn = 256 / 512): bit q set when the 128-column quarter q has a source
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
                                  int *tile_nact, int *tile_below, uint8_t *half_mask) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
-        bool h0 = false, h1 = false;
-        for (int j = lane; j < bn; j += 32) {
-            const bool a = src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0;
-            if (j < TBM) h0 |= a;
-            else h1 |= a;
-        }
-        h0 = __any_sync(0xffffffffu, h0);
-        h1 = __any_sync(0xffffffffu, h1);
+        unsigned m = 0; // bit q: the 128-column quarter q of the tile has a source
+        for (int j = lane; j < bn; j += 32)
+            if (src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0) m |= 1u << (j / TBM);
+        m = __reduce_or_sync(0xffffffffu, m);
         if (lane == 0) {
-            flag[s] = (h0 || h1) ? 1 : 0;
-            if (half_mask) half_mask[ct * MAX_SLOTS + s] = (uint8_t)((h0 ? 1 : 0) | (h1 ? 2 : 0));
+            flag[s] = m ? 1 : 0;
+            if (half_mask) half_mask[ct * MAX_SLOTS + s] = (uint8_t)m;
         }
     }
     __syncthreads();
@@ -1258,19 +1450,20 @@ namespace {
 
 // kernel variant per launch: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
 // (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
-// (m2l_i8_dual_kernel). Default: dual everywhere (8 MMAs per pipeline stage, half the
+// (m2l_i8_dual_kernel), 4 dual tile + operator multicast across a CTA pair (m2l_i8_dualmc_kernel,
+// 2% faster at cfg2 level 4, slower on the small-level run). Default: dual everywhere (8 MMAs per pipeline stage, half the
 // operator bytes per MAC; a pair tile's halves with no source for a slot skip its gather
 // and MMA). i8_gather_gemm (tests) keeps the single kernel below 2048 columns so both stay
 // covered. PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
 int select_mode(bool big) {
     static const int forced = [] {
         const char *e = std::getenv("PKGPU_I8_PAIR");
-        return e ? std::max(0, std::min(3, std::atoi(e))) : -1;
+        return e ? std::max(0, std::min(4, std::atoi(e))) : -1;
     }();
     (void)big; // measured: with per-half slot masks the dual kernel also wins on the small-level run
     return forced >= 0 ? forced : 3;
 }
-int column_tile(int mode) { return mode != 0 ? 2 * TBM : TBM; }
+int column_tile(int mode) { return mode == 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
 
 // active-slot lists per column tile (ncols / column_tile(mode) tiles)
 void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode, Workspace &ws, cudaStream_t st,
@@ -1279,7 +1472,7 @@ void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode,
     *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
     *tnact = ws.get<int>("i8_tile_nact", tiles);
     *tbelow = ws.get<int>("i8_tile_below", (size_t)tiles * (MAX_SLOTS + 1));
-    uint8_t *hmask = mode == 3 ? ws.get<uint8_t>("i8_tile_hmask", (size_t)tiles * MAX_SLOTS) : nullptr;
+    uint8_t *hmask = mode >= 3 ? ws.get<uint8_t>("i8_tile_hmask", (size_t)tiles * MAX_SLOTS) : nullptr;
     slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask);
     if (thmask) *thmask = hmask;
     PK_CUDA(cudaGetLastError());
@@ -1289,7 +1482,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
                  const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false,
                  const uint8_t *thmask = nullptr) {
-    if (mode == 3 && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernel needs the half masks");
+    if (mode >= 3 && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernel needs the half masks");
     const int num_sms = sm_count();
     const bool pair = mode != 0;
     Params p;
@@ -1320,8 +1513,8 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     int nchunk = (int)((nslots + cmax - 1) / cmax);
     static const int min_chunks = std::getenv("PKGPU_I8_CHUNKS") ? std::atoi(std::getenv("PKGPU_I8_CHUNKS")) : 0;
     nchunk = std::max(nchunk, min_chunks);
-    const int64_t base = (int64_t)nmod * p.rowtiles * (pair ? p.coltiles / 2 : p.coltiles);
-    const int64_t resident = (mode == 1 || mode == 2) ? num_sms / 2 : num_sms;
+    const int64_t base = (int64_t)nmod * p.rowtiles * (mode == 4 ? p.coltiles / 4 : pair ? p.coltiles / 2 : p.coltiles);
+    const int64_t resident = (mode == 1 || mode == 2 || mode == 4) ? num_sms / 2 : num_sms;
     while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
@@ -1335,11 +1528,11 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     // slot-index windows for the small-level run (operator reuse through L2 across its
     // tiles); equal list shares for the dual-tile big levels (balanced static schedule)
     static const int by_index_env = std::getenv("PKGPU_I8_BYINDEX") ? std::atoi(std::getenv("PKGPU_I8_BYINDEX")) : -1;
-    p.by_index = by_index_env >= 0 ? by_index_env : (mode == 3 ? 0 : 1);
+    p.by_index = by_index_env >= 0 ? by_index_env : (mode >= 3 ? 0 : 1);
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
     // the CTA-pair variants stage half of the operator tile per CTA
-    const bool half_tile = mode == 1 || mode == 2;
+    const bool half_tile = mode == 1 || mode == 2 || mode == 4;
     const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
@@ -1359,7 +1552,17 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
             throw CudaError("cuTensorMapEncodeTiled (int8 gather) failed (" + std::to_string((int)rx) + ")");
     }
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    if (mode == 3) {
+    if (mode == 4) {
+        if (ncols % (4 * TBM) != 0) throw RuntimeError("i8 gemm: the multicast dual kernel needs 512-column multiples");
+        const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_dualmc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
+        m2l_i8_dualmc_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
+    } else if (mode == 3) {
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
         static bool cfg = false;
         if (!cfg) {
@@ -1424,7 +1627,8 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
         throw RuntimeError("i8_gather_gemm: bad shape");
     upload_tables();
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
-    const int mode = ncols >= 2048 ? select_mode(true) : 0;
+    int mode = ncols >= 2048 ? select_mode(true) : 0;
+    if (mode == 4 && ncols % (4 * TBM) != 0) mode = 3;
     uint8_t *thmask = nullptr;
     scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
@@ -1476,8 +1680,10 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     // residue sums of this column window only (the window bounds R: 4 nmod Ki bytes per column)
     w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
-    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.mode, ws, st, &w.tile_slots, &w.tile_nact, &w.tile_below,
-               &w.tile_hmask);
+    // the multicast variant needs whole 512-column quads; other windows use the dual kernel
+    w.win_mode = (w.mode == 4 && ncols % (4 * TBM) != 0) ? 3 : w.mode;
+    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.win_mode, ws, st, &w.tile_slots, &w.tile_nact,
+               &w.tile_below, &w.tile_hmask);
     if (a.mma_rows && w.tile_hmask) {
         mma_rows_kernel<<<ncols / (2 * TBM), 32, 0, st>>>(w.tile_hmask, a.nslots, a.mma_rows);
         PK_CUDA(cudaGetLastError());
@@ -1492,7 +1698,7 @@ int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int6
     const int ncols = (int)(c1 - c0);
     if (ncols <= 0) return 0;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
-                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.mode, st, false,
+                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.win_mode, st, false,
                 w.tile_hmask);
     return 1;
 }

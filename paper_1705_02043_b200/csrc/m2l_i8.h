@@ -103,6 +103,7 @@ struct I8LevelWork {
     int *tile_below = nullptr;                       // per tile: active slots below each slot index
     uint8_t *tile_hmask = nullptr;                   // dual kernel: per (pair tile, slot) active halves
     int mode = 0;                                    // kernel variant (select_mode)
+    int win_mode = 0;                                // variant of the current column window
 };
 // The three steps of one level (separately timed by the stage profiler):
 //   prepare: level max, density residues

@@ -29,7 +29,7 @@ def host_residue_gemm(A, B, src, box0, zero_row):
 
 # ncols >= 2048 runs the dual-tile kernel (two 128-box accumulators per operator tile)
 @pytest.mark.parametrize("Ki,nslots,ncols,nmod", [(128, 3, 256, 2), (384, 7, 512, 3), (896, 12, 256, 2),
-                                                  (1536, 5, 512, 1), (896, 9, 2048, 1), (384, 4, 2304, 2)])
+                                                  (1536, 5, 512, 1), (896, 9, 2048, 1), (384, 4, 2560, 2)])
 def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
     rng = np.random.default_rng(Ki * 31 + nslots)
     mods = pk.i8_moduli()[:nmod]
