@@ -57,30 +57,45 @@ __device__ __forceinline__ int lower_digit(const unsigned long long *__restrict_
     return lo;
 }
 
-// per box of level l: split decision and child ranges
+// per box of level l: split decision and child ranges. 16 lanes per box: lane g searches
+// one child boundary (g < 8: sources, digit g; g >= 8: targets, digit g - 8) over the whole
+// box range, so the boundaries come from independent binary searches (one dependent chain
+// of ~log2(n) loads) instead of 14 chained ones -- the top levels, where one box spans all
+// points, were latency-bound
 __global__ void split_kernel(int n, int level, int cap, const int2 *__restrict__ srng, const int2 *__restrict__ trng,
                              const unsigned long long *__restrict__ skeys, const unsigned long long *__restrict__ tkeys,
                              int *__restrict__ childcnt, int4 *__restrict__ crange, int *__restrict__ err) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int2 s = srng[i], t = trng[i];
-    const bool split = (s.y - s.x) > cap || (t.y - t.x) > cap;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = gt >> 4, g = gt & 15;
+    const bool live = i < n;
+    const int2 s = live ? srng[i] : make_int2(0, 0), t = live ? trng[i] : make_int2(0, 0);
+    const bool split = live && ((s.y - s.x) > cap || (t.y - t.x) > cap);
+    const bool deep = level >= kMaxDepth;
+    int b = 0;
+    if (split && !deep) {
+        const int shift = 3 * (kMaxDepth - 1 - level);
+        const unsigned o = g & 7;
+        b = g < 8 ? (o == 0 ? s.x : lower_digit(skeys, s.x, s.y, shift, o))
+                  : (o == 0 ? t.x : lower_digit(tkeys, t.x, t.y, shift, o));
+    }
+    // gather the 16 boundaries of the box into its first lane
+    int sb[9], tb[9];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        sb[k] = __shfl_sync(0xffffffffu, b, (threadIdx.x & 16) + k);
+        tb[k] = __shfl_sync(0xffffffffu, b, (threadIdx.x & 16) + 8 + k);
+    }
+    if (!live || g != 0) return;
     if (!split) {
         childcnt[i] = 0;
         return;
     }
-    if (level >= kMaxDepth) {
+    if (deep) {
         atomicExch(err, 1);
         childcnt[i] = 0;
         return;
     }
-    const int shift = 3 * (kMaxDepth - 1 - level);
-    int sb[9], tb[9];
-    sb[0] = s.x, sb[8] = s.y, tb[0] = t.x, tb[8] = t.y;
-    for (unsigned o = 1; o < 8; o++) {
-        sb[o] = lower_digit(skeys, sb[o - 1], s.y, shift, o);
-        tb[o] = lower_digit(tkeys, tb[o - 1], t.y, shift, o);
-    }
+    sb[8] = s.y, tb[8] = t.y;
     int cnt = 0;
     for (int o = 0; o < 8; o++) {
         crange[8 * (int64_t)i + o] = make_int4(sb[o], sb[o + 1], tb[o], tb[o + 1]);
@@ -275,7 +290,7 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         int *childcnt = ws.get<int>("childcnt", nl + 1);
         int *childoff = ws.get<int>("childoff", nl + 1);
         int4 *crange = ws.get<int4>("crange", 8 * nl);
-        split_kernel<<<blocks_for(nl, 128), 128, 0, st>>>((int)nl, level, leaf_capacity, T.srng + base,
+        split_kernel<<<blocks_for(16 * nl, 128), 128, 0, st>>>((int)nl, level, leaf_capacity, T.srng + base,
                                                           T.trng + base, skeys, tkeys, childcnt, crange, flags + 1);
         size_t sb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, sb, childcnt, childoff, (int)nl + 1, st);
