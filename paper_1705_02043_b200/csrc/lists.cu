@@ -194,6 +194,195 @@ template <class Sink> __device__ void enumerate_box(const TreeView &T, const Par
             }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-box enumeration (evaluate path): lane d < 27 handles neighbour direction d of the
+// serial enumerate_box, so the ~27 dependent deepest_box searches run concurrently instead
+// of one after another. Entries keep the serial order (direction-major, the descent order
+// within a direction): each lane counts its entries, an exclusive warp scan gives its
+// offset, and the lane emits again at that offset. Coarse-leaf deduplication compares
+// against the lower directions through shuffles.
+struct LaneCount {
+    int nu = 0, nv = 0, nw = 0, nx = 0;
+    __device__ void u(int, int) { nu++; }
+    __device__ void v(int, int) { nv++; }
+    __device__ void w(int, int) { nw++; }
+    __device__ void x(int, int) { nx++; }
+};
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane) {
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x - v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// direction d's U/W entries of leaf b (lanes >= 27 or invalid directions emit nothing)
+template <class Sink>
+__device__ void lane_uw(const TreeView &T, const Params &P, int b, int4 bc, int d, bool dup, int k, int scode,
+                        bool valid, Sink &sink) {
+    if (!valid) return;
+    const bool eval = P.eval_mode != 0;
+    const int l = bc.w;
+    const int4 kc = T.cell[k];
+    if (kc.w < l) {
+        if (!T.isleaf[k] || dup) return;
+        if (!eval || has_src(T, k)) sink.u(k, scode);
+        return;
+    }
+    if (T.isleaf[k]) {
+        if (!eval || has_src(T, k)) sink.u(k, scode);
+        return;
+    }
+    int sx, sy, sz;
+    shift_decode(scode, sx, sy, sz);
+    int stack[12 * 8 + 8];
+    int top = 0;
+    stack[top++] = k;
+    while (top > 0) {
+        const int x = stack[--top];
+        for (int o = 0; o < 8; o++) {
+            const int cc = T.child[8 * x + o];
+            if (cc < 0) continue;
+            const int4 ccell = T.cell[cc];
+            if (adjacent(bc, ccell, sx, sy, sz)) {
+                if (T.isleaf[cc]) {
+                    if (!eval || has_src(T, cc)) sink.u(cc, scode);
+                } else {
+                    stack[top++] = cc;
+                }
+            } else {
+                if (!eval || has_src(T, cc)) sink.w(cc, scode);
+            }
+        }
+    }
+    (void)b;
+    (void)d;
+}
+
+// direction d's V/X entries of box b
+template <class Sink>
+__device__ void lane_vx(const TreeView &T, const Params &P, int4 bc, bool dup, int k, int scode, bool valid,
+                        Sink &sink) {
+    if (!valid) return;
+    const bool eval = P.eval_mode != 0;
+    const int l = bc.w;
+    const int4 kc = T.cell[k];
+    int sx, sy, sz;
+    shift_decode(scode, sx, sy, sz);
+    if (!T.isleaf[k]) {
+        if (kc.w != l - 1) return;
+        for (int o = 0; o < 8; o++) {
+            const int cc = T.child[8 * k + o];
+            if (cc < 0) continue;
+            const int4 ccell = T.cell[cc];
+            if (adjacent(bc, ccell, sx, sy, sz)) continue;
+            if (eval && !has_src(T, cc)) continue;
+            sink.v(cc, offset_code(ccell.x + (sx << l) - bc.x, ccell.y + (sy << l) - bc.y, ccell.z + (sz << l) - bc.z));
+        }
+    } else {
+        if (dup || adjacent(bc, kc, sx, sy, sz)) return;
+        if (eval && !has_src(T, k)) return;
+        sink.x(k, scode);
+    }
+}
+
+// neighbour cell of direction d (27 directions, dz-major as the serial loop) around cell c
+// of level lev: wrapped cell, its shift code and the deepest box holding it
+__device__ __forceinline__ bool lane_neighbour(const TreeView &T, const Params &P, int4 c, int lev, int d, int &k,
+                                               int &scode) {
+    if (d >= 27) return false;
+    const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+    const int size = 1 << lev;
+    int wx, wy, wz, sx, sy, sz;
+    if (!wrap1(c.x + dx, size, P.per[0], wx, sx) || !wrap1(c.y + dy, size, P.per[1], wy, sy) ||
+        !wrap1(c.z + dz, size, P.per[2], wz, sz))
+        return false;
+    scode = shift_code(sx, sy, sz);
+    k = deepest_box(T, lev, wx, wy, wz);
+    return true;
+}
+
+// duplicate coarse candidate: a lower direction already produced the same (box, shift)
+__device__ __forceinline__ bool lane_dup(bool coarse, int k, int scode, int lane) {
+    bool dup = false;
+    for (int q = 0; q < 27; q++) {
+        const int qk = __shfl_sync(0xffffffffu, k, q), qs = __shfl_sync(0xffffffffu, scode, q);
+        const int qc = __shfl_sync(0xffffffffu, coarse ? 1 : 0, q);
+        dup |= q < lane && qc && qk == k && qs == scode;
+    }
+    return coarse && dup;
+}
+
+struct LaneFill {
+    int2 *eu, *ew, *ex;
+    int *table;
+    int64_t ld;
+    int col;
+    const int *slot_of_code;
+    __device__ void u(int c, int code) { *eu++ = make_int2(c, code); }
+    __device__ void v(int c, int code) { table[(int64_t)slot_of_code[code] * ld + col] = c; }
+    __device__ void w(int c, int code) { *ew++ = make_int2(c, code); }
+    __device__ void x(int c, int code) { *ex++ = make_int2(c, code); }
+};
+
+// fill == false: per-box counts; true: entries at the box's offsets (M2L table for V)
+template <bool FILL>
+__global__ void eval_warp_kernel(TreeView T, Params P, int64_t *cu, int64_t *cv, int64_t *cw, int64_t *cx,
+                                 const int64_t *ou, const int64_t *ow, const int64_t *ox, int2 *eu, int2 *ew, int2 *ex,
+                                 int *table, int64_t ld, const int *col_of_box, const int *slot_of_code) {
+    const int b = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (b >= T.nboxes) return; // whole warps exit together
+    const int4 bc = T.cell[b];
+    const int l = bc.w;
+    bool skip = P.eval_mode != 0 && T.trng[b].y == T.trng[b].x;
+    if (P.mask && !P.mask[b]) skip = true;
+    LaneCount c;
+    int2 *pu = nullptr, *pw = nullptr, *px = nullptr;
+    if (FILL && !skip) pu = eu + ou[b], pw = ew + ow[b], px = ex + ox[b];
+    // ---- U / W ----
+    if (!skip && T.isleaf[b]) {
+        int k = 0, scode = 0;
+        const bool valid = lane_neighbour(T, P, bc, l, lane, k, scode);
+        const bool coarse = valid && T.cell[k].w < l;
+        const bool dup = lane_dup(coarse, k, scode, lane);
+        LaneCount n;
+        lane_uw(T, P, b, bc, lane, dup, k, scode, valid, n);
+        if (FILL) {
+            const int offu = warp_excl_scan(n.nu, lane), offw = warp_excl_scan(n.nw, lane);
+            LaneFill f{pu + offu, pw + offw, nullptr, nullptr, 0, 0, nullptr};
+            lane_uw(T, P, b, bc, lane, dup, k, scode, valid, f);
+        }
+        c.nu = n.nu, c.nw = n.nw;
+    }
+    // ---- V / X ----
+    if (!skip && l > 0) {
+        const int pb = T.parent[b];
+        const int4 pc = T.cell[pb];
+        int k = 0, scode = 0;
+        const bool valid = lane_neighbour(T, P, pc, l - 1, lane, k, scode);
+        const bool leafk = valid && T.isleaf[k];
+        const bool dup = lane_dup(leafk, k, scode, lane);
+        LaneCount n;
+        lane_vx(T, P, bc, dup, k, scode, valid, n);
+        if (FILL) {
+            const int offx = warp_excl_scan(n.nx, lane);
+            LaneFill f{nullptr, nullptr, px + offx, table, ld, col_of_box[b], slot_of_code};
+            lane_vx(T, P, bc, dup, k, scode, valid, f);
+        }
+        c.nv = n.nv, c.nx = n.nx;
+    }
+    if (!FILL) {
+        const int nu = warp_sum(c.nu), nv = warp_sum(c.nv), nw = warp_sum(c.nw), nx = warp_sum(c.nx);
+        if (lane == 0) cu[b] = nu, cv[b] = nv, cw[b] = nw, cx[b] = nx;
+    }
+}
+
 struct CountSink {
     int nu = 0, nv = 0, nw = 0, nx = 0;
     __device__ void u(int, int) { nu++; }
@@ -313,7 +502,9 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
         off[i] = ws.get<int64_t>(std::string("off_") + names[i], nb + 1);
         PK_CUDA(cudaMemsetAsync(cnt[i] + nb, 0, sizeof(int64_t), st));
     }
-    count_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(tv, P, cnt[0], cnt[1], cnt[2], cnt[3]);
+    eval_warp_kernel<false><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
+        tv, P, cnt[0], cnt[1], cnt[2], cnt[3], nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+        nullptr, nullptr);
     int64_t tot[4];
     for (int i = 0; i < 4; i++) scan_counts(ws, cnt[i], off[i], nb, st, tot[i]);
     PK_CUDA(cudaStreamSynchronize(st));
@@ -327,8 +518,9 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
         lists[i]->count = tot[i];
         lists[i]->ent = ws.get<int2>(std::string("ent_") + names[i], tot[i] + 1);
     }
-    eval_fill_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(tv, P, off[0], off[2], off[3], L.u.ent, L.w.ent, L.x.ent,
-                                                        m2l_table, ld, col_of_box, slot_of_code);
+    eval_warp_kernel<true><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
+        tv, P, nullptr, nullptr, nullptr, nullptr, off[0], off[2], off[3], L.u.ent, L.w.ent, L.x.ent, m2l_table, ld,
+        col_of_box, slot_of_code);
     *launches += 5;
 }
 
