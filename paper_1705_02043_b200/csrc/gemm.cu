@@ -456,7 +456,8 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     const int64_t base = (int64_t)rowtiles * coltiles;
     const int resident = num_sms * (bnt == 128 ? 1 : 2);
     // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
-    // still at least 16 iterations long
+    // still at least PKGPU_GEMM_MINIT (default 16) iterations long (shorter units measured
+    // slower at cfg2: more partials to reduce, no gain on the small levels)
     const int64_t iters = (int64_t)a.nslots * (a.Kp / BK);
     static const int64_t units_per_cta = [] {
         const char *e = std::getenv("PKGPU_GEMM_UNITS"); // tuning knob: work units per resident CTA
@@ -464,7 +465,12 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     }();
     const int64_t want = tma_path ? units_per_cta * resident : 4 * (int64_t)resident;
     int nsplit = 1;
-    if (base < want) nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / 16), 64});
+    static const int64_t min_iters = [] {
+        const char *e = std::getenv("PKGPU_GEMM_MINIT");
+        return (int64_t)(e ? std::max(1, std::atoi(e)) : 16);
+    }();
+    if (base < want)
+        nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / min_iters), 64});
     nsplit = std::max(nsplit, 1);
     KParams kp{};
     kp.a = a;
