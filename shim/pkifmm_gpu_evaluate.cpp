@@ -1,5 +1,6 @@
 // Drop-in replacement for pkifmm::evaluate (include/pkifmm/fmm.hpp:141,
-// src/fmm.cpp:690-742) that runs on the B200 through the C ABI in include/pkgpu.h.
+// src/fmm.cpp:690-742) and pkifmm::solve_m2l (include/pkifmm/periodize.hpp:42-46,
+// src/periodize.cpp:113-158) that run on the B200 through the C ABI in include/pkgpu.h.
 //
 // Compiled against the reference's own headers; linking this object ahead of the
 // reference's fmm.o (whose evaluate symbol is weakened) makes every existing caller —
@@ -12,6 +13,7 @@
 
 #include "pkgpu.h"
 #include "pkifmm/fmm.hpp"
+#include "pkifmm/periodize.hpp"
 
 namespace {
 
@@ -97,5 +99,41 @@ EvalResult evaluate(const EvalRequest &request) {
     result.compat.violated = cp.violated;
     return result;
 }
+
+// solve_m2l on the GPU (pkgpu_operator_solve): K^{P,F} by per-pair Ewald / image sums,
+// T = pinv(a_dn) K^{P,F} with the device's own downward factors (cuSOLVER; equivalent to
+// the caller's up to rounding), the same 1e-11 residual gate and messages.
+namespace {
+PeriodizingOperator solve_on_gpu(const PeriodicKernelSpec &spec, int p) {
+    validate_method(spec);
+    const pkgpu_setup s = to_setup(spec.setup);
+    const pkgpu_ewald e{spec.params.xi, spec.params.real_shells, spec.params.wave_cutoff, spec.params.n_images};
+    pkgpu_operator *op = nullptr;
+    char err[2048] = {0};
+    const pkgpu_status st =
+        pkgpu_operator_solve(context(), static_cast<int>(spec.kernel.type), &s, p, &e, 1, &op, err, sizeof err);
+    if (st != PKGPU_OK) rethrow(st, err);
+    int64_t dim = 0;
+    double residual = 0.0;
+    pkgpu_operator_info(op, nullptr, nullptr, nullptr, &dim, &residual);
+    PeriodizingOperator out;
+    out.matrix = DenseMatrix(static_cast<int>(dim), static_cast<int>(dim));
+    pkgpu_operator_matrix(op, out.matrix.data.data());
+    pkgpu_operator_free(op);
+    out.kernel = spec.kernel;
+    out.setup = spec.setup;
+    out.p = p;
+    out.method = spec.method;
+    out.params = spec.params;
+    out.residual_max = residual;
+    return out;
+}
+} // namespace
+
+PeriodizingOperator solve_m2l(const PeriodicKernelSpec &spec, int p, const SvdFactors &) {
+    return solve_on_gpu(spec, p);
+}
+
+PeriodizingOperator solve_m2l(const PeriodicKernelSpec &spec, int p) { return solve_on_gpu(spec, p); }
 
 } // namespace pkifmm
