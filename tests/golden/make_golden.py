@@ -160,6 +160,16 @@ EVAL_CASES = [
 ]
 
 
+# adaptive evaluate cases: clustered sources (deep, graded octrees with W and X lists),
+# (name, kernel, per, axes, ell, p, leaf, n, op-spec, nclusters, sigma)
+EVAL_ADAPTIVE = [
+    ("lap_none_p6_clu", "laplace", "none", "", 2, 6, 30, 4000, None, 4, 0.02),
+    ("lap_sp_p8_clu", "laplace", "sp", "", 2, 8, 30, 4000, "gated", 4, 0.02),
+    ("lap_dp_p6_clu", "laplace", "dp", "", 2, 6, 30, 4000, "gated", 3, 0.03),
+    ("sto_tp_p6_clu", "stokeslet", "tp", "", 2, 6, 30, 4000, "gated", 4, 0.02),
+]
+
+
 def op_path(kernel, per, axes, ell, p, kind):
     tag = f"{kernel}_{per}{axes}_ell{ell}_p{p}_{kind}.pkm2l"
     return os.path.join(OPS, tag)
@@ -182,11 +192,16 @@ def make_op(kernel, per, axes, ell, p, kind):
     return path
 
 
-def golden_eval(tmp):
-    for (name, kernel, per, axes, ell, p, leaf, n, opk) in EVAL_CASES:
+def golden_eval(tmp, cases=None):
+    for case in cases or EVAL_CASES:
+        (name, kernel, per, axes, ell, p, leaf, n, opk), extra = case[:9], case[9:]
         ks = 1 if kernel == "laplace" else 3
         gaxes = {"none": "xyz", "sp": axes or "z", "dp": "xy", "tp": "xyz"}[per]
-        src, rho = gen(tmp, "e", n, kind="uniform", ks=ks, seed=1000 + n + len(name), axes=gaxes)
+        if extra:
+            src, rho = gen(tmp, "e", n, kind="clusters", ks=ks, seed=2000 + n + len(name), axes=gaxes,
+                           nclusters=extra[0], sigma=extra[1])
+        else:
+            src, rho = gen(tmp, "e", n, kind="uniform", ks=ks, seed=1000 + n + len(name), axes=gaxes)
         ps, pr = save_pts(tmp, "es", src), save_pts(tmp, "er", rho)
         args = ["eval", "--kernel", kernel, "--per", per, "--ell", ell, "--p", p, "--leaf", leaf, "--src", ps,
                 "--str", pr, "--out", os.path.join(tmp, "ev")]
@@ -213,6 +228,10 @@ def golden_eval(tmp):
         out["meta"] = np.array(json.dumps(meta))
         np.savez_compressed(os.path.join(HERE, f"eval_{name}.npz"), **out)
         print(name, "spread", spread)
+
+
+def golden_eval_adaptive(tmp):
+    golden_eval(tmp, EVAL_ADAPTIVE)
 
 
 def golden_direct(tmp):
@@ -288,6 +307,7 @@ def main():
         golden_trees(tmp)
         golden_direct(tmp)
         golden_eval(tmp)
+        golden_eval_adaptive(tmp)
 
 
 if __name__ == "__main__":

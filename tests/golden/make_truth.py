@@ -21,11 +21,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REFDUMP = os.path.join(HERE, "..", "..", "oracle", "_ref", "refdump")
 # cases with a periodic truth evaluator: Laplace SP/DP/TP, Stokes TP
 # (Stokes DP has no K^P in the reference, src/refsum.cpp:620-622; cfg1 is SP-x)
-CASES = ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8"]
+CASES = ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8", "lap_sp_p8_clu", "lap_dp_p6_clu",
+         "sto_tp_p6_clu"]
 
 
 def main():
-    for case in CASES:
+    for case in sys.argv[1:] or CASES:
         g = np.load(os.path.join(HERE, f"eval_{case}.npz"))
         meta = json.loads(str(g["meta"]))
         with tempfile.TemporaryDirectory() as tmp:

@@ -152,7 +152,9 @@ def test_tree_errors():
 # evaluate (end to end)
 
 EVAL_ALL = ["lap_none_p6", "lap_sp_p8", "lap_spx_p8", "lap_dp_p6", "lap_tp_p8", "lap_tp_p6_ell1", "sto_none_p6",
-            "sto_tp_p6", "sto_tp_p8", "sto_dp_p6", "cfg1"]
+            "sto_tp_p6", "sto_tp_p8", "sto_dp_p6", "cfg1",
+            # adaptive: clustered sources, depth 6-7 octrees with W and X lists (make_golden.py EVAL_ADAPTIVE)
+            "lap_none_p6_clu", "lap_sp_p8_clu", "lap_dp_p6_clu", "sto_tp_p6_clu"]
 
 
 def golden_request(g):

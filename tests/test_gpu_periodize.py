@@ -99,7 +99,8 @@ def test_evaluate_with_gpu_built_operator(case, opname, solved):
     assert rel <= tol
 
 
-@pytest.mark.parametrize("case", ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8"])
+@pytest.mark.parametrize("case", ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8", "lap_sp_p8_clu",
+                                  "lap_dp_p6_clu", "sto_tp_p6_clu"])
 def test_oracle_system_eval_matches_reference_truth(case):
     g = load(f"eval_{case}.npz")
     t = np.load(os.path.join(GOLDEN, f"truth_{case}.npz"))
