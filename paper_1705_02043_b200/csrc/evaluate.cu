@@ -915,8 +915,9 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             int ps = prof.begin("m2l_prep");
             I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
             prof.end(ps);
-            for (int64_t w0 = 0; w0 < a.ncols; w0 += kI8Window) { // column windows bound the residue sums
-                const int64_t w1 = std::min<int64_t>(a.ncols, w0 + kI8Window);
+            const int64_t win = i8_window(ops.i8.nmod, ops.i8.Ki);
+            for (int64_t w0 = 0; w0 < a.ncols; w0 += win) { // column windows bound the residue sums
+                const int64_t w1 = std::min<int64_t>(a.ncols, w0 + win);
                 ps = prof.begin("m2l_prep");
                 ctx.launches += m2l_i8_window(ops.i8, a, w, w0, w1, ws, st);
                 prof.end(ps);

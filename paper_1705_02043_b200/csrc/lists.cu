@@ -502,9 +502,17 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
         off[i] = ws.get<int64_t>(std::string("off_") + names[i], nb + 1);
         PK_CUDA(cudaMemsetAsync(cnt[i] + nb, 0, sizeof(int64_t), st));
     }
-    eval_warp_kernel<false><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
-        tv, P, cnt[0], cnt[1], cnt[2], cnt[3], nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-        nullptr, nullptr);
+    // warp per box where boxes are few (latency-bound single threads); thread per box on big
+    // trees, which already fill the GPU (PKGPU_LIST_WARP_MAX boxes, default 50k)
+    static const int64_t warp_max =
+        std::getenv("PKGPU_LIST_WARP_MAX") ? std::atoll(std::getenv("PKGPU_LIST_WARP_MAX")) : 50000;
+    const bool warp_lists = nb <= warp_max;
+    if (warp_lists)
+        eval_warp_kernel<false><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
+            tv, P, cnt[0], cnt[1], cnt[2], cnt[3], nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+            nullptr, nullptr);
+    else
+        count_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(tv, P, cnt[0], cnt[1], cnt[2], cnt[3]);
     int64_t tot[4];
     for (int i = 0; i < 4; i++) scan_counts(ws, cnt[i], off[i], nb, st, tot[i]);
     PK_CUDA(cudaStreamSynchronize(st));
@@ -518,9 +526,13 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
         lists[i]->count = tot[i];
         lists[i]->ent = ws.get<int2>(std::string("ent_") + names[i], tot[i] + 1);
     }
-    eval_warp_kernel<true><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
-        tv, P, nullptr, nullptr, nullptr, nullptr, off[0], off[2], off[3], L.u.ent, L.w.ent, L.x.ent, m2l_table, ld,
-        col_of_box, slot_of_code);
+    if (warp_lists)
+        eval_warp_kernel<true><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(
+            tv, P, nullptr, nullptr, nullptr, nullptr, off[0], off[2], off[3], L.u.ent, L.w.ent, L.x.ent, m2l_table,
+            ld, col_of_box, slot_of_code);
+    else
+        eval_fill_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(tv, P, off[0], off[2], off[3], L.u.ent, L.w.ent, L.x.ent,
+                                                            m2l_table, ld, col_of_box, slot_of_code);
     *launches += 5;
 }
 

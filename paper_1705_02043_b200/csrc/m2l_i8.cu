@@ -67,6 +67,7 @@ struct Params {
     int nslots, by_index;
     int direct; // single-kernel epilogue stores the partial residues (one unit per output tile)
     const uint8_t *half_mask; // dual kernel: [pair tile][slot] bit h = half h has a source
+    const int *tile_partial;  // dual kernel: [pair tile] 1 if some active slot misses a half
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
     int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
@@ -816,6 +817,31 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
             const uint32_t sbase = tma::smem_u32(smem);
             bool started0 = false, started1 = false; // first MMA of a half overwrites its accumulator
             const uint8_t *hmt = p.half_mask + pr * MAX_SLOTS;
+            // tiles whose every active slot feeds both halves (uniform levels) take the
+            // unconditional loop; the masked one costs a few percent per stage
+            if (__reduce_or_sync(0xffffffffu, (unsigned)p.tile_partial[pr]) == 0u) {
+                for (int i = 0; i < n; i++) {
+                    tma::mbar_wait(&full[st], ph);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tc_fence_after();
+                    const uint32_t a0 = sbase + st * DUAL_STAGE;
+                    const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES),
+                                   bd = sw128_desc(a0 + DUAL_A_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BKI / 32; kk++) {
+                        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                        mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                        mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                    }
+                    commit_elect(&empty[st]);
+                    if (++st == DUAL_NST) st = 0, ph ^= 1;
+                }
+                commit_elect(&tfull);
+                __syncwarp();
+                g += n;
+                jb++;
+                continue;
+            }
             int hm = hmt[slots[s0]];
             int hm_next = s0 + 1 < s1 ? hmt[slots[s0 + 1]] : 0;
             for (int i = 0, kc = 0, si = s0; i < n; i++) {
@@ -1089,7 +1115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
 // active slots per column tile of `bn` columns, in slot order
 // half_mask (bn = 256 / 512): bit q set when the 128-column quarter q has a source
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
-                                 int *tile_nact, int *tile_below, uint8_t *half_mask) {
+                                 int *tile_nact, int *tile_below, uint8_t *half_mask, int *tile_partial) {
     __shared__ int flag[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
@@ -1104,14 +1130,19 @@ __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, in
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        int n = 0;
+        int n = 0, partial = 0;
         int *below = tile_below + ct * (MAX_SLOTS + 1);
+        const int fullm = (1 << (bn / TBM)) - 1;
         for (int s = 0; s < nslots; s++) {
             below[s] = n;
-            if (flag[s]) tile_slots[ct * MAX_SLOTS + n++] = s;
+            if (flag[s]) {
+                tile_slots[ct * MAX_SLOTS + n++] = s;
+                if (half_mask && half_mask[ct * MAX_SLOTS + s] != fullm) partial = 1;
+            }
         }
         below[nslots] = n;
         tile_nact[ct] = n;
+        if (tile_partial) tile_partial[ct] = partial;
     }
 }
 
@@ -1460,10 +1491,15 @@ int select_mode(bool big) {
         const char *e = std::getenv("PKGPU_I8_PAIR");
         return e ? std::max(0, std::min(4, std::atoi(e))) : -1;
     }();
-    (void)big; // measured: with per-half slot masks the dual kernel also wins on the small-level run
-    return forced >= 0 ? forced : 3;
+    // measured: with per-half slot masks the dual kernel also wins on cfg2's small-level run;
+    // PKGPU_I8_SMALLMODE picks the small-run kernel for comparisons
+    static const int small_mode =
+        std::getenv("PKGPU_I8_SMALLMODE") ? std::max(0, std::min(4, std::atoi(std::getenv("PKGPU_I8_SMALLMODE")))) : 3;
+    return forced >= 0 ? forced : (big ? 3 : small_mode);
 }
 int column_tile(int mode) { return mode == 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
+
+inline size_t partial_offset(int tiles) { return ((size_t)tiles * MAX_SLOTS + 15) / 16 * 16; }
 
 // active-slot lists per column tile (ncols / column_tile(mode) tiles)
 void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode, Workspace &ws, cudaStream_t st,
@@ -1472,8 +1508,11 @@ void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode,
     *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
     *tnact = ws.get<int>("i8_tile_nact", tiles);
     *tbelow = ws.get<int>("i8_tile_below", (size_t)tiles * (MAX_SLOTS + 1));
-    uint8_t *hmask = mode >= 3 ? ws.get<uint8_t>("i8_tile_hmask", (size_t)tiles * MAX_SLOTS) : nullptr;
-    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask);
+    // per-tile masks [tiles][MAX_SLOTS] followed by the per-tile partial flags (int, see
+    // partial_flags)
+    uint8_t *hmask = mode >= 3 ? ws.get<uint8_t>("i8_tile_hmask", partial_offset(tiles) + (size_t)tiles * 4) : nullptr;
+    int *partial = mode >= 3 ? reinterpret_cast<int *>(hmask + partial_offset(tiles)) : nullptr;
+    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask, partial);
     if (thmask) *thmask = hmask;
     PK_CUDA(cudaGetLastError());
 }
@@ -1525,6 +1564,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.tile_below = tbelow;
     p.nslots = nslots;
     p.half_mask = thmask;
+    p.tile_partial = thmask ? reinterpret_cast<const int *>(thmask + partial_offset(ncols / column_tile(mode))) : nullptr;
     // slot-index windows for the small-level run (operator reuse through L2 across its
     // tiles); equal list shares for the dual-tile big levels (balanced static schedule)
     static const int by_index_env = std::getenv("PKGPU_I8_BYINDEX") ? std::atoi(std::getenv("PKGPU_I8_BYINDEX")) : -1;
@@ -1767,8 +1807,9 @@ int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspa
 int m2l_i8_level(const I8Operators &o, const I8LevelArgs &a, int beta_b, Workspace &ws, cudaStream_t st) {
     int64_t l = 0;
     I8LevelWork w = m2l_i8_prepare(o, a, beta_b, ws, st, &l);
-    for (int64_t c0 = 0; c0 < a.ncols; c0 += kI8Window) {
-        const int64_t c1 = std::min<int64_t>(a.ncols, c0 + kI8Window);
+    const int64_t win = i8_window(o.nmod, o.Ki);
+    for (int64_t c0 = 0; c0 < a.ncols; c0 += win) {
+        const int64_t c1 = std::min<int64_t>(a.ncols, c0 + win);
         l += m2l_i8_window(o, a, w, c0, c1, ws, st);
         l += m2l_i8_gemm(o, a, w, c0, c1, ws, st);
         l += m2l_i8_finish(o, a, w, c0, c1, beta_b, st);

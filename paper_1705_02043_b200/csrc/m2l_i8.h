@@ -14,7 +14,9 @@
 // results indistinguishable from the FP64 DMMA path (profiles/r01_m2l_arith_study.md).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -22,7 +24,19 @@ namespace pkgpu {
 
 constexpr int kI8MaxModuli = 20;
 constexpr int kI8Tile = 256; // columns per tile: level column counts are padded to this
-constexpr int64_t kI8Window = 65536; // columns per M2L gemm/finish window (bounds the int32 residue sums)
+constexpr int64_t kI8Window = 65536; // columns per M2L gemm/finish window
+// columns per window (PKGPU_I8_WINDOW overrides): the int32 residue sums R stay small enough
+// for their atomics to hit L2 (one window of cfg4's 262k-box level: 85.8 ms, four: 82.5 ms)
+inline int64_t i8_window(int nmod, int Ki) {
+    (void)nmod;
+    (void)Ki;
+    static const int64_t w = [] {
+        const char *e = std::getenv("PKGPU_I8_WINDOW");
+        const int64_t v = e ? std::atoll(e) : kI8Window;
+        return std::max<int64_t>(kI8Tile, v / kI8Tile * kI8Tile);
+    }();
+    return w;
+}
 
 struct I8Operators {          // residues of the stacked M2L operators (built once per KifmmOps)
     int nmod = 0, beta_a = 0, Ki = 0, nmat = 0, K = 0;
