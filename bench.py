@@ -182,8 +182,8 @@ def roofline_entry(stats, steps):
         n = max(1, i8.get("launches", 1))
         s, fl = i8["seconds"] / n, i8["flops"] / n
         achieved = fl / s / 1e12
-        return {"kernel": "m2l_i8_dual_kernel (levels 1-3 packed, level 4): M2L, tcgen05.mma kind::i8, "
-                          "TMEM accumulators", "bound": "tensor",
+        return {"kernel": "m2l_i8_dual_kernel (levels 1-3 packed) + m2l_i8_pairdual_kernel (level 4, "
+                          "cta_group::2): M2L, tcgen05.mma kind::i8, TMEM accumulators", "bound": "tensor",
                 "achieved": achieved, "peak": I8_PEAK_TOPS, "unit": "TOP/s (int8)", "frac": achieved / I8_PEAK_TOPS,
                 "traffic": I8_NCU_TRAFFIC, "traffic_note": I8_NCU_NOTE,
                 "ops_per_launch": fl, "ms_per_launch": 1e3 * s, "launches_per_step": i8["launches"] / steps,

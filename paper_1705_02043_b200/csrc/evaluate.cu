@@ -372,12 +372,15 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
         }
         if (!grouped[l]) cm += L.i8[l] ? (nl + 7) / 8 * 8 : (nl + BN - 1) / BN * BN;
         if (L.i8[l]) {
-            // close the run unless the next level is small too (runs are whole 256-column tiles)
+            // close the run unless the next level is small too. Runs are whole 256-column pair
+            // tiles (the dual kernel's); a big level is whole 512-column quads (the pair-dual
+            // kernel's tile; quarters without sources are skipped by the masks)
             const bool cont = small_level(l) && i8_level(l + 1) && small_level(l + 1) && l + 1 - run_first < kI8MaxLevels;
             if (!cont) {
-                cm = L.colbase[run_first] + (cm - L.colbase[run_first] + kI8Tile - 1) / kI8Tile * kI8Tile;
                 L.i8_last[run_first] = l;
                 L.i8_big[run_first] = run_first == l && !small_level(l) ? 1 : 0;
+                const int64_t q = L.i8_big[run_first] ? 2 * kI8Tile : kI8Tile;
+                cm = L.colbase[run_first] + (cm - L.colbase[run_first] + q - 1) / q * q;
                 run_first = -1;
             }
         }

@@ -373,6 +373,11 @@ __device__ __forceinline__ uint32_t map_to_rank(const void *p, uint32_t rank) {
 __device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
+// CTA-scope release (the PTX default): what a stage relay needs -- the relaying thread has
+// observed the stage's cp.async completion on its own barrier
+__device__ __forceinline__ void remote_arrive_cta(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
 // TMA gather4 of four 128-byte rows into consecutive (swizzled) rows at dst, completing on
 // the pair leader's barrier `bar` (a shared::cluster address)
 __device__ __forceinline__ void gather4_pair(uint32_t dst, const CUtensorMap *map, int c0, int r0, int r1, int r2,
@@ -1111,6 +1116,266 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pair-dual (cluster of 2, cta_group::2): a 512-column quad per unit, two M256 x Nt MMAs per
+// k-step issued by the leader. MMA h covers quad columns 256 h .. 256 h + 255: its rows
+// 0-127 come from CTA 0's shared memory, 128-255 from CTA 1's, and each CTA holds half of
+// the operator tile (Nt / 2 rows). Per SM and stage: 256 gathered rows + Nt / 2 operator
+// rows (46 KB at Nt = 224) for the same MACs as the dual kernel's 256 + Nt rows (60 KB) --
+// the dual kernel is bound by the per-SM L2 ingest, so the MMA rate rises with it.
+// Both CTAs gather with cp.async onto their own "full" barrier; the peer's MMA-warp lane
+// relays its completed stages to the leader ("pfull"), which issues once both are in and
+// commits "empty" / "tfull" to both CTAs (multicast). Quarter masks (bit b = quad columns
+// 128 b .. 128 b + 127 have a source) pick which MMAs run: MMA h if bit 2h or 2h+1.
+__device__ __forceinline__ void mma_i8_pair_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void commit_pair_elect(uint64_t *bar) {
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+                     tma::smem_u32(bar)),
+                 "h"((uint16_t)3)
+                 : "memory");
+}
+constexpr int PD_B_BYTES = 128 * BKI; // half operator tile, Nt / 2 <= 128 rows
+constexpr int PD_NA = 4;               // gathered-row ring (32 KB stages)
+constexpr int PD_NB = 5;               // operator ring (16 KB stages): runs further ahead
+constexpr int PD_OPER_WARP = DUAL_THREADS / 32; // warp 9: operator TMA producer
+constexpr int PD_THREADS = DUAL_THREADS + 32;
+constexpr size_t PD_RING_BYTES = (size_t)PD_NA * DUAL_A_BYTES + (size_t)PD_NB * PD_B_BYTES;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
+    m2l_i8_pairdual_kernel(const __grid_constant__ Params p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    unsigned char *ringB = smem + PD_NA * DUAL_A_BYTES;
+    int *s_epi = reinterpret_cast<int *>(smem + PD_RING_BYTES); // [4 warps][32][33]
+    __shared__ __align__(8) uint64_t fullA[PD_NA], pfullA[PD_NA], emptyA[PD_NA], fullB[PD_NB], emptyB[PD_NB], tfull,
+        tempty;
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    constexpr int NPT = DUAL_NPROD * 32;
+    const int half = p.Nt / 2;
+    if (tid == 0) {
+        for (int s = 0; s < PD_NA; s++) {
+            tma::mbar_init(&fullA[s], NPT);  // local cp.async arrivals
+            tma::mbar_init(&pfullA[s], 1);   // leader: the peer's relayed "rows landed"
+            tma::mbar_init(&emptyA[s], 1);   // the leader's multicast MMA commit
+        }
+        for (int s = 0; s < PD_NB; s++) {
+            tma::mbar_init(&fullB[s], 1);    // leader: its expect_tx (both halves' bytes land on it)
+            tma::mbar_init(&emptyB[s], 1);   // the leader's multicast MMA commit
+        }
+        tma::mbar_init(&tfull, 1);
+        tma::mbar_init(&tempty, 8); // leader: 4 local + 4 remote epilogue warps
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == DUAL_MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         tma::smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    int g = 0, jb = 0;
+    const int nquads = p.coltiles / 4;
+    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
+        int v = u;
+        const int rt = v % p.rowtiles;
+        v /= p.rowtiles;
+        const int qd = v % nquads;
+        v /= nquads;
+        const int chunk = v % p.nchunk;
+        const int t = v / p.nchunk;
+        int s0, s1;
+        chunk_range(p, qd, chunk, s0, s1);
+        const int n = (s1 - s0) * p.KC;
+        if (n == 0) continue;
+        const int *slots = p.tile_slots + qd * MAX_SLOTS;
+        const int colq = qd * 4 * TBM;
+        const uint8_t *hmt = p.half_mask + qd * MAX_SLOTS;
+        if (warp < DUAL_NPROD) {
+            // ---------------- gather producers (both CTAs): this CTA's 128 rows of each MMA ----------------
+            const int c = lane & 7, j0 = tid >> 3; // stage rows j0 + 16 i, i < 16 (row j: MMA j / 128)
+            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
+            const int cbase = colq + (int)rank * TBM;
+            for (int si = s0; si < s1; si++) {
+                const int slot = slots[si];
+                const int *srow = p.src + (int64_t)slot * p.ld_src + cbase;
+                const int hm = hmt[slot];
+                const int on = ((hm & 3) ? 1 : 0) | ((hm & 12) ? 2 : 0);
+                int bx[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int j = j0 + 16 * i;
+                    bx[i] = srow[(j & (TBM - 1)) + (j / TBM) * 2 * TBM];
+                }
+                int64_t off[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    off[i] = (int64_t)(bx[i] >= 0 ? (int)(bx[i] - p.box0) : p.zero_row) * p.Ki;
+                for (int kc = 0; kc < p.KC; kc++) {
+                    const int gi = g + (si - s0) * p.KC + kc, st = gi % PD_NA;
+                    tma::mbar_wait(&emptyA[st], ((gi / PD_NA) & 1) ^ 1);
+                    unsigned char *as = smem + st * DUAL_A_BYTES;
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 16 * i;
+                        if (((on >> (i >> 3)) & 1) && !(p.debug & 1))
+                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
+                    }
+                    tma::cp_async_mbar_arrive(&fullA[st]);
+                }
+            }
+        } else if (warp == PD_OPER_WARP) {
+            // ---------------- operator producer (both CTAs): own half tile, onto the leader's barrier ----------------
+            for (int i = 0; i < n; i++) {
+                const int gi = g + i, st = gi % PD_NB;
+                const int slot = slots[s0 + i / p.KC], kc = i % p.KC;
+                tma::mbar_wait(&emptyB[st], ((gi / PD_NB) & 1) ^ 1);
+                if (lane == 0) {
+                    const uint32_t bar = map_to_rank(&fullB[st], 0);
+                    if (leader)
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(bar),
+                                     "r"(2 * half * BKI)
+                                     : "memory");
+                    const int mat = (p.debug & 16) ? 0 : slot; // 16: one L2-resident operator
+                    asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+                                 "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tma::smem_u32(ringB + st * PD_B_BYTES)),
+                                 "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
+                                 "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + mat), "r"(bar)
+                                 : "memory");
+                }
+                __syncwarp();
+            }
+        } else if (warp == DUAL_MMA_WARP) {
+            if (!leader) {
+                // ---------------- relay (peer): own rows landed -> leader's pfullA ----------------
+                for (int i = 0; i < n; i++) {
+                    const int gi = g + i, st = gi % PD_NA;
+                    tma::mbar_wait(&fullA[st], (gi / PD_NA) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    if (lane == 0) {
+                        if (p.debug & 64)
+                            remote_arrive(map_to_rank(&pfullA[st], 0));
+                        else
+                            remote_arrive_cta(map_to_rank(&pfullA[st], 0));
+                    }
+                    __syncwarp();
+                }
+            } else {
+                // ---------------- MMA issuer (leader; whole warp, elected lane) ----------------
+                tma::mbar_wait(&tempty, (jb & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t abase = tma::smem_u32(smem), bbase = tma::smem_u32(ringB);
+                // tiles whose every active slot feeds all four quarters issue unconditionally
+                const bool all = __reduce_or_sync(0xffffffffu, (unsigned)p.tile_partial[qd]) == 0u;
+                bool started0 = false, started1 = false;
+                int hm = hmt[slots[s0]];
+                int hm_next = s0 + 1 < s1 ? hmt[slots[s0 + 1]] : 0;
+                for (int i = 0, kc = 0, si = s0; i < n; i++) {
+                    const int gi = g + i, sa = gi % PD_NA, sb = gi % PD_NB;
+                    tma::mbar_wait(&fullA[sa], (gi / PD_NA) & 1);
+                    tma::mbar_wait(&pfullA[sa], (gi / PD_NA) & 1);
+                    tma::mbar_wait(&fullB[sb], (gi / PD_NB) & 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    tc_fence_after();
+                    const uint32_t a0 = abase + sa * DUAL_A_BYTES;
+                    const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES),
+                                   bd = sw128_desc(bbase + sb * PD_B_BYTES);
+                    if (all) {
+#pragma unroll
+                        for (int kk = 0; kk < BKI / 32; kk++) {
+                            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                            mma_i8_pair_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                            mma_i8_pair_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, acc);
+                        }
+                    } else {
+                        const unsigned hu = __reduce_or_sync(0xffffffffu, (unsigned)hm);
+                        const bool on0 = (hu & 3u) != 0, on1 = (hu & 12u) != 0;
+#pragma unroll
+                        for (int kk = 0; kk < BKI / 32; kk++) {
+                            if (on0)
+                                mma_i8_pair_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc,
+                                                  (started0 || kk > 0) ? 1u : 0u);
+                            if (on1)
+                                mma_i8_pair_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc,
+                                                  (started1 || kk > 0) ? 1u : 0u);
+                        }
+                        started0 |= on0;
+                        started1 |= on1;
+                        if (++kc == p.KC) {
+                            kc = 0;
+                            si++;
+                            hm = hm_next;
+                            hm_next = si + 1 < s1 ? hmt[slots[si + 1]] : 0;
+                        }
+                    }
+                    commit_pair_elect(&emptyA[sa]);
+                    commit_pair_elect(&emptyB[sb]);
+                }
+                commit_pair_elect(&tfull);
+            }
+            __syncwarp();
+        } else {
+            // ---------------- epilogue (both CTAs: own 128 lanes of each accumulator) ----------------
+            const int q = warp & 3;
+            int *tile = s_epi + (warp - DUAL_MMA_WARP - 1) * 32 * EPI_PITCH;
+            tma::mbar_wait(&tfull, jb & 1);
+            tc_fence_after();
+            const int m = c_mod[t];
+            const float inv = 1.0f / (float)m;
+            const int r0 = rt * p.Nt;
+            const int nr = min(p.Nt, p.Ki - r0);
+            int used = 0; // MMAs issued in this unit (the others' TMEM is stale)
+            for (int si = s0 + lane; si < s1; si += 32) used |= hmt[slots[si]];
+            for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
+            for (int h = 0; h < 2; h++) {
+                if (!((used >> (2 * h)) & 3)) continue;
+                int *Rt = p.R + ((int64_t)t * p.ncols + colq + h * 2 * TBM + (int)rank * TBM + q * 32) * p.Ki + r0;
+                for (int j0 = 0; j0 < p.Nt; j0 += 32) {
+                    uint32_t vv[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + j0, vv);
+#pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        const int a = (int)vv[j];
+                        tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
+                    }
+                    __syncwarp();
+                    const bool ok = j0 + lane < nr;
+#pragma unroll 8
+                    for (int b = 0; b < 32; b++) {
+                        const int r = tile[b * EPI_PITCH + lane];
+                        if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
+                    }
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) remote_arrive(map_to_rank(&tempty, 0));
+        }
+        g += n;
+        jb++;
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == DUAL_MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+    }
+}
+
 
 // active slots per column tile of `bn` columns, in slot order
 // half_mask (bn = 256 / 512): bit q set when the 128-column quarter q has a source
@@ -1482,22 +1747,36 @@ namespace {
 // kernel variant per launch: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
 // (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
 // (m2l_i8_dual_kernel), 4 dual tile + operator multicast across a CTA pair (m2l_i8_dualmc_kernel,
-// 2% faster at cfg2 level 4, slower on the small-level run). Default: dual everywhere (8 MMAs per pipeline stage, half the
-// operator bytes per MAC; a pair tile's halves with no source for a slot skip its gather
-// and MMA). i8_gather_gemm (tests) keeps the single kernel below 2048 columns so both stay
-// covered. PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
+// 2% faster at cfg2 level 4, slower on the small-level run), 5 pair-dual (cta_group::2, 512-column
+// quads, m2l_i8_pairdual_kernel). Default: pair-dual for big levels (cfg2 level 4 6.86 -> 6.63
+// ms, cfg3 608 -> 518 ms per evaluate), dual for the small-level runs (the pair-dual kernel's
+// 1024-column run streams the operators as often and balances worse: 2.6 -> 3.9 ms at cfg2).
+// A tile's quarters / halves with no source for a slot skip their gather and MMA.
+// i8_gather_gemm (tests) keeps the single kernel below 2048 columns so all stay covered.
+// PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
 int select_mode(bool big) {
     static const int forced = [] {
         const char *e = std::getenv("PKGPU_I8_PAIR");
-        return e ? std::max(0, std::min(4, std::atoi(e))) : -1;
+        return e ? std::max(0, std::min(5, std::atoi(e))) : -1;
     }();
     // measured: with per-half slot masks the dual kernel also wins on cfg2's small-level run;
     // PKGPU_I8_SMALLMODE picks the small-run kernel for comparisons
     static const int small_mode =
-        std::getenv("PKGPU_I8_SMALLMODE") ? std::max(0, std::min(4, std::atoi(std::getenv("PKGPU_I8_SMALLMODE")))) : 3;
-    return forced >= 0 ? forced : (big ? 3 : small_mode);
+        std::getenv("PKGPU_I8_SMALLMODE") ? std::max(0, std::min(5, std::atoi(std::getenv("PKGPU_I8_SMALLMODE")))) : 3;
+    static const int big_mode =
+        std::getenv("PKGPU_I8_BIGMODE") ? std::max(0, std::min(5, std::atoi(std::getenv("PKGPU_I8_BIGMODE")))) : 5;
+    return forced >= 0 ? forced : (big ? big_mode : small_mode);
 }
-int column_tile(int mode) { return mode == 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
+// operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
+int rowtiles_of(int Ki) { return (Ki + 255) / 256; }
+int nt_of(int Ki) { return ((Ki + rowtiles_of(Ki) - 1) / rowtiles_of(Ki) + 15) / 16 * 16; }
+// the 512-column variants need whole quads; the pair-dual one also Nt / 2 a multiple of 16
+int window_mode(int mode, int ncols, int Ki) {
+    if (mode >= 4 && ncols % (4 * TBM) != 0) return 3;
+    if (mode == 5 && nt_of(Ki) % 32 != 0) return 3;
+    return mode;
+}
+int column_tile(int mode) { return mode >= 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
 
 inline size_t partial_offset(int tiles) { return ((size_t)tiles * MAX_SLOTS + 15) / 16 * 16; }
 
@@ -1535,16 +1814,15 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.nmat = nmat;
     p.nmod = nmod;
     p.KC = Ki / BKI;
-    // operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
-    p.rowtiles = (Ki + 255) / 256;
-    p.Nt = ((Ki + p.rowtiles - 1) / p.rowtiles + 15) / 16 * 16;
+    p.rowtiles = rowtiles_of(Ki);
+    p.Nt = nt_of(Ki);
     p.coltiles = ncols / TBM;
     p.ncols = ncols;
     p.Ki = Ki;
     p.R = R;
     // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
     // both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the CTA pair)
-    const int M = mode == 1 ? 2 * TBM : TBM;
+    const int M = (mode == 1 || mode == 5) ? 2 * TBM : TBM;
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     static const int debug = std::getenv("PKGPU_I8_DEBUG") ? std::atoi(std::getenv("PKGPU_I8_DEBUG")) : 0;
     p.debug = debug;
@@ -1552,8 +1830,8 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     int nchunk = (int)((nslots + cmax - 1) / cmax);
     static const int min_chunks = std::getenv("PKGPU_I8_CHUNKS") ? std::atoi(std::getenv("PKGPU_I8_CHUNKS")) : 0;
     nchunk = std::max(nchunk, min_chunks);
-    const int64_t base = (int64_t)nmod * p.rowtiles * (mode == 4 ? p.coltiles / 4 : pair ? p.coltiles / 2 : p.coltiles);
-    const int64_t resident = (mode == 1 || mode == 2 || mode == 4) ? num_sms / 2 : num_sms;
+    const int64_t base = (int64_t)nmod * p.rowtiles * (mode >= 4 ? p.coltiles / 4 : pair ? p.coltiles / 2 : p.coltiles);
+    const int64_t resident = (mode == 1 || mode == 2 || mode >= 4) ? num_sms / 2 : num_sms;
     while (base * nchunk < 3 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
@@ -1572,7 +1850,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
     // the CTA-pair variants stage half of the operator tile per CTA
-    const bool half_tile = mode == 1 || mode == 2 || mode == 4;
+    const bool half_tile = mode == 1 || mode == 2 || mode >= 4;
     const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
@@ -1592,7 +1870,20 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
             throw CudaError("cuTensorMapEncodeTiled (int8 gather) failed (" + std::to_string((int)rx) + ")");
     }
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    if (mode == 4) {
+    if (mode == 5) {
+        static const int prefetch = std::getenv("PKGPU_I8_PREFETCH") ? std::atoi(std::getenv("PKGPU_I8_PREFETCH")) : 0;
+        p.prefetch = prefetch;
+        if (ncols % (4 * TBM) != 0) throw RuntimeError("i8 gemm: the pair-dual kernel needs 512-column multiples");
+        if (p.Nt % 32 != 0 || p.Nt / 2 > 128) throw RuntimeError("i8 pair-dual kernel: Nt / 2 must be a multiple of 16");
+        const size_t smem = PD_RING_BYTES + epi;
+        static bool cfg = false;
+        if (!cfg) {
+            PK_CUDA(cudaFuncSetAttribute(m2l_i8_pairdual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cfg = true;
+        }
+        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
+        m2l_i8_pairdual_kernel<<<grid, PD_THREADS, smem, st>>>(p);
+    } else if (mode == 4) {
         if (ncols % (4 * TBM) != 0) throw RuntimeError("i8 gemm: the multicast dual kernel needs 512-column multiples");
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
         static bool cfg = false;
@@ -1668,7 +1959,7 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     upload_tables();
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
     int mode = ncols >= 2048 ? select_mode(true) : 0;
-    if (mode == 4 && ncols % (4 * TBM) != 0) mode = 3;
+    mode = window_mode(mode, ncols, Ki);
     uint8_t *thmask = nullptr;
     scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
@@ -1721,7 +2012,7 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
     // the multicast variant needs whole 512-column quads; other windows use the dual kernel
-    w.win_mode = (w.mode == 4 && ncols % (4 * TBM) != 0) ? 3 : w.mode;
+    w.win_mode = window_mode(w.mode, ncols, o.Ki);
     scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.win_mode, ws, st, &w.tile_slots, &w.tile_nact,
                &w.tile_below, &w.tile_hmask);
     if (a.mma_rows && w.tile_hmask) {

@@ -6,6 +6,10 @@
     same tolerances against the reference as the FP64 DMMA path, with every level >= 1
     forced onto it.
 """
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -27,7 +31,8 @@ def host_residue_gemm(A, B, src, box0, zero_row):
     return R.astype(np.int64)
 
 
-# ncols >= 2048 runs the dual-tile kernel (two 128-box accumulators per operator tile)
+# ncols >= 2048 runs the big-level kernel (pair-dual: cta_group::2, 512-column quads); the
+# other variants are covered by test_gather_gemm_exact_other_variants
 @pytest.mark.parametrize("Ki,nslots,ncols,nmod", [(128, 3, 256, 2), (384, 7, 512, 3), (896, 12, 256, 2),
                                                   (1536, 5, 512, 1), (896, 9, 2048, 1), (384, 4, 2560, 2)])
 def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
@@ -51,6 +56,16 @@ def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
         bad = np.count_nonzero((got[t] - ref[t]) % m)
         assert bad == 0, f"modulus {m}: {bad} of {got[t].size} entries wrong"
         assert np.abs(got[t]).max() <= 128 * nslots  # reduced per unit before the atomics
+
+
+@pytest.mark.parametrize("mode", [3, 4])
+def test_gather_gemm_exact_other_variants(mode):
+    """The exactness cases with every launch forced onto another kernel variant (3 dual tile,
+    4 dual tile + operator multicast); the variant is read once per process."""
+    env = dict(os.environ, PKGPU_I8_PAIR=str(mode))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_i8_gather_gemm_exact"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 @pytest.fixture(scope="module")

@@ -1,0 +1,6 @@
+R=r119
+source tools/gpu_run45_fn.sh
+PKGPU_I8_PAIR=5 timeout 300 python -m pytest tests/test_gpu_i8.py -q -x -k "exact" 2>&1 | tail -1
+PKGPU_I8_PAIR=5 ll pd
+PKGPU_I8_PAIR=5 PKGPU_I8_DEBUG=1 ll pd_d1
+PKGPU_I8_PAIR=5 PKGPU_I8_DEBUG=16 ll pd_d16
