@@ -40,9 +40,9 @@ FP64_PEAK_SOURCE = "measured: DMMA.8x8x4 loop, 148 SMs @1965 MHz (profiles/r01_f
 I8_PEAK_TOPS = 4595.7  # measured tcgen05 kind::i8 loop (tools/i8_peak.cu, profiles/r01_i8_peak.json)
 I8_PEAK_SOURCE = "measured: tcgen05.mma kind::i8 M128 N256 K32 loop from shared memory, 148 SMs " \
                  "(tools/i8_peak.cu, profiles/r01_i8_peak.json)"
-I8_NCU_TRAFFIC = 10.42e9  # dram read + write bytes per int8 M2L launch (profiles/r01_final_m2l_ncu.txt)
-I8_NCU_NOTE = "ncu --set full capture of the cfg2 step's two int8 M2L launches (small-level run: 10.11 GB, " \
-              "level 4: 10.74 GB), mean per launch"
+I8_NCU_TRAFFIC = 10.62e9  # dram read + write bytes per int8 M2L launch (profiles/r01_pairdual_m2l_ncu.txt)
+I8_NCU_NOTE = "ncu --set full capture of the cfg2 step's two int8 M2L launches (small-level run on the dual " \
+              "kernel: 9.93 GB, level 4 on the pair-dual kernel: 11.31 GB), mean per launch"
 REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",

@@ -469,8 +469,17 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
         const char *e = std::getenv("PKGPU_GEMM_MINIT");
         return (int64_t)(e ? std::max(1, std::atoi(e)) : 16);
     }();
+    // pseudo-inverse factors (one slot) on grids smaller than the resident CTAs (the top
+    // levels: 1-512 columns) are latency-bound -- shorter units spread them over the machine
+    // (measured at cfg2: pinv 1.06 -> 0.91 ms per direction with 4; the 8-slot M2M / L2L
+    // lose with shorter units: more partials to reduce)
+    static const int64_t min_iters_small = [] {
+        const char *e = std::getenv("PKGPU_GEMM_MINIT_SMALL");
+        return (int64_t)(e ? std::max(1, std::atoi(e)) : 4);
+    }();
+    const int64_t mi = (base < resident && a.nslots == 1) ? min_iters_small : min_iters;
     if (base < want)
-        nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / min_iters), 64});
+        nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / mi), 64});
     nsplit = std::max(nsplit, 1);
     KParams kp{};
     kp.a = a;
