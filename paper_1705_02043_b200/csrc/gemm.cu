@@ -54,8 +54,8 @@ struct KParams {
     GemmArgs a;
     int nsplit;
     double *part;           // [nsplit][ncols][Kp] when nsplit > 1
-    const int *tile_slots;  // [coltiles][MAX_SLOTS] active slots per column tile
-    const int *tile_nact;   // [coltiles]
+    const int *tile_slots;  // [coltiles][MAX_SLOTS] active slots per column tile (null: slot si = si)
+    const int *tile_nact;   // [coltiles] (null: every tile has the one slot of an identity gather)
     int rowtiles, coltiles; // unit = row + rowtiles * (col + coltiles * split)
     int total_units;
     int *counter;           // persistent scheduler
@@ -135,9 +135,9 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rt = blockIdx.x, ct = blockIdx.y, split = blockIdx.z;
     const int row0 = rt * BM, col0 = ct * BN;
-    const int *slots = kp.tile_slots + ct * MAX_SLOTS;
+    const int *slots = kp.tile_slots ? kp.tile_slots + ct * MAX_SLOTS : nullptr;
     int it0, it1;
-    unit_range(kp, kp.tile_nact[ct], split, it0, it1);
+    unit_range(kp, kp.tile_nact ? kp.tile_nact[ct] : 1, split, it0, it1);
     const int nk = a.Kp / BK;
 
     double acc[4][4][2];
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams k
         for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     auto load_stage = [&](int it, int stage) {
-        const int slot = slots[it / nk];
+        const int slot = slots ? slots[it / nk] : it / nk;
         const int k0 = (it % nk) * BK;
         const double *Am = a.A + (int64_t)slot_matrix(a, slot, ct) * a.Kp * a.Kp;
         double *as = As + stage * BM * PAD;
@@ -267,9 +267,9 @@ __global__ void __maxnreg__(96)
         const int rest = unit / kp.rowtiles;
         const int ct = rest % kp.coltiles, split = rest / kp.coltiles;
         const int row0 = rt * BM, col0 = ct * BNT;
-        const int *slots = kp.tile_slots + ct * MAX_SLOTS;
+        const int *slots = kp.tile_slots ? kp.tile_slots + ct * MAX_SLOTS : nullptr;
         int it0, it1;
-        unit_range(kp, kp.tile_nact[ct], split, it0, it1);
+        unit_range(kp, kp.tile_nact ? kp.tile_nact[ct] : 1, split, it0, it1);
         const int n = it1 - it0;
         if (warp == NCW) {
             // ---------------- producer ----------------
@@ -282,7 +282,7 @@ __global__ void __maxnreg__(96)
                 const int si = it / nk, k0 = (it % nk) * BK;
                 if (si != cur) {
                     cur = si;
-                    const int slot = slots[si];
+                    const int slot = slots ? slots[si] : si;
                     mat = slot_matrix(a, slot, ct);
                     __syncwarp();
                     for (int j = lane; j < BNT; j += 32) s_rowsrc[j] = col_src(a, slot, col0 + j);
@@ -488,12 +488,15 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     kp.coltiles = coltiles;
     kp.total_units = (int)(base * nsplit);
     if (nsplit > 1) kp.part = ws.get<double>("gemm_part", (size_t)nsplit * a.ncols * a.Kp);
-    int *tslots = ws.get<int>("gemm_tile_slots", (size_t)coltiles * MAX_SLOTS);
-    int *tnact = ws.get<int>("gemm_tile_nact", coltiles);
-    slot_scan_kernel<<<coltiles, 256, 0, st>>>(a, bnt, tslots, tnact);
-    kp.tile_slots = tslots;
-    kp.tile_nact = tnact;
-    int launches = 1;
+    int launches = 0;
+    if (a.src || a.nslots != 1) { // an identity gather's one slot is active in every tile
+        int *tslots = ws.get<int>("gemm_tile_slots", (size_t)coltiles * MAX_SLOTS);
+        int *tnact = ws.get<int>("gemm_tile_nact", coltiles);
+        slot_scan_kernel<<<coltiles, 256, 0, st>>>(a, bnt, tslots, tnact);
+        kp.tile_slots = tslots;
+        kp.tile_nact = tnact;
+        launches = 1;
+    }
     if (tma_path) {
         kp.counter = ws.get<int>("gemm_counter", 1);
         PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
