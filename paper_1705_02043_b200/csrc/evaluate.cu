@@ -379,7 +379,9 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             if (!cont) {
                 L.i8_last[run_first] = l;
                 L.i8_big[run_first] = run_first == l && !small_level(l) ? 1 : 0;
-                const int64_t q = L.i8_big[run_first] ? 2 * kI8Tile : kI8Tile;
+                static const int64_t small_pad =
+                    std::getenv("PKGPU_I8_SMALLPAD") ? std::atoll(std::getenv("PKGPU_I8_SMALLPAD")) : kI8Tile;
+                const int64_t q = L.i8_big[run_first] ? 2 * kI8Tile : small_pad;
                 cm = L.colbase[run_first] + (cm - L.colbase[run_first] + q - 1) / q * q;
                 run_first = -1;
             }

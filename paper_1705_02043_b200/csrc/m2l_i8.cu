@@ -801,6 +801,16 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
                             tma::mbar_expect_tx(&full[st], p.Nt * BKI);
                             tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot,
                                              &full[st]);
+                            if (p.prefetch > 0) { // L2 prefetch of the operator tile p.prefetch stages ahead
+                                const int ia = (si - s0) * p.KC + kc + p.prefetch;
+                                const int sa = s0 + ia / p.KC, ka = ia % p.KC;
+                                if (sa < s1)
+                                    asm volatile(
+                                        "cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
+                                            reinterpret_cast<uint64_t>(&p.tmB)),
+                                        "r"(ka * BKI), "r"(rt * p.Nt), "r"(t * p.nmat + slots[sa])
+                                        : "memory");
+                            }
                         }
                     }
 #pragma unroll
@@ -1894,6 +1904,8 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
         m2l_i8_dualmc_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
     } else if (mode == 3) {
+        static const int prefetch = std::getenv("PKGPU_I8_DUALPF") ? std::atoi(std::getenv("PKGPU_I8_DUALPF")) : 0;
+        p.prefetch = prefetch;
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
         static bool cfg = false;
         if (!cfg) {
