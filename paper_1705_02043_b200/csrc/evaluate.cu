@@ -690,11 +690,13 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
     const double *d_src = req.sources, *d_str = req.strengths, *d_trg = req.targets;
     double *d_out = out;
     if (!req.device_pointers) {
+        // targets passed as the sources' own buffer (the usual self-evaluation) go over once
+        const bool same = req.targets == req.sources && nt == ns;
         double *s = ws.get<double>("in_src", 3 * ns + 1), *q = ws.get<double>("in_str", ks * ns + 1),
-               *t = ws.get<double>("in_trg", 3 * nt + 1);
+               *t = same ? s : ws.get<double>("in_trg", 3 * nt + 1);
         if (ns) PK_CUDA(cudaMemcpyAsync(s, req.sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
         if (ns) PK_CUDA(cudaMemcpyAsync(q, req.strengths, ks * ns * sizeof(double), cudaMemcpyHostToDevice, st));
-        if (nt) PK_CUDA(cudaMemcpyAsync(t, req.targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (nt && !same) PK_CUDA(cudaMemcpyAsync(t, req.targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
         d_src = s, d_str = q, d_trg = t;
         d_out = ws.get<double>("out", kt * nt + 1);
     }

@@ -242,9 +242,16 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     size_t temp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, k_in, skeys, i_in, T.src_perm, (int)nmax, 0, 36, st);
     void *temp = ws.get<char>("sort_temp", temp_bytes);
+    // targets that are the sources (same buffer) sort once; the keys and order are copied
+    const bool same = d_trg == d_src && nt == ns;
     for (int pass = 0; pass < 2; pass++) {
         const int64_t n = pass == 0 ? ns : nt;
         if (n == 0) continue;
+        if (pass == 1 && same) {
+            PK_CUDA(cudaMemcpyAsync(tkeys, skeys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            PK_CUDA(cudaMemcpyAsync(T.trg_perm, T.src_perm, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+            continue;
+        }
         keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(pass == 0 ? d_src : d_trg, n, k_in, i_in, flags);
         size_t tb = temp_bytes;
         PK_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k_in, pass == 0 ? skeys : tkeys, i_in,
@@ -253,6 +260,7 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     }
     PK_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
     PK_CUDA(cudaStreamSynchronize(st));
+    if (same) h_flags[0] *= 2; // the reference counts the targets' offenders as well
     if (h_flags[0] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[0]);
 
     // level-synchronous construction
