@@ -1391,33 +1391,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
 // half_mask (bn = 256 / 512): bit q set when the 128-column quarter q has a source
 __global__ void slot_scan_kernel(const int *__restrict__ src, int64_t ld_src, int nslots, int bn, int *tile_slots,
                                  int *tile_nact, int *tile_below, uint8_t *half_mask, int *tile_partial) {
-    __shared__ int flag[MAX_SLOTS];
+    __shared__ unsigned qm[MAX_SLOTS];
     const int ct = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = warp; s < nslots; s += blockDim.x / 32) {
         unsigned m = 0; // bit q: the 128-column quarter q of the tile has a source
+#pragma unroll 4
         for (int j = lane; j < bn; j += 32)
             if (src[(int64_t)s * ld_src + (int64_t)ct * bn + j] >= 0) m |= 1u << (j / TBM);
         m = __reduce_or_sync(0xffffffffu, m);
         if (lane == 0) {
-            flag[s] = m ? 1 : 0;
+            qm[s] = m;
             if (half_mask) half_mask[ct * MAX_SLOTS + s] = (uint8_t)m;
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int n = 0, partial = 0;
+    if (warp == 0) { // active-slot list, "below" prefix counts and the partial flag, 32 slots per step
+        int n = 0;
+        unsigned partial = 0;
         int *below = tile_below + ct * (MAX_SLOTS + 1);
-        const int fullm = (1 << (bn / TBM)) - 1;
-        for (int s = 0; s < nslots; s++) {
-            below[s] = n;
-            if (flag[s]) {
-                tile_slots[ct * MAX_SLOTS + n++] = s;
-                if (half_mask && half_mask[ct * MAX_SLOTS + s] != fullm) partial = 1;
+        const unsigned fullm = (1u << (bn / TBM)) - 1;
+        for (int s0 = 0; s0 < nslots; s0 += 32) {
+            const int s = s0 + lane;
+            const unsigned m = s < nslots ? qm[s] : 0u;
+            const unsigned bal = __ballot_sync(0xffffffffu, m != 0);
+            const int pre = n + __popc(bal & ((1u << lane) - 1));
+            if (s < nslots) {
+                below[s] = pre;
+                if (m) tile_slots[ct * MAX_SLOTS + pre] = s;
             }
+            partial |= (m && m != fullm) ? 1u : 0u;
+            n += __popc(bal);
         }
-        below[nslots] = n;
-        tile_nact[ct] = n;
-        if (tile_partial) tile_partial[ct] = partial;
+        partial = __reduce_or_sync(0xffffffffu, partial);
+        if (lane == 0) {
+            below[nslots] = n;
+            tile_nact[ct] = n;
+            if (tile_partial) tile_partial[ct] = (int)partial;
+        }
     }
 }
 
@@ -1801,7 +1811,7 @@ void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode,
     // partial_flags)
     uint8_t *hmask = mode >= 3 ? ws.get<uint8_t>("i8_tile_hmask", partial_offset(tiles) + (size_t)tiles * 4) : nullptr;
     int *partial = mode >= 3 ? reinterpret_cast<int *>(hmask + partial_offset(tiles)) : nullptr;
-    slot_scan_kernel<<<tiles, 256, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask, partial);
+    slot_scan_kernel<<<tiles, 1024, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask, partial);
     if (thmask) *thmask = hmask;
     PK_CUDA(cudaGetLastError());
 }
