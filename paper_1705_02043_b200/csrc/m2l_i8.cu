@@ -1788,12 +1788,13 @@ int select_mode(bool big) {
     return forced >= 0 ? forced : (big ? big_mode : small_mode);
 }
 // operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
-int rowtiles_of(int Ki) { return (Ki + 255) / 256; }
-int nt_of(int Ki) { return ((Ki + rowtiles_of(Ki) - 1) / rowtiles_of(Ki) + 15) / 16 * 16; }
+// (from the true K: operator rows past K inside the 128-padded Ki are never computed)
+int rowtiles_of(int K) { return (K + 255) / 256; }
+int nt_of(int K) { return ((K + rowtiles_of(K) - 1) / rowtiles_of(K) + 31) / 32 * 32; }
 // the 512-column variants need whole quads; the pair-dual one also Nt / 2 a multiple of 16
-int window_mode(int mode, int ncols, int Ki) {
+int window_mode(int mode, int ncols, int K) {
     if (mode >= 4 && ncols % (4 * TBM) != 0) return 3;
-    if (mode == 5 && nt_of(Ki) % 32 != 0) return 3;
+    if (mode == 5 && nt_of(K) % 32 != 0) return 3;
     return mode;
 }
 int column_tile(int mode) { return mode >= 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
@@ -1819,7 +1820,7 @@ void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode,
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
                  const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false,
-                 const uint8_t *thmask = nullptr) {
+                 const uint8_t *thmask = nullptr, int K = 0) {
     if (mode >= 3 && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernel needs the half masks");
     const int num_sms = sm_count();
     const bool pair = mode != 0;
@@ -1834,8 +1835,9 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.nmat = nmat;
     p.nmod = nmod;
     p.KC = Ki / BKI;
-    p.rowtiles = rowtiles_of(Ki);
-    p.Nt = nt_of(Ki);
+    if (K <= 0) K = Ki;
+    p.rowtiles = rowtiles_of(K);
+    p.Nt = nt_of(K);
     p.coltiles = ncols / TBM;
     p.ncols = ncols;
     p.Ki = Ki;
@@ -2034,7 +2036,7 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
     // the multicast variant needs whole 512-column quads; other windows use the dual kernel
-    w.win_mode = window_mode(w.mode, ncols, o.Ki);
+    w.win_mode = window_mode(w.mode, ncols, o.K);
     scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.win_mode, ws, st, &w.tile_slots, &w.tile_nact,
                &w.tile_below, &w.tile_hmask);
     if (a.mma_rows && w.tile_hmask) {
@@ -2052,7 +2054,7 @@ int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int6
     if (ncols <= 0) return 0;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
                 a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.win_mode, st, false,
-                w.tile_hmask);
+                w.tile_hmask, o.K);
     return 1;
 }
 
@@ -2098,7 +2100,7 @@ int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspa
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
     scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, 0, ws, st, &tslots, &tnact, &tbelow);
     launch_gemm(o.res, o.nmat, xres, (int)(nsrc + 1), (int)nsrc, Ki, nmod, a.src, a.ld_src, a.src_lo, a.nslots,
-                a.ncols, R, tslots, tnact, tbelow, 0, st, direct);
+                a.ncols, R, tslots, tnact, tbelow, 0, st, direct, nullptr, o.K);
     const int64_t n = (int64_t)a.ncols * Ki;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
     const int bs = o.beta_a + beta_b;
