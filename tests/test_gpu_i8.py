@@ -68,6 +68,17 @@ def test_gather_gemm_exact_other_variants(mode):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_int8_all_levels_on_the_pair_dual_kernel():
+    """End to end with every level >= 1 laid out as its own big run (PKGPU_I8_SMALL=0): the
+    pair-dual kernel then serves levels of 8-4096 boxes on the adaptive golden cases too --
+    quads with empty quarters and partial offset masks."""
+    env = dict(os.environ, PKGPU_I8_SMALL="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_evaluate_int8_all_levels_vs_reference"], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.fixture(scope="module")
 def i8_everywhere():
     ctx = pk.Context(0)
