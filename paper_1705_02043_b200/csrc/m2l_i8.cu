@@ -1875,9 +1875,17 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     const bool half_tile = mode == 1 || mode == 2 || mode >= 4;
     const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    // L2 sector promotion of the operator rows (PKGPU_I8_L2PROMO = 0 / 64 / 128 / 256, default 256)
+    static const CUtensorMapL2promotion promo = [] {
+        const int v = std::getenv("PKGPU_I8_L2PROMO") ? std::atoi(std::getenv("PKGPU_I8_L2PROMO")) : 256;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
     if (mode == 1) {
         if (p.Nt % 32 != 0) throw RuntimeError("i8 pair kernel: Nt / 2 must be a multiple of 16");
