@@ -44,6 +44,11 @@ I8_NCU_TRAFFIC = 10.62e9  # dram read + write bytes per int8 M2L launch (profile
 I8_NCU_NOTE = "ncu --set full capture of the cfg2 step's two int8 M2L launches (small-level run on the dual " \
               "kernel: 9.93 GB, level 4 on the pair-dual kernel: 11.31 GB), mean per launch"
 REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
+# the reference arm: built for the GPU host's CPU (oracle/refbuild/Makefile refdump_native)
+REFDUMP_NATIVE = os.path.join(REPO, "oracle", "_ref", "refdump_native")
+FP64_VEC_PEAK_TFLOPS = 34.23  # measured DFMA loop on this pool (profiles/r01_fp64_peaks.jsonl)
+FP64_VEC_PEAK_SOURCE = "measured: DFMA loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl)"
+LEAF_NCU_TRAFFIC = 40.5e6  # dram read + write bytes per leaf_kernel launch (profiles/r02_leaf_ncu.txt)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
            0x100: "display_clock_setting"}
@@ -121,34 +126,77 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_info():
+    """CPU model, logical CPUs and physical cores of this host (/proc/cpuinfo)."""
+    model, cores = None, set()
+    phys = core = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and model is None:
+                    model = v
+                elif k == "physical id":
+                    phys = v
+                elif k == "core id":
+                    core = v
+                elif not k and phys is not None:
+                    cores.add((phys, core))
+                    phys = core = None
+    except OSError:
+        pass
+    if phys is not None:
+        cores.add((phys, core))
+    logical = len(os.sched_getaffinity(0))
+    return {"model": model, "logical_cpus": logical, "physical_cores": min(logical, len(cores) or logical)}
+
+
+def reference_binary():
+    """refdump_native where it runs on this host, else the portable refdump."""
+    for b in (REFDUMP_NATIVE, REFDUMP):
+        if os.path.exists(b):
+            r = subprocess.run([b], capture_output=True, text=True)
+            if "usage" in (r.stderr + r.stdout):
+                return b
+    return None
+
+
 def cpu_reference(steps, warmup, threads=None, budget_s=150.0):
     """The reference's own CPU evaluate (oracle/_ref, compiled from /root/reference) on
-    this host's cores: full cfg2 evaluate per step, warm (operators prebuilt)."""
-    if not os.path.exists(REFDUMP):
+    this host's physical cores (OMP / OpenBLAS threads): full cfg2 evaluate
+    per step, warm -- the warm-up evaluates (the first builds the KIFMM operators) run in
+    the same process as the timed ones and are dropped."""
+    binary = reference_binary()
+    if binary is None:
         return None
-    threads = threads or os.cpu_count()
+    ci = cpu_info()
+    threads = threads or ci["physical_cores"]
     env = dict(os.environ, OMP_NUM_THREADS=str(threads), OPENBLAS_NUM_THREADS=str(threads))
     with tempfile.TemporaryDirectory() as tmp:
         base = os.path.join(tmp, "c2")
-        subprocess.run([REFDUMP, "gen", "--n", str(N_POINTS), "--kind", "uniform", "--ks", "3", "--seed", "12345",
+        subprocess.run([binary, "gen", "--n", str(N_POINTS), "--kind", "uniform", "--ks", "3", "--seed", "12345",
                         "--out", base], check=True, capture_output=True, env=env)
-        args = [REFDUMP, "eval", "--kernel", "stokeslet", "--per", "tp", "--ell", "2", "--p", str(P_ORDER),
+        args = [binary, "eval", "--kernel", "stokeslet", "--per", "tp", "--ell", "2", "--p", str(P_ORDER),
                 "--leaf", str(LEAF), "--src", base + ".src.f64", "--str", base + ".str.f64", "--op", OP_PATH,
                 "--threads", str(threads)]
-        # warm-up run (also measures one step to size the sample)
+        # sizing probe (one cold evaluate; not reported)
         t0 = time.time()
-        r = subprocess.run(args + ["--repeat", str(max(1, warmup))], check=True, capture_output=True, text=True,
-                           env=env)
-        t_step = (time.time() - t0) / max(1, warmup)
-        n = max(1, min(steps, int(budget_s / max(t_step, 1e-3))))
-        r = subprocess.run(args + ["--repeat", str(n)], check=True, capture_output=True, text=True, env=env)
+        subprocess.run(args + ["--repeat", "1"], check=True, capture_output=True, text=True, env=env)
+        t_step = time.time() - t0
+        wu = max(1, warmup)
+        n = max(1, min(steps, int(budget_s / max(t_step, 1e-3)) - wu))
+        r = subprocess.run(args + ["--repeat", str(wu + n)], check=True, capture_output=True, text=True, env=env)
         res = json.loads(r.stdout.strip().splitlines()[-1])
-    walls = [x["wall"] for x in res["runs"]]
+    runs = res["runs"][wu:]
+    walls = [x["wall"] for x in runs]
     return {"value": N_POINTS / float(np.mean(walls)), "unit": UNIT, "cores": threads, "kind": "reference",
             "steps_timed": n, "seconds_per_step": float(np.mean(walls)),
-            "phases_s": {k: float(np.mean([x[k] for x in res["runs"]])) for k in ("tree", "near", "m2l_apply", "far")},
-            "sample": f"full cfg2 evaluate (N={N_POINTS}, warm, operators prebuilt), {n} step(s) after "
-                      f"{max(1, warmup)} warm-up; OMP/OpenBLAS threads = {threads}"}
+            "phases_s": {k: float(np.mean([x[k] for x in runs])) for k in ("tree", "near", "m2l_apply", "far")},
+            "cpu": ci, "binary": os.path.basename(binary),
+            "sample": f"full cfg2 evaluate (N={N_POINTS}), {n} timed step(s) after {wu} warm-up evaluate(s) in "
+                      f"the same process (the first builds the KIFMM operators); OMP/OpenBLAS threads = {threads} "
+                      f"(physical cores of a {ci['model']}); {os.path.basename(binary)}"}
 
 
 def run_reference(args):
@@ -163,19 +211,19 @@ def run_reference(args):
             "warmup": max(1, args.warmup), "ms_per_step": 1e3 * cb["seconds_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD}, "impl": "reference",
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "phases_s": cb["phases_s"]}
     print(json.dumps(line))
 
 
 def roofline_entry(stats, steps):
-    """Roofline of the dominant kernel from the live per-stage events of the timed region.
+    """Roofline of the dominant kernel from the per-stage CUDA events of the profiled pass.
 
-    int8 M2L (default): m2l_i8_kernel, achieved = algorithmic int8 ops (2 nmod K^2 per V
-    application, K = 888, no padding) / its device time, against the measured kind::i8
-    peak. The FP64-equivalent rate (2 K^2 per application / the same time) is reported
-    beside it. DMMA M2L (PKGPU_M2L=dmma): the FP64 gather-GEMM against the DMMA peak."""
+    int8 M2L (default): achieved = algorithmic int8 ops (2 nmod K^2 per V application,
+    K = 888, no padding) / the kernels' device time, against the measured kind::i8 peak;
+    the FP64-equivalent rate (2 K^2 per application / the same time) is reported beside
+    it. DMMA M2L (PKGPU_M2L=dmma): the FP64 gather-GEMM against the DMMA peak."""
     i8 = stats.get("m2l_i8", {})
     m2l = stats.get("m2l", {})
     if i8.get("seconds", 0) > 0:
@@ -197,6 +245,24 @@ def roofline_entry(stats, steps):
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
             "traffic": None, "flops_per_launch": fl, "ms_per_launch": 1e3 * s, "peak_source": FP64_PEAK_SOURCE,
             "flop_convention": "2 K^2 per V-list application, K = 888 (SURVEY §8d)"}
+
+
+def p2p_roofline(stats, steps):
+    """The P2P half of BASELINE's metric: leaf_kernel (U-list P2P + L2T + W + the fused
+    periodic far field, FP64 vector pipe) against the measured DFMA peak."""
+    lf = stats.get("leaf", {})
+    if not lf.get("seconds"):
+        return None
+    n = max(1, lf.get("launches", 1))
+    s, fl = lf["seconds"] / n, lf["flops"] / n
+    achieved = fl / s / 1e12
+    return {"kernel": "leaf_kernel<Stokes> (P2P over U lists + L2T + W + periodic far field, fused)",
+            "bound": "fp64 vector", "achieved": achieved, "peak": FP64_VEC_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_VEC_PEAK_TFLOPS, "traffic": LEAF_NCU_TRAFFIC,
+            "flops_per_launch": fl, "ms_per_launch": 1e3 * s, "pairs_per_launch": lf["units"] / n,
+            "peak_source": FP64_VEC_PEAK_SOURCE,
+            "flop_convention": "28 FLOP per Stokeslet pair (SURVEY §8d: 3 sub, r^2 5, rsqrt 1, r^-2 1, r.f 5, "
+                               "x r^-2 1, 3 x (FMA + FMA) 12)"}
 
 
 def run_ours(args):
@@ -236,9 +302,8 @@ def run_ours(args):
     # warm-up (operators built, workspaces sized)
     for _ in range(max(3, args.warmup)):
         pk.evaluate(req, context=ctx, out=d_out, comm=comm)
-    # ---- device-resident timed region (profiling on: live per-stage CUDA events) ----
-    ctx.set_profiling(True)
-    ctx.reset_stats()
+    # ---- device-resident timed region (`value`): profiling off ----
+    ctx.set_profiling(False)
     l0 = ctx.launches
     clocks = ClockSampler(local)
     clocks.start()
@@ -252,14 +317,28 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = (ctx.launches - l0) / args.steps
-    stats = ctx.stage_stats()
-    ctx.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(ms_t.item())
+
+    # ---- profiled pass (not the timed region): per-stage CUDA events on the work stream
+    # and algorithmic work counts, for the stage table and the rooflines ----
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    barrier()
+    pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        pe[i][0].record(stream)
+        pk.evaluate(req, context=ctx, out=d_out, comm=comm)
+        pe[i][1].record(stream)
+    barrier()
+    stats = ctx.stage_stats()
+    ctx.set_profiling(False)
+    prof_ms = float(np.mean([a.elapsed_time(b) for a, b in pe]))
 
     # ---- e2e: public API with pinned host buffers (H2D + D2H inside each step) ----
     h_pts = torch.from_numpy(pts.reshape(-1).copy()).pin_memory()
@@ -295,6 +374,10 @@ def run_ours(args):
                          "launches_per_step": v["launches"] / args.steps}
                      for k, v in stats.items() if k != "u_pairs"}
         roofline = roofline_entry(stats, args.steps)
+        roofline["p2p"] = p2p_roofline(stats, args.steps)
+        roofline["measured_in"] = (f"profiled pass of {args.steps} steps right after the timed region (per-stage "
+                                   f"CUDA events on the work stream; {prof_ms:.3f} ms/step with profiling on vs "
+                                   f"{ms:.3f} unprofiled)")
         line = {
             "metric": METRIC, "value": N_POINTS / (ms_max * 1e-3), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
@@ -313,15 +396,28 @@ def run_ours(args):
             "gpu_launches": int(round(launches)),
             "roofline": roofline,
             "stages": stage_tab,
+            "stages_note": "profiled pass (not the timed region)",
             "clocks": clk,
         }
         if ws == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(steps=2, warmup=1, budget_s=30.0)
             if cb is not None:
-                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")}
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without torchrun: relaunch as N ranks (one process per GPU,
+    torch.distributed.run, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -332,6 +428,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -434,6 +434,7 @@ class Context:
         _check(lib().pkgpu_context_create(device, ctypes.byref(h), err, 1024), err)
         self._h = h
         self.device = device
+        self._explicit_stream = False
 
     def close(self):
         if self._h and self._h.value:
@@ -447,7 +448,11 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: int):
+        """Run this context's work on `stream_ptr` (a cudaStream_t; 0 = the context's own
+        stream). Without an explicit stream, device-resident evaluates run on torch's
+        current stream of the inputs' device (see evaluate)."""
         lib().pkgpu_context_set_stream(self._h, ctypes.c_void_p(stream_ptr))
+        self._explicit_stream = True
 
     @property
     def stream(self) -> int:
@@ -539,17 +544,33 @@ def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None, 
     r.force = 1 if request.force else 0
     r.device_pointers = 1 if dev else 0
     if dev:
+        import torch
         src, q, trg = request.sources, request.strengths, request.targets
-        for t in (src, q, trg):
-            if not (t.is_contiguous() and str(t.dtype) == "torch.float64"):
-                raise ValueError("device inputs must be contiguous float64 CUDA tensors")
+        for name, t in (("sources", src), ("strengths", q), ("targets", trg)):
+            if not _is_torch_cuda(t) or t.device.index != ctx.device:
+                raise ValueError(f"{name}: device inputs must all be CUDA tensors on the context's device "
+                                 f"cuda:{ctx.device}")
+            if not (t.is_contiguous() and t.dtype == torch.float64):
+                raise ValueError(f"{name}: device inputs must be contiguous float64 CUDA tensors")
+        if src.numel() % 3 or trg.numel() % 3:
+            raise ValueError("sources / targets: xyz triples expected (numel divisible by 3)")
         ns, nq, nt = src.numel() // 3, q.numel(), trg.numel() // 3
         r.sources, r.strengths, r.targets = src.data_ptr(), q.data_ptr(), trg.data_ptr()
         if out is None:
-            import torch
             out = torch.empty(k.kt * nt, dtype=torch.float64, device=src.device)
+        elif not (_is_torch_cuda(out) and out.device.index == ctx.device and out.dtype == torch.float64
+                  and out.is_contiguous() and out.numel() == k.kt * nt):
+            raise ValueError(f"out: a contiguous float64 CUDA tensor on cuda:{ctx.device} with {k.kt * nt} "
+                             "elements is required")
+        # stream contract: without an explicit context stream the evaluate runs on torch's
+        # current stream, ordered after the kernels / copies that produced the inputs
+        if not ctx._explicit_stream:
+            lib().pkgpu_context_set_stream(ctx._h, ctypes.c_void_p(torch.cuda.current_stream(src.device).cuda_stream))
         optr = out.data_ptr()
     else:
+        for name, t in (("strengths", request.strengths), ("targets", request.targets)):
+            if _is_torch_cuda(t):
+                raise ValueError(f"{name}: mixed host and device inputs")
         src = np.ascontiguousarray(request.sources, dtype=np.float64).reshape(-1, 3)
         q = np.ascontiguousarray(request.strengths, dtype=np.float64).reshape(-1)
         trg = np.ascontiguousarray(request.targets, dtype=np.float64).reshape(-1, 3)
@@ -557,6 +578,9 @@ def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None, 
         r.sources, r.strengths, r.targets = _ptr(src), _ptr(q), _ptr(trg)
         if out is None:
             out = np.zeros(k.kt * nt)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous
+                  and out.size == k.kt * nt):
+            raise ValueError(f"out: a C-contiguous float64 numpy array with {k.kt * nt} elements is required")
         optr = out.ctypes.data
     r.n_sources, r.n_strengths, r.n_targets = ns, nq, nt
     tm, cp, err = _Timings(), _Compat(), _errbuf()

@@ -143,16 +143,18 @@ const JVal &at(const JVal &o, const std::string &k) {
 
 uint64_t crc64_xz(const void *data, size_t len) {
     // CRC-64/XZ: ECMA-182 polynomial, reflected (src/periodize.cpp:40-55)
-    static uint64_t table[256];
-    static bool init = false;
-    if (!init) {
-        for (uint64_t i = 0; i < 256; i++) {
-            uint64_t c = i;
-            for (int k = 0; k < 8; k++) c = (c & 1) ? (c >> 1) ^ 0xC96C5795D7870F42ull : c >> 1;
-            table[i] = c;
+    struct Table {
+        uint64_t t[256];
+        Table() {
+            for (uint64_t i = 0; i < 256; i++) {
+                uint64_t c = i;
+                for (int k = 0; k < 8; k++) c = (c & 1) ? (c >> 1) ^ 0xC96C5795D7870F42ull : c >> 1;
+                t[i] = c;
+            }
         }
-        init = true;
-    }
+    };
+    static const Table tab; // thread-safe one-time initialisation
+    const uint64_t *table = tab.t;
     uint64_t crc = ~0ull;
     const auto *p = static_cast<const unsigned char *>(data);
     for (size_t i = 0; i < len; i++) crc = table[(crc ^ p[i]) & 0xff] ^ (crc >> 8);
@@ -238,27 +240,27 @@ pkgpu_operator *load_pkm2l(const std::string &path) {
 } // namespace
 
 pkgpu_operator::~pkgpu_operator() {
-    if (d_matrix) {
-        int cur = 0;
-        cudaGetDevice(&cur);
-        cudaSetDevice(d_device);
-        cudaFree(d_matrix);
-        cudaSetDevice(cur);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : d_matrix) {
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second);
     }
+    cudaSetDevice(cur);
 }
 
+// one device copy per device, uploaded on first use and kept until the operator is
+// destroyed (contexts on other devices never free a copy another one may be using)
 const double *pkgpu_operator::device_matrix(int device, cudaStream_t st) const {
     std::lock_guard<std::mutex> lock(mtx);
-    if (d_matrix && d_device == device) return d_matrix;
-    if (d_matrix) {
-        cudaFree(d_matrix);
-        d_matrix = nullptr;
-    }
-    PK_CUDA(cudaMalloc(&d_matrix, matrix.size() * sizeof(double)));
-    PK_CUDA(cudaMemcpyAsync(d_matrix, matrix.data(), matrix.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    auto it = d_matrix.find(device);
+    if (it != d_matrix.end()) return it->second;
+    double *d = nullptr;
+    PK_CUDA(cudaMalloc(&d, matrix.size() * sizeof(double)));
+    PK_CUDA(cudaMemcpyAsync(d, matrix.data(), matrix.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     PK_CUDA(cudaStreamSynchronize(st));
-    d_device = device;
-    return d_matrix;
+    d_matrix.emplace(device, d);
+    return d;
 }
 
 extern "C" {

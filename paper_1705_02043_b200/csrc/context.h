@@ -23,10 +23,9 @@ struct pkgpu_operator {
     int real_shells = 2, wave_cutoff = 64;
     long long n_images = 1000000;
     std::string created;
-    // device copy, uploaded lazily per device
+    // device copies, uploaded lazily, one per device
     mutable std::mutex mtx;
-    mutable double *d_matrix = nullptr;
-    mutable int d_device = -1;
+    mutable std::map<int, double *> d_matrix;
     ~pkgpu_operator();
     const double *device_matrix(int device, cudaStream_t st) const;
 };

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include "context.h"
+#include "tuning.h"
 #include "gemm.h"
 #include "pairs.h"
 
@@ -327,8 +328,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
     // int8 runs: consecutive small levels (<= PKGPU_I8_SMALL boxes, default 1024: nearly all
     // 316 offsets active, few columns, bound by streaming the operator residues) share one
     // launch and are packed into as few 128-column tiles as possible; a big level runs alone
-    static const int64_t small_max =
-        std::getenv("PKGPU_I8_SMALL") ? std::atoll(std::getenv("PKGPU_I8_SMALL")) : 1024;
+    const int64_t small_max = tuning().i8_small_boxes;
     const I8Settings &is = ctx.i8;
     auto i8_level = [&](int lv) {
         return is.enabled && lv >= 1 && lv <= T.depth && T.level_off[lv + 1] - T.level_off[lv] >= is.min_boxes;
@@ -345,11 +345,10 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             padded128 += (count[l * 8 + o] + 127) / 128 * 128;
         }
         grouped[l] = padded * 189 <= (nl + BN - 1) / BN * BN * 316 ? 1 : 0;
-        // 128-column M2L tiles (one 17-warp CTA per SM, half the operator traffic) are
-        // opt-in (PKGPU_GEMM_WIDE=1): measured slower than two 64-column CTAs per SM on
-        // cfg2/3/4 (49.3 vs 46.3 ms M2L at cfg2)
-        static const bool wide_ok = std::getenv("PKGPU_GEMM_WIDE") != nullptr;
-        L.wide[l] = wide_ok && grouped[l] && padded128 * 100 <= padded * 103 ? 1 : 0;
+        // 128-column DMMA M2L tiles (one 17-warp CTA per SM) measured slower than two
+        // 64-column CTAs per SM on cfg2/3/4 (49.3 vs 46.3 ms M2L at cfg2): not used
+        (void)padded128;
+        L.wide[l] = 0;
         const int padm = L.wide[l] ? 128 : BN;
         L.i8[l] = i8_level(l) ? 1 : 0;
         const bool in_run = L.i8[l] && run_first >= 0; // continues the current int8 run
@@ -379,9 +378,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             if (!cont) {
                 L.i8_last[run_first] = l;
                 L.i8_big[run_first] = run_first == l && !small_level(l) ? 1 : 0;
-                static const int64_t small_pad =
-                    std::getenv("PKGPU_I8_SMALLPAD") ? std::atoll(std::getenv("PKGPU_I8_SMALLPAD")) : kI8Tile;
-                const int64_t q = L.i8_big[run_first] ? 2 * kI8Tile : small_pad;
+                const int64_t q = L.i8_big[run_first] ? 2 * kI8Tile : kI8Tile;
                 cm = L.colbase[run_first] + (cm - L.colbase[run_first] + q - 1) / q * q;
                 run_first = -1;
             }
@@ -789,6 +786,14 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         prof.end(pm);
         PK_CUDA(cudaEventRecord(ctx.ev[1], st));
         KifmmOps &ops = ctx.ops.get(kernel, req.p, st, &ctx.launches);
+        // residue range of the int8 M2L for this K (m2l_i8.h): more moduli, or DMMA, when
+        // |S| <= 316 K 2^(beta_a + beta_b) could reach M / 2; restored when the call ends
+        struct I8Restore {
+            pkgpu_context &c;
+            I8Settings saved;
+            ~I8Restore() { c.i8 = saved; }
+        } i8_restore{ctx, ctx.i8};
+        ctx.i8 = i8_settings_for(ctx.i8, kNumM2L, ops.K);
         const int Kp = ops.Kp;
         const int64_t nb = T.nboxes;
         PairGeom g{kernel, req.p, ops.n, Kp, ops.d_tmpl};

@@ -26,6 +26,7 @@
 
 #include "gemm.h"
 #include "gemm_tma.cuh"
+#include "tuning.h"
 
 namespace pkgpu {
 
@@ -33,8 +34,6 @@ namespace {
 
 constexpr int BN = kGemmBN;
 constexpr int BK = 16;
-constexpr int PAD = BK + 4;
-constexpr int STAGES = 3;
 constexpr int MAX_SLOTS = 320;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
@@ -120,89 +119,6 @@ __device__ __forceinline__ void unit_range(const KParams &kp, int nact, int spli
     const int64_t niter = (int64_t)nact * (kp.a.Kp / BK);
     it0 = (int)(niter * split / kp.nsplit);
     it1 = (int)(niter * (split + 1) / kp.nsplit);
-}
-
-// ---------------------------------------------------------------------------
-// cp.async mainloop: one CTA per unit; warps (BM/32) x 2, warp tile 32 x 32.
-template <int BM>
-__global__ void __launch_bounds__(BM / 32 * 2 * 32) gather_gemm_kernel(KParams kp) {
-    constexpr int WARPS_M = BM / 32;
-    constexpr int NT = WARPS_M * 2 * 32;
-    const GemmArgs &a = kp.a;
-    extern __shared__ __align__(16) double smem[];
-    double *As = smem;                     // [STAGES][BM][PAD]
-    double *Bs = smem + STAGES * BM * PAD; // [STAGES][BN][PAD]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rt = blockIdx.x, ct = blockIdx.y, split = blockIdx.z;
-    const int row0 = rt * BM, col0 = ct * BN;
-    const int *slots = kp.tile_slots ? kp.tile_slots + ct * MAX_SLOTS : nullptr;
-    int it0, it1;
-    unit_range(kp, kp.tile_nact ? kp.tile_nact[ct] : 1, split, it0, it1);
-    const int nk = a.Kp / BK;
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    auto load_stage = [&](int it, int stage) {
-        const int slot = slots ? slots[it / nk] : it / nk;
-        const int k0 = (it % nk) * BK;
-        const double *Am = a.A + (int64_t)slot_matrix(a, slot, ct) * a.Kp * a.Kp;
-        double *as = As + stage * BM * PAD;
-        double *bs = Bs + stage * BN * PAD;
-        for (int ch = tid; ch < BM * (BK / 2); ch += NT) {
-            const int r = ch / (BK / 2), cc = ch % (BK / 2);
-            const bool in = row0 + r < a.Kp;
-            cp_async16(as + r * PAD + cc * 2, in ? Am + (int64_t)(row0 + r) * a.Kp + k0 + cc * 2 : Am, in ? 16 : 0);
-        }
-        for (int ch = tid; ch < BN * (BK / 2); ch += NT) {
-            const int j = ch / (BK / 2), cc = ch % (BK / 2);
-            const int sb = col_src(a, slot, col0 + j);
-            const double *g = sb >= 0 ? a.X + (int64_t)sb * a.Kp + k0 + cc * 2 : a.X;
-            cp_async16(bs + j * PAD + cc * 2, g, sb >= 0 ? 16 : 0);
-        }
-    };
-
-    const int n = it1 - it0;
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; s++) {
-        if (s < n) load_stage(it0 + s, s);
-        cp_async_commit();
-    }
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-    for (int i = 0; i < n; i++) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        const int nxt = i + STAGES - 1;
-        if (nxt < n) load_stage(it0 + nxt, nxt % STAGES);
-        cp_async_commit();
-        const double *as = As + (i % STAGES) * BM * PAD + (wm * 32 + (lane >> 2)) * PAD + (lane & 3);
-        const double *bs = Bs + (i % STAGES) * BN * PAD + (wn * 32 + (lane >> 2)) * PAD + (lane & 3);
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double af[4], bf[4];
-#pragma unroll
-            for (int m = 0; m < 4; m++) af[m] = as[m * 8 * PAD + kk];
-#pragma unroll
-            for (int q = 0; q < 4; q++) bf[q] = bs[q * 8 * PAD + kk];
-#pragma unroll
-            for (int m = 0; m < 4; m++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) dmma(acc[m][q], af[m], bf[q]);
-        }
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int m = 0; m < 4; m++) {
-        const int r = row0 + wm * 32 + m * 8 + (lane >> 2);
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-#pragma unroll
-            for (int h = 0; h < 2; h++)
-                store_out(kp, split, r, col0 + wn * 32 + q * 8 + 2 * (lane & 3) + h, acc[m][q][h]);
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -383,14 +299,21 @@ __global__ void gemv_kernel(const double *__restrict__ A, int rows, int cols, in
     }
 }
 
-template <int BM> size_t smem_bytes() { return (size_t)STAGES * (BM + BN) * PAD * sizeof(double); }
-
 // (BNT, stages): 64 -> 4 x 26 KB, two CTAs per SM; 128 -> 6 x 36 KB, one CTA per SM
 template <int BNT> constexpr int tma_stages() { return BNT == 64 ? 4 : 6; }
 template <int BNT> size_t tma_smem_bytes() { return (size_t)tma_stages<BNT>() * tma_stage_bytes<128, BNT>() + 1024; }
 
+// dynamic shared memory opt-in, once per (kernel, device): the attribute is per device
 template <class K> void set_smem(K kernel, size_t bytes) {
+    static std::mutex mtx;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mtx);
+    size_t &d = done[{reinterpret_cast<const void *>(kernel), dev}];
+    if (d >= bytes) return;
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    d = bytes;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -406,7 +329,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // tensor map over the stacked operator array, cached per (pointer, nmat, Kp, BM)
-const CUtensorMap &operator_map(const double *A, int nmat, int Kp, int BM) {
+CUtensorMap operator_map(const double *A, int nmat, int Kp, int BM) {
     static std::map<std::tuple<const double *, int, int, int>, CUtensorMap> cache;
     static std::mutex mtx; // contexts may run on several host threads
     std::lock_guard<std::mutex> lock(mtx);
@@ -425,59 +348,32 @@ const CUtensorMap &operator_map(const double *A, int nmat, int Kp, int BM) {
     return cache.emplace(key, m).first->second;
 }
 
-// mainloop selection: PKGPU_GEMM = tma (default) | cpasync
-bool use_tma() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = std::getenv("PKGPU_GEMM");
-        v = (e && std::strcmp(e, "cpasync") == 0) ? 0 : 1;
-    }
-    return v == 1;
-}
-
 } // namespace
 
 int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) {
     if (a.ncols == 0 || a.nslots == 0) return 0;
     if (a.Kp % 64 != 0 || a.ncols % BN != 0 || a.nslots > MAX_SLOTS)
         throw RuntimeError("gather_gemm: bad shape");
-    const bool tma_path = use_tma();
     // 128-row tiles for every K: the TMA zero-fills operator rows past Kp (3D tensor map,
-    // out-of-bounds) and the epilogue drops them. BM = 64 tiles only stream half the
-    // operator per stage and run the DMMA pipe at ~60% of the 128-row tiles' rate.
-    static const int bm_env = [] {
-        const char *e = std::getenv("PKGPU_GEMM_BM"); // 64: legacy half-height tiles (comparison runs)
-        return (e && std::strcmp(e, "64") == 0) ? 64 : 128;
-    }();
-    const int BMsel = tma_path ? 128 : bm_env;
+    // out-of-bounds) and the epilogue drops them
+    constexpr int BMsel = 128;
     // 128-column tiles when the caller's column layout allows (big octant-grouped levels)
-    const int bnt = (tma_path && a.bn == 128 && a.ncols % 128 == 0) ? 128 : BN;
+    const int bnt = (a.bn == 128 && a.ncols % 128 == 0) ? 128 : BN;
     const int rowtiles = (a.Kp + BMsel - 1) / BMsel, coltiles = a.ncols / bnt;
     const int64_t base = (int64_t)rowtiles * coltiles;
     const int resident = num_sms * (bnt == 128 ? 1 : 2);
-    // enough units for ~8 per resident CTA (dynamic scheduling evens them out), each
-    // still at least PKGPU_GEMM_MINIT (default 16) iterations long (shorter units measured
+    // enough units for ~32 per resident CTA (dynamic scheduling evens them out), each
+    // still at least gemm_min_iters (default 16) iterations long (shorter units measured
     // slower at cfg2: more partials to reduce, no gain on the small levels)
     const int64_t iters = (int64_t)a.nslots * (a.Kp / BK);
-    static const int64_t units_per_cta = [] {
-        const char *e = std::getenv("PKGPU_GEMM_UNITS"); // tuning knob: work units per resident CTA
-        return (int64_t)(e ? std::max(1, std::atoi(e)) : 32);
-    }();
-    const int64_t want = tma_path ? units_per_cta * resident : 4 * (int64_t)resident;
+    const Tuning &tu = tuning();
+    const int64_t want = tu.gemm_units_per_cta * resident;
     int nsplit = 1;
-    static const int64_t min_iters = [] {
-        const char *e = std::getenv("PKGPU_GEMM_MINIT");
-        return (int64_t)(e ? std::max(1, std::atoi(e)) : 16);
-    }();
     // pseudo-inverse factors (one slot) on grids smaller than the resident CTAs (the top
     // levels: 1-512 columns) are latency-bound -- shorter units spread them over the machine
     // (measured at cfg2: pinv 1.06 -> 0.91 ms per direction with 4; the 8-slot M2M / L2L
     // lose with shorter units: more partials to reduce)
-    static const int64_t min_iters_small = [] {
-        const char *e = std::getenv("PKGPU_GEMM_MINIT_SMALL");
-        return (int64_t)(e ? std::max(1, std::atoi(e)) : 4);
-    }();
-    const int64_t mi = (base < resident && a.nslots == 1) ? min_iters_small : min_iters;
+    const int64_t mi = (base < resident && a.nslots == 1) ? tu.gemm_min_iters_small : tu.gemm_min_iters;
     if (base < want)
         nsplit = (int)std::min<int64_t>({(want + base - 1) / base, std::max<int64_t>(1, iters / mi), 64});
     nsplit = std::max(nsplit, 1);
@@ -497,48 +393,21 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
         kp.tile_nact = tnact;
         launches = 1;
     }
-    if (tma_path) {
-        kp.counter = ws.get<int>("gemm_counter", 1);
-        PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
-        TmaParams tp;
-        std::memset(&tp, 0, sizeof tp);
-        tp.kp = kp;
-        tp.tmA = operator_map(a.A, a.nmat > 0 ? a.nmat : 1, a.Kp, BMsel);
-        const unsigned grid = (unsigned)std::min<int64_t>(kp.total_units, resident);
-        // one-time residency check (PKGPU_GEMM_VERBOSE=1): CTAs per SM actually achievable
-        auto report = [](auto kernel, int threads, size_t bytes, const char *name) {
-            if (!std::getenv("PKGPU_GEMM_VERBOSE")) return;
-            int blocks = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, bytes);
-            cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, kernel);
-            std::fprintf(stderr, "[pkgpu] %s: %d CTA/SM, %d regs, %zu B dynamic smem\n", name, blocks, fa.numRegs,
-                         bytes);
-        };
-        if (bnt == 128) {
-            constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<128>(), 128, 16>;
-            static bool cfg = false;
-            if (!cfg) set_smem(k, tma_smem_bytes<128>()), report(k, 17 * 32, tma_smem_bytes<128>(), "tma<128,128>"),
-                cfg = true;
-            k<<<grid, 17 * 32, tma_smem_bytes<128>(), st>>>(tp);
-        } else {
-            constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<64>(), 64, 8>;
-            static bool cfg = false;
-            if (!cfg) set_smem(k, tma_smem_bytes<64>()), report(k, 9 * 32, tma_smem_bytes<64>(), "tma<128,64>"),
-                cfg = true;
-            k<<<grid, 9 * 32, tma_smem_bytes<64>(), st>>>(tp);
-        }
+    kp.counter = ws.get<int>("gemm_counter", 1);
+    PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
+    TmaParams tp;
+    std::memset(&tp, 0, sizeof tp);
+    tp.kp = kp;
+    tp.tmA = operator_map(a.A, a.nmat > 0 ? a.nmat : 1, a.Kp, BMsel);
+    const unsigned grid = (unsigned)std::min<int64_t>(kp.total_units, resident);
+    if (bnt == 128) {
+        constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<128>(), 128, 16>;
+        set_smem(k, tma_smem_bytes<128>());
+        k<<<grid, 17 * 32, tma_smem_bytes<128>(), st>>>(tp);
     } else {
-        dim3 grid(rowtiles, coltiles, nsplit);
-        if (BMsel == 128) {
-            static bool cfg = false;
-            if (!cfg) set_smem(gather_gemm_kernel<128>, smem_bytes<128>()), cfg = true;
-            gather_gemm_kernel<128><<<grid, 256, smem_bytes<128>(), st>>>(kp);
-        } else {
-            static bool cfg = false;
-            if (!cfg) set_smem(gather_gemm_kernel<64>, smem_bytes<64>()), cfg = true;
-            gather_gemm_kernel<64><<<grid, 128, smem_bytes<64>(), st>>>(kp);
-        }
+        constexpr auto k = gather_gemm_tma_kernel<128, tma_stages<64>(), 64, 8>;
+        set_smem(k, tma_smem_bytes<64>());
+        k<<<grid, 9 * 32, tma_smem_bytes<64>(), st>>>(tp);
     }
     PK_CUDA(cudaGetLastError());
     launches++;

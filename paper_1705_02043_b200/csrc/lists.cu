@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include "tree.h"
+#include "tuning.h"
 
 namespace pkgpu {
 
@@ -504,8 +505,7 @@ void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, i
     }
     // warp per box where boxes are few (latency-bound single threads); thread per box on big
     // trees, which already fill the GPU (PKGPU_LIST_WARP_MAX boxes, default 50k)
-    static const int64_t warp_max =
-        std::getenv("PKGPU_LIST_WARP_MAX") ? std::atoll(std::getenv("PKGPU_LIST_WARP_MAX")) : 50000;
+    const int64_t warp_max = tuning().list_warp_max;
     const bool warp_lists = nb <= warp_max;
     if (warp_lists)
         eval_warp_kernel<false><<<blocks_for(32 * (size_t)nb, 128), 128, 0, st>>>(

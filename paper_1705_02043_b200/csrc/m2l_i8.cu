@@ -19,15 +19,19 @@
 // Work unit = (modulus, operator row tile, 128-column tile, chunk of the tile's active
 // slots); chunks keep |int32 accumulator| <= slots * Ki * 128^2 < 2^31.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include <cudaTypedefs.h>
 
 #include "gemm_tma.cuh"
 #include "m2l_i8.h"
+#include "tuning.h"
 
 namespace pkgpu {
 
@@ -57,7 +61,6 @@ __constant__ float c_finv[kI8MaxModuli];            // 1 / m_t
 
 struct Params {
     CUtensorMap tmB; // operators: (Ki, Ki, nmod * nmat) int8, box (128, Nt, 1), 128B swizzle
-    CUtensorMap tmX; // box residues (Ki, nmod * rows_per_mod) int8, box (128, 1), 128B swizzle (gather4)
     const int8_t *X; // box residues [nmod][rows_per_mod][Ki]
     const int *src;
     int64_t ld_src, box0;
@@ -70,12 +73,8 @@ struct Params {
     const int *tile_partial;  // dual kernel: [pair tile] 1 if some active slot misses a half
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
-    int debug; // PKGPU_I8_DEBUG timing experiments (results invalid): 1 no gather, 2 no operator
-               // loads, 4 no epilogue atomics, 8 no MMA proxy fence, 16 one operator, 32 plain
-               // per-warp "full" arrivals instead of cp.async-tracked ones
     int nst, stage_bytes; // single-CTA kernel: stage ring depth and stride
     int epi_transpose;    // epilogue atomics through a shared-memory transpose (coalesced)
-    int prefetch;         // stages of L2 prefetch ahead for the operator tiles (0: off)
     int *R; // [nmod][ncols][Ki]
 };
 
@@ -169,8 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     constexpr int NPT = NPROD * 32;
     if (tid == 0) {
         for (int s = 0; s < NS; s++) {
-            // cp.async arrivals + the TMA expect_tx arrival (debug 32: one plain arrival per warp)
-            tma::mbar_init(&full[s], (p.debug & 32) ? NPROD + 1 : NPT + 1);
+            tma::mbar_init(&full[s], NPT + 1); // cp.async arrivals + the TMA expect_tx arrival
             tma::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
@@ -216,42 +214,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                     tma::mbar_wait(&empty[st], ((gi / NS) & 1) ^ 1);
                     unsigned char *as = smem + st * SB;
                     if (tid == 0) {
-                        if (p.debug & 2) { // timing experiment: no operator loads
-                            tma::mbar_arrive(&full[st]);
-                        } else {
-                            const int mat = (p.debug & 16) ? 0 : slot; // 16: one L2-resident operator
-                            tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                            tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + mat,
-                                             &full[st]);
-                            // L2 prefetch of the operator tile p.prefetch stages ahead (same unit):
-                            // takes the DRAM latency of the operator stream off the smem ring
-                            if (p.prefetch > 0) {
-                                const int ia = (si - x.s0) * p.KC + kc + p.prefetch;
-                                const int sa = x.s0 + ia / p.KC, ka = ia % p.KC;
-                                if (sa < x.s1) {
-                                    const int ma = (p.debug & 16) ? 0 : slots[sa];
-                                    asm volatile(
-                                        "cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
-                                            reinterpret_cast<uint64_t>(&p.tmB)),
-                                        "r"(ka * BKI), "r"(x.rt * p.Nt), "r"(x.t * p.nmat + ma)
-                                        : "memory");
-                                }
-                            }
-                        }
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot, &full[st]);
                     }
-                    if (!(p.debug & 1)) { // (bit 0: timing experiment without the gather)
 #pragma unroll
-                        for (int i = 0; i < 16; i++) {
-                            const int j = j0 + 8 * i;
-                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
-                        }
+                    for (int i = 0; i < 16; i++) {
+                        const int j = j0 + 8 * i;
+                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                     }
-                    if (p.debug & 32) { // timing experiment: plain per-warp arrival (no cp.async tracking)
-                        __syncwarp();
-                        if (lane == 0) tma::mbar_arrive(&full[st]);
-                    } else {
-                        tma::cp_async_mbar_arrive(&full[st]);
-                    }
+                    tma::cp_async_mbar_arrive(&full[st]);
                 }
             }
         } else if (warp == MMA_WARP) {
@@ -267,7 +238,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
             for (int i = 0; i < n; i++) {
                 tma::mbar_wait(&full[st], ph);
                 // the gathered rows were written by cp.async through the generic proxy
-                if (!(p.debug & 8)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 tc_fence_after();
                 const uint32_t a0 = sbase + st * SB;
                 const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
@@ -301,7 +272,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                     for (int j = 0; j < 32; j++) {
                         const int a = (int)v[j];
                         const int r = a - __float2int_rn((float)a * inv) * m;
-                        if (r && j0 + j < nr && !(p.debug & 4)) atomicAdd(Rb + j, r);
+                        if (r && j0 + j < nr) atomicAdd(Rb + j, r);
                     }
                     continue;
                 }
@@ -316,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
 #pragma unroll 8
                 for (int b = 0; b < 32; b++) {
                     const int r = tile[b * EPI_PITCH + lane]; // box col0 + b, row r0 + j0 + lane
-                    if (ok && !(p.debug & 4)) {
+                    if (ok) {
                         if (p.direct)
                             Rt[(int64_t)b * p.Ki + j0 + lane] = r;
                         else if (r)
@@ -340,23 +311,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
     }
 }
 
-// ---------------------------------------------------------------------------
-// CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256), all loads by TMA:
-// the pair shares one 256-column tile (CTA r owns boxes [256 p + 128 r, +128)) and one
-// operator row tile. Per stage each CTA stages its 128 gathered box rows (32 TMA gather4
-// loads of 4 rows, hardware 128B swizzle) and HALF of the operator tile (Nt / 2 rows, one
-// TMA 3D load): 16 KB + Nt/2 x 128 B per CTA, i.e. 2/3 of the single-CTA bytes per MAC,
-// and up to eight stages deep (runtime ring). Every load signals the LEADER's "full" barrier (.cta_group::2
-// TMA, complete_tx across the pair), so no thread relays arrivals and no generic-proxy
-// writes need fencing.
-//   warp 0      producer (both CTAs): lane i issues the gather4 of rows 4i..4i+3, lane 0
-//               the operator half; the leader's lane 0 posts expect_tx for both CTAs
-//   warp 1      MMA issuer (leader, whole warp, elected lane): tcgen05.mma.cta_group::2
-//               M256 x Nt x K32 kind::i8, commits "empty" / "tfull" to both CTAs
-//   warps 2-5   epilogue (both CTAs, own 128 TMEM lanes = own boxes) as in m2l_i8_kernel;
-//               releases the accumulator on the leader's "tempty" (4 local + 4 remote)
-constexpr int PAIR_THREADS = 6 * 32;
-
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -378,342 +332,6 @@ __device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
 __device__ __forceinline__ void remote_arrive_cta(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
-// TMA gather4 of four 128-byte rows into consecutive (swizzled) rows at dst, completing on
-// the pair leader's barrier `bar` (a shared::cluster address)
-__device__ __forceinline__ void gather4_pair(uint32_t dst, const CUtensorMap *map, int c0, int r0, int r1, int r2,
-                                             int r3, uint32_t bar) {
-    asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::"
-                 "bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
-                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-                 : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
-    m2l_i8_pair_kernel(const __grid_constant__ Params p) {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    const int NS = p.nst, SB = p.stage_bytes; // runtime ring: 16 KB gathered rows + half operator tile
-    int *s_epi = reinterpret_cast<int *>(smem + NS * SB); // [4 warps][32][33]
-    __shared__ __align__(8) uint64_t full[NST_MAX], empty[NST_MAX], tfull[2], tempty[2];
-    __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
-    const uint32_t rank = cluster_rank();
-    const bool leader = rank == 0;
-    const int half = p.Nt / 2;
-    if (tid == 0) {
-        for (int s = 0; s < NS; s++) {
-            tma::mbar_init(&full[s], 1);  // leader: its expect_tx arrival (+ 60 KB of transactions)
-            tma::mbar_init(&empty[s], 1); // the leader's multicast MMA commit
-        }
-        for (int b = 0; b < 2; b++) {
-            tma::mbar_init(&tfull[b], 1);
-            tma::mbar_init(&tempty[b], 8); // leader: 4 local + 4 remote epilogue warps
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         tma::smem_u32(&s_tmem))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem = s_tmem;
-
-    int g = 0, jb = 0;
-    const int npairs = p.coltiles / 2;
-    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
-        int v = u;
-        const int rt = v % p.rowtiles;
-        v /= p.rowtiles;
-        const int pr = v % npairs;
-        v /= npairs;
-        const int chunk = v % p.nchunk;
-        const int t = v / p.nchunk;
-        int s0, s1;
-        chunk_range(p, pr, chunk, s0, s1);
-        const int n = (s1 - s0) * p.KC;
-        if (n == 0) continue;
-        const int *slots = p.tile_slots + pr * MAX_SLOTS;
-        const int col0 = pr * 2 * TBM + (int)rank * TBM; // this CTA's 128 boxes
-        if (warp == 0) {
-            // ---------------- producer (both CTAs) ----------------
-            const uint32_t sbase = tma::smem_u32(smem);
-            int st = g % NS;
-            uint32_t ph = (g / NS) & 1;
-            const int rowbase = t * p.rows_per_mod;
-            for (int si = s0; si < s1; si++) {
-                const int slot = slots[si];
-                const int4 b4 = *reinterpret_cast<const int4 *>(p.src + (int64_t)slot * p.ld_src + col0 + 4 * lane);
-                const int r0 = rowbase + (b4.x >= 0 ? (int)(b4.x - p.box0) : p.zero_row);
-                const int r1 = rowbase + (b4.y >= 0 ? (int)(b4.y - p.box0) : p.zero_row);
-                const int r2 = rowbase + (b4.z >= 0 ? (int)(b4.z - p.box0) : p.zero_row);
-                const int r3 = rowbase + (b4.w >= 0 ? (int)(b4.w - p.box0) : p.zero_row);
-                for (int kc = 0; kc < p.KC; kc++) {
-                    tma::mbar_wait(&empty[st], ph ^ 1);
-                    const uint32_t as = sbase + st * SB;
-                    const uint32_t bar = map_to_rank(&full[st], 0);
-                    if (lane == 0) {
-                        if (leader)
-                            asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::
-                                             "r"(bar),
-                                         "r"(2 * (A_BYTES + half * BKI))
-                                         : "memory");
-                        asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
-                                     "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(as + A_BYTES),
-                                     "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
-                                     "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + slot), "r"(bar)
-                                     : "memory");
-                    }
-                    gather4_pair(as + lane * 4 * BKI, &p.tmX, kc * BKI, r0, r1, r2, r3, bar);
-                    if (++st == NS) st = 0, ph ^= 1;
-                }
-            }
-        } else if (warp == 1) {
-            if (leader) {
-                // ---------------- MMA issuer (leader; whole warp, elected lane) ----------------
-                const int buf = jb & 1;
-                tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t dt = tmem + buf * 256;
-                int st = g % NS;
-                uint32_t ph = (g / NS) & 1;
-                const uint32_t sbase = tma::smem_u32(smem);
-                for (int i = 0; i < n; i++) {
-                    tma::mbar_wait(&full[st], ph);
-                    tc_fence_after();
-                    const uint32_t a0 = sbase + st * SB;
-                    const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
-#pragma unroll
-                    for (int kk = 0; kk < BKI / 32; kk++)
-                        asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-                                     "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
-                                     "l"(ad + 2 * kk), "l"(bd + 2 * kk), "r"(p.idesc),
-                                     "r"((i > 0 || kk > 0) ? 1u : 0u));
-                    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
-                                 "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
-                                 "h"((uint16_t)3)
-                                 : "memory");
-                    if (++st == NS) st = 0, ph ^= 1;
-                }
-                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                             "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
-                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&tfull[buf])),
-                             "h"((uint16_t)3)
-                             : "memory");
-            }
-            __syncwarp();
-        } else {
-            // ---------------- epilogue (both CTAs: own 128 lanes = own boxes) ----------------
-            const int buf = jb & 1, q = warp & 3;
-            int *tile = s_epi + (warp - 2) * 32 * EPI_PITCH;
-            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
-            tc_fence_after();
-            const int m = c_mod[t];
-            const float inv = c_finv[t];
-            const int cw = col0 + q * 32;
-            const int r0 = rt * p.Nt;
-            const int nr = min(p.Nt, p.Ki - r0);
-            int *Rt = p.R + ((int64_t)t * p.ncols + cw) * p.Ki + r0;
-            for (int j0 = 0; j0 < p.Nt; j0 += 32) {
-                uint32_t vv[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, vv);
-#pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const int a = (int)vv[j];
-                    tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
-                }
-                __syncwarp();
-                const bool ok = j0 + lane < nr;
-#pragma unroll 8
-                for (int b = 0; b < 32; b++) {
-                    const int r = tile[b * EPI_PITCH + lane];
-                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
-                }
-                __syncwarp();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) remote_arrive(map_to_rank(&tempty[buf], 0));
-        }
-        g += n;
-        jb++;
-    }
-    tc_fence_before();
-    cluster_sync();
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Multicast pair (cluster of 2, cta_group::1 MMAs): each CTA computes its own 128 boxes with
-// its own TMEM, like m2l_i8_kernel, but the two CTAs walk the same (modulus, operator row
-// tile, slot) sequence and each TMA-loads HALF of the operator tile with .multicast::cluster
-// into both CTAs' shared memory -- the operator tile is read from L2 once per pair. A stage
-// is refilled only when both CTAs' MMAs are done with it: each MMA thread commits "empty"
-// to both CTAs (multicast commit, count 2). No cross-CTA software arrivals or fences.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-    m2l_i8_mc_kernel(const __grid_constant__ Params p) {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    int *s_epi = reinterpret_cast<int *>(smem + NST * STAGE_BYTES); // [4 warps][32][33]
-    __shared__ __align__(8) uint64_t full[NST], empty[NST], tfull[2], tempty[2];
-    __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
-    const uint32_t rank = cluster_rank();
-    constexpr int NPT = NPROD * 32;
-    const int half = p.Nt / 2;
-    if (tid == 0) {
-        for (int s = 0; s < NST; s++) {
-            tma::mbar_init(&full[s], NPT + 1); // local cp.async + local expect_tx (both halves' bytes)
-            tma::mbar_init(&empty[s], 2);      // both CTAs' MMA commits
-        }
-        for (int b = 0; b < 2; b++) {
-            tma::mbar_init(&tfull[b], 1);
-            tma::mbar_init(&tempty[b], 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         tma::smem_u32(&s_tmem))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem = s_tmem;
-
-    int g = 0, jb = 0;
-    const int npairs = p.coltiles / 2;
-    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
-        int v = u;
-        const int rt = v % p.rowtiles;
-        v /= p.rowtiles;
-        const int pr = v % npairs;
-        v /= npairs;
-        const int chunk = v % p.nchunk;
-        const int t = v / p.nchunk;
-        int s0, s1;
-        chunk_range(p, pr, chunk, s0, s1);
-        const int n = (s1 - s0) * p.KC;
-        if (n == 0) continue;
-        const int *slots = p.tile_slots + pr * MAX_SLOTS;
-        const int col0 = pr * 2 * TBM + (int)rank * TBM; // this CTA's 128 boxes
-        if (warp < NPROD) {
-            // ---------------- producers ----------------
-            const int c = lane & 7, j0 = tid >> 3;
-            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
-            for (int si = s0; si < s1; si++) {
-                const int slot = slots[si];
-                const int *srow = p.src + (int64_t)slot * p.ld_src + col0;
-                int64_t off[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    const int b = srow[j0 + 8 * i];
-                    off[i] = (int64_t)(b >= 0 ? (int)(b - p.box0) : p.zero_row) * p.Ki;
-                }
-                for (int kc = 0; kc < p.KC; kc++) {
-                    const int gi = g + (si - s0) * p.KC + kc, st = gi % NST;
-                    tma::mbar_wait(&empty[st], ((gi / NST) & 1) ^ 1);
-                    unsigned char *as = smem + st * STAGE_BYTES;
-                    if (tid == 0) {
-                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        asm volatile(
-                            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
-                            "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
-                                tma::smem_u32(as + A_BYTES + (int)rank * half * BKI)),
-                            "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI), "r"(rt * p.Nt + (int)rank * half),
-                            "r"(t * p.nmat + slot), "r"(tma::smem_u32(&full[st])), "h"((uint16_t)3)
-                            : "memory");
-                    }
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int j = j0 + 8 * i;
-                        tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
-                    }
-                    tma::cp_async_mbar_arrive(&full[st]);
-                }
-            }
-        } else if (warp == MMA_WARP) {
-            // ---------------- MMA issuer (each CTA; whole warp, elected lane issues) ----------------
-            const int buf = jb & 1;
-            tma::mbar_wait(&tempty[buf], ((jb >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t dt = tmem + buf * 256;
-            int st = g % NST;
-            uint32_t ph = (g / NST) & 1;
-            const uint32_t sbase = tma::smem_u32(smem);
-            for (int i = 0; i < n; i++) {
-                tma::mbar_wait(&full[st], ph);
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                tc_fence_after();
-                const uint32_t a0 = sbase + st * STAGE_BYTES;
-                const uint64_t ad = sw128_desc(a0), bd = sw128_desc(a0 + A_BYTES);
-#pragma unroll
-                for (int kk = 0; kk < BKI / 32; kk++)
-                    mma_i8_elect(dt, ad + 2 * kk, bd + 2 * kk, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
-                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
-                             "h"((uint16_t)3)
-                             : "memory");
-                if (++st == NST) st = 0, ph ^= 1;
-            }
-            commit_elect(&tfull[buf]);
-            __syncwarp();
-        } else {
-            // ---------------- epilogue ----------------
-            const int buf = jb & 1, q = warp & 3;
-            int *tile = s_epi + (warp - MMA_WARP - 1) * 32 * EPI_PITCH;
-            tma::mbar_wait(&tfull[buf], (jb >> 1) & 1);
-            tc_fence_after();
-            const int m = c_mod[t];
-            const float inv = 1.0f / (float)m;
-            const int cw = col0 + q * 32;
-            const int r0 = rt * p.Nt;
-            const int nr = min(p.Nt, p.Ki - r0);
-            int *Rt = p.R + ((int64_t)t * p.ncols + cw) * p.Ki + r0;
-            for (int j0 = 0; j0 < p.Nt; j0 += 32) {
-                uint32_t vv[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + j0, vv);
-#pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const int a = (int)vv[j];
-                    tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
-                }
-                __syncwarp();
-                const bool ok = j0 + lane < nr;
-#pragma unroll 8
-                for (int b = 0; b < 32; b++) {
-                    const int r = tile[b * EPI_PITCH + lane];
-                    if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
-                }
-                __syncwarp();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tma::mbar_arrive(&tempty[buf]);
-        }
-        g += n;
-        jb++;
-    }
-    tc_fence_before();
-    cluster_sync();
-    if (warp == MMA_WARP) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Dual-tile variant (one CTA per SM): a unit covers TWO 128-box column tiles (a 256-column
 // pair tile with one slot list) and one operator row tile. Per stage: 2 x 16 KB gathered
@@ -795,28 +413,13 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
                     tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
                     unsigned char *as = smem + st * DUAL_STAGE;
                     if (tid == 0) {
-                        if (p.debug & 2) { // timing experiment: no operator loads (results invalid)
-                            tma::mbar_arrive(&full[st]);
-                        } else {
-                            tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                            tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot,
-                                             &full[st]);
-                            if (p.prefetch > 0) { // L2 prefetch of the operator tile p.prefetch stages ahead
-                                const int ia = (si - s0) * p.KC + kc + p.prefetch;
-                                const int sa = s0 + ia / p.KC, ka = ia % p.KC;
-                                if (sa < s1)
-                                    asm volatile(
-                                        "cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
-                                            reinterpret_cast<uint64_t>(&p.tmB)),
-                                        "r"(ka * BKI), "r"(rt * p.Nt), "r"(t * p.nmat + slots[sa])
-                                        : "memory");
-                            }
-                        }
+                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
+                        tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot, &full[st]);
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
-                        if (((hm >> (i >> 3)) & 1) && !(p.debug & 1))
+                        if ((hm >> (i >> 3)) & 1)
                             tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                     }
                     tma::cp_async_mbar_arrive(&full[st]);
@@ -930,196 +533,6 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == DUAL_MMA_WARP) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Dual tile + operator multicast (cluster of 2): each CTA runs the dual-tile pipeline on its
-// own 256-column pair tile; the two pair tiles of a 512-column quad share one offset list,
-// and each CTA TMA-loads HALF of the operator tile with .multicast::cluster into both CTAs'
-// shared memory -- half the operator bytes per CTA from L2 (the dual kernel's dominant load,
-// profiles/r01_i8_pipe_probe.md). A stage is refilled only when both CTAs' MMAs are done with
-// it (each MMA commit is multicast to both "empty" barriers).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DUAL_THREADS, 1)
-    m2l_i8_dualmc_kernel(const __grid_constant__ Params p) {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    int *s_epi = reinterpret_cast<int *>(smem + DUAL_NST * DUAL_STAGE); // [4 warps][32][33]
-    __shared__ __align__(8) uint64_t full[DUAL_NST], empty[DUAL_NST], tfull, tempty;
-    __shared__ uint32_t s_tmem;
-    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
-    constexpr int NPT = DUAL_NPROD * 32;
-    if (tid == 0) {
-        for (int s = 0; s < DUAL_NST; s++) {
-            tma::mbar_init(&full[s], NPT + 1); // local cp.async + local expect_tx (both B halves' bytes)
-            tma::mbar_init(&empty[s], 2);      // both CTAs' MMA commits (the peer writes our B half)
-        }
-        tma::mbar_init(&tfull, 1);
-        tma::mbar_init(&tempty, 4);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (warp == DUAL_MMA_WARP) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         tma::smem_u32(&s_tmem))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    const uint32_t rank = cluster_rank();
-    const int half = p.Nt / 2;
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem = s_tmem;
-
-    int g = 0, jb = 0;
-    const int nquads = p.coltiles / 4;
-    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
-        int v = u;
-        const int rt = v % p.rowtiles;
-        v /= p.rowtiles;
-        const int qd = v % nquads; // 512-column quad: this CTA owns pair tile 2 qd + rank
-        v /= nquads;
-        const int chunk = v % p.nchunk;
-        const int t = v / p.nchunk;
-        int s0, s1;
-        chunk_range(p, qd, chunk, s0, s1);
-        const int n = (s1 - s0) * p.KC;
-        if (n == 0) continue;
-        const int *slots = p.tile_slots + qd * MAX_SLOTS;
-        const int colp = (2 * qd + (int)rank) * 2 * TBM; // first of this CTA's 256 columns
-        const int hsh = 2 * (int)rank;                      // this CTA's bits of the quad's quarter masks
-        if (warp < DUAL_NPROD) {
-            // ---------------- producers: 256 rows, 16 cp.async of 16 B per thread ----------------
-            const int c = lane & 7, j0 = tid >> 3; // rows j0 + 16 i, i < 16
-            const int8_t *Xt = p.X + (int64_t)t * p.rows_per_mod * p.Ki + c * 16;
-            for (int si = s0; si < s1; si++) {
-                const int slot = slots[si];
-                const int *srow = p.src + (int64_t)slot * p.ld_src + colp;
-                // halves without a source for this slot are neither gathered nor multiplied
-                const int hm = p.half_mask[qd * MAX_SLOTS + slot] >> hsh; // loaded alongside the rows
-                int bx[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++) bx[i] = srow[j0 + 16 * i];
-                int64_t off[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++)
-                    off[i] = (int64_t)(bx[i] >= 0 ? (int)(bx[i] - p.box0) : p.zero_row) * p.Ki;
-                for (int kc = 0; kc < p.KC; kc++) {
-                    const int gi = g + (si - s0) * p.KC + kc, st = gi % DUAL_NST;
-                    tma::mbar_wait(&empty[st], ((gi / DUAL_NST) & 1) ^ 1);
-                    unsigned char *as = smem + st * DUAL_STAGE;
-                    if (tid == 0) {
-                        // this CTA's half of the operator tile, multicast into both CTAs; the
-                        // local barrier expects both halves
-                        tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        asm volatile(
-                            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
-                            "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
-                                tma::smem_u32(as + DUAL_A_BYTES + (int)rank * half * BKI)),
-                            "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI), "r"(rt * p.Nt + (int)rank * half),
-                            "r"(t * p.nmat + slot), "r"(tma::smem_u32(&full[st])), "h"((uint16_t)3)
-                            : "memory");
-                    }
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        const int j = j0 + 16 * i; // rows 0..127: tile 0, 128..255: tile 1 (contiguous)
-                        if (((hm >> (i >> 3)) & 1) && !(p.debug & 1))
-                            tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
-                    }
-                    tma::cp_async_mbar_arrive(&full[st]);
-                }
-            }
-        } else if (warp == DUAL_MMA_WARP) {
-            // ---------------- MMA issuer: two M128 x Nt MMAs per k-step (whole warp,
-            // elected lane issues) ----------------
-            tma::mbar_wait(&tempty, (jb & 1) ^ 1);
-            tc_fence_after();
-            int st = g % DUAL_NST;
-            uint32_t ph = (g / DUAL_NST) & 1;
-            const uint32_t sbase = tma::smem_u32(smem);
-            bool started0 = false, started1 = false; // first MMA of a half overwrites its accumulator
-            const uint8_t *hmt = p.half_mask + qd * MAX_SLOTS;
-            int hm = hmt[slots[s0]] >> hsh;
-            int hm_next = s0 + 1 < s1 ? hmt[slots[s0 + 1]] >> hsh : 0;
-            for (int i = 0, kc = 0, si = s0; i < n; i++) {
-                tma::mbar_wait(&full[st], ph);
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                tc_fence_after();
-                const uint32_t a0 = sbase + st * DUAL_STAGE;
-                const uint64_t ad0 = sw128_desc(a0), ad1 = sw128_desc(a0 + A_BYTES), bd = sw128_desc(a0 + DUAL_A_BYTES);
-                // REDUX writes a uniform register: the conditional MMAs stay on the uniform datapath
-                // (a branch on a loaded value would bring back the per-MMA R2UR waterfall)
-                const unsigned hu = __reduce_or_sync(0xffffffffu, (unsigned)hm);
-                const bool on0 = (hu & 1u) != 0, on1 = (hu & 2u) != 0;
-#pragma unroll
-                for (int kk = 0; kk < BKI / 32; kk++) {
-                    if (on0) mma_i8_elect(tmem, ad0 + 2 * kk, bd + 2 * kk, p.idesc, (started0 || kk > 0) ? 1u : 0u);
-                    if (on1) mma_i8_elect(tmem + 256, ad1 + 2 * kk, bd + 2 * kk, p.idesc, (started1 || kk > 0) ? 1u : 0u);
-                }
-                started0 |= on0;
-                started1 |= on1;
-                asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
-                             "cluster.b64 [%0], %1;\n}\n" ::"r"(tma::smem_u32(&empty[st])),
-                             "h"((uint16_t)3)
-                             : "memory");
-                if (++st == DUAL_NST) st = 0, ph ^= 1;
-                if (++kc == p.KC) { // next slot: its mask was loaded a slot ahead
-                    kc = 0;
-                    si++;
-                    hm = hm_next;
-                    hm_next = si + 1 < s1 ? hmt[slots[si + 1]] >> hsh : 0;
-                }
-            }
-            commit_elect(&tfull);
-            __syncwarp();
-        } else {
-            // ---------------- epilogue: both accumulators ----------------
-            const int q = warp & 3;
-            int *tile = s_epi + (warp - DUAL_MMA_WARP - 1) * 32 * EPI_PITCH;
-            tma::mbar_wait(&tfull, jb & 1);
-            tc_fence_after();
-            const int m = c_mod[t];
-            const float inv = 1.0f / (float)m;
-            const int r0 = rt * p.Nt;
-            const int nr = min(p.Nt, p.Ki - r0);
-            int used = 0; // halves that received an MMA in this unit (others hold stale TMEM)
-            for (int si = s0 + lane; si < s1; si += 32) used |= p.half_mask[qd * MAX_SLOTS + slots[si]] >> hsh;
-            for (int o = 16; o; o >>= 1) used |= __shfl_xor_sync(0xffffffffu, used, o);
-            for (int h = 0; h < 2; h++) {
-                if (!((used >> h) & 1)) continue;
-                int *Rt = p.R + ((int64_t)t * p.ncols + colp + h * TBM + q * 32) * p.Ki + r0;
-                for (int j0 = 0; j0 < p.Nt; j0 += 32) {
-                    uint32_t vv[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + h * 256 + j0, vv);
-#pragma unroll
-                    for (int j = 0; j < 32; j++) {
-                        const int a = (int)vv[j];
-                        tile[lane * EPI_PITCH + j] = a - __float2int_rn((float)a * inv) * m;
-                    }
-                    __syncwarp();
-                    const bool ok = j0 + lane < nr;
-#pragma unroll 8
-                    for (int b = 0; b < 32; b++) {
-                        const int r = tile[b * EPI_PITCH + lane];
-                        if (ok && r) atomicAdd(Rt + (int64_t)b * p.Ki + j0 + lane, r);
-                    }
-                    __syncwarp();
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tma::mbar_arrive(&tempty);
-        }
-        g += n;
-        jb++;
-    }
-    tc_fence_before();
-    cluster_sync(); // no CTA leaves while the peer may still multicast into it
     if (warp == DUAL_MMA_WARP) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
@@ -1241,7 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
                         const int j = j0 + 16 * i;
-                        if (((on >> (i >> 3)) & 1) && !(p.debug & 1))
+                        if ((on >> (i >> 3)) & 1)
                             tma::cp_async16(as + j * BKI + ((c ^ (j & 7)) << 4), Xt + off[i] + kc * BKI, 16);
                     }
                     tma::cp_async_mbar_arrive(&fullA[st]);
@@ -1259,11 +672,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
                         asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(bar),
                                      "r"(2 * half * BKI)
                                      : "memory");
-                    const int mat = (p.debug & 16) ? 0 : slot; // 16: one L2-resident operator
                     asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
                                  "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tma::smem_u32(ringB + st * PD_B_BYTES)),
                                  "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
-                                 "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + mat), "r"(bar)
+                                 "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + slot), "r"(bar)
                                  : "memory");
                 }
                 __syncwarp();
@@ -1275,12 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
                     const int gi = g + i, st = gi % PD_NA;
                     tma::mbar_wait(&fullA[st], (gi / PD_NA) & 1);
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                    if (lane == 0) {
-                        if (p.debug & 64)
-                            remote_arrive(map_to_rank(&pfullA[st], 0));
-                        else
-                            remote_arrive_cta(map_to_rank(&pfullA[st], 0));
-                    }
+                    if (lane == 0) remote_arrive_cta(map_to_rank(&pfullA[st], 0));
                     __syncwarp();
                 }
             } else {
@@ -1723,24 +1130,41 @@ int sm_count() {
 
 const int *i8_moduli() { return kModuli; }
 
+int64_t i8_window(int nmod, int Ki) {
+    (void)nmod;
+    (void)Ki;
+    return std::max<int64_t>(kI8Tile, tuning().i8_window / kI8Tile * kI8Tile);
+}
+
 const I8Settings &i8_settings() {
-    static I8Settings s = [] {
+    static const I8Settings s = [] {
+        const Tuning &t = tuning();
         I8Settings r;
-        const char *e = std::getenv("PKGPU_M2L");
-        r.enabled = !(e && std::strcmp(e, "dmma") == 0);
+        r.enabled = t.m2l_int8;
         // measured at cfg2: the int8 translations lose to the DMMA gather-GEMM (the per-column
         // residue / CRT traffic outweighs the GEMM for 1-8 slots), so they are opt-in
-        const char *t = std::getenv("PKGPU_TRANS");
-        r.trans = r.enabled && t && std::strcmp(t, "i8") == 0;
-        if (const char *c = std::getenv("PKGPU_M2L_I8")) {
-            int a = r.nmod, b = r.beta_a, d = r.beta_b;
-            if (std::sscanf(c, "%d,%d,%d", &a, &b, &d) == 3) r.nmod = a, r.beta_a = b, r.beta_b = d;
-        }
-        if (const char *c = std::getenv("PKGPU_M2L_I8_MIN")) r.min_boxes = std::atoll(c);
-        r.nmod = std::max(14, std::min(r.nmod, kI8MaxModuli));
+        r.trans = r.enabled && t.trans_int8;
+        r.nmod = std::max(14, std::min(t.nmod, kI8MaxModuli));
+        r.beta_a = t.beta_a;
+        r.beta_b = t.beta_b;
+        r.min_boxes = t.i8_min_boxes;
         return r;
     }();
     return s;
+}
+
+I8Settings i8_settings_for(const I8Settings &s, int64_t nslots, int K) {
+    I8Settings r = s;
+    if (!r.enabled) return r;
+    const double need = r.beta_a + r.beta_b + std::log2((double)nslots * K) + 1.0;
+    auto bits = [](int nmod) {
+        double b = 0;
+        for (int t = 0; t < nmod; t++) b += std::log2((double)kModuli[t]);
+        return b;
+    };
+    while (bits(r.nmod) <= need && r.nmod < kI8MaxModuli) r.nmod++;
+    if (bits(r.nmod) <= need) r.enabled = r.trans = false;
+    return r;
 }
 
 void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat, int K, int Kp, int nmod,
@@ -1764,66 +1188,67 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
 
 namespace {
 
-// kernel variant per launch: 0 single CTA (m2l_i8_kernel), 1 cta_group::2 pair
-// (m2l_i8_pair_kernel), 2 operator-multicast pair (m2l_i8_mc_kernel), 3 dual tile
-// (m2l_i8_dual_kernel), 4 dual tile + operator multicast across a CTA pair (m2l_i8_dualmc_kernel,
-// 2% faster at cfg2 level 4, slower on the small-level run), 5 pair-dual (cta_group::2, 512-column
-// quads, m2l_i8_pairdual_kernel). Default: pair-dual for big levels (cfg2 level 4 6.86 -> 6.63
-// ms, cfg3 608 -> 518 ms per evaluate), dual for the small-level runs (the pair-dual kernel's
-// 1024-column run streams the operators as often and balances worse: 2.6 -> 3.9 ms at cfg2).
-// A tile's quarters / halves with no source for a slot skip their gather and MMA.
-// i8_gather_gemm (tests) keeps the single kernel below 2048 columns so all stay covered.
-// PKGPU_I8_PAIR forces one variant everywhere. See DESIGN.md §4.
-int select_mode(bool big) {
-    static const int forced = [] {
-        const char *e = std::getenv("PKGPU_I8_PAIR");
-        return e ? std::max(0, std::min(5, std::atoi(e))) : -1;
-    }();
-    // measured: with per-half slot masks the dual kernel also wins on cfg2's small-level run;
-    // PKGPU_I8_SMALLMODE picks the small-run kernel for comparisons
-    static const int small_mode =
-        std::getenv("PKGPU_I8_SMALLMODE") ? std::max(0, std::min(5, std::atoi(std::getenv("PKGPU_I8_SMALLMODE")))) : 3;
-    static const int big_mode =
-        std::getenv("PKGPU_I8_BIGMODE") ? std::max(0, std::min(5, std::atoi(std::getenv("PKGPU_I8_BIGMODE")))) : 5;
-    return forced >= 0 ? forced : (big ? big_mode : small_mode);
+// Kernel variant per launch (I8Kernel): pair-dual (cta_group::2, 512-column quads) for big
+// levels (cfg2 level 4: 6.86 -> 6.63 ms against the dual kernel, cfg3 608 -> 518 ms per
+// evaluate); dual for the packed small-level runs (the pair-dual kernel's 1024-column run
+// streams the operators as often and balances worse: 2.6 -> 3.9 ms at cfg2). A tile's
+// quarters / halves with no source for a slot skip their gather and MMA. i8_gather_gemm
+// (tests) keeps the single-CTA kernel below 2048 columns so all three stay covered.
+// PKGPU_I8_KERNEL forces one variant everywhere. See DESIGN.md §4.
+I8Kernel select_kernel(bool big) {
+    const I8Kernel forced = tuning().i8_kernel;
+    if (forced != I8Kernel::automatic) return forced;
+    return big ? I8Kernel::pairdual : I8Kernel::dual;
 }
 // operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
 // (from the true K: operator rows past K inside the 128-padded Ki are never computed)
 int rowtiles_of(int K) { return (K + 255) / 256; }
 int nt_of(int K) { return ((K + rowtiles_of(K) - 1) / rowtiles_of(K) + 31) / 32 * 32; }
-// the 512-column variants need whole quads; the pair-dual one also Nt / 2 a multiple of 16
-int window_mode(int mode, int ncols, int K) {
-    if (mode >= 4 && ncols % (4 * TBM) != 0) return 3;
-    if (mode == 5 && nt_of(K) % 32 != 0) return 3;
-    return mode;
+// the pair-dual kernel needs whole 512-column quads and Nt / 2 a multiple of 16
+I8Kernel window_kernel(I8Kernel k, int ncols, int K) {
+    if (k == I8Kernel::pairdual && (ncols % (4 * TBM) != 0 || nt_of(K) % 32 != 0)) return I8Kernel::dual;
+    return k;
 }
-int column_tile(int mode) { return mode >= 4 ? 4 * TBM : mode != 0 ? 2 * TBM : TBM; }
+int column_tile(I8Kernel k) { return k == I8Kernel::pairdual ? 4 * TBM : k == I8Kernel::dual ? 2 * TBM : TBM; }
+bool masked(I8Kernel k) { return k != I8Kernel::single; }
 
 inline size_t partial_offset(int tiles) { return ((size_t)tiles * MAX_SLOTS + 15) / 16 * 16; }
 
-// active-slot lists per column tile (ncols / column_tile(mode) tiles)
-void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, int mode, Workspace &ws, cudaStream_t st,
+// active-slot lists per column tile (ncols / column_tile(k) tiles)
+void scan_tiles(const int *src, int64_t ld_src, int nslots, int ncols, I8Kernel k, Workspace &ws, cudaStream_t st,
                 int **tslots, int **tnact, int **tbelow, uint8_t **thmask = nullptr) {
-    const int bn = column_tile(mode), tiles = ncols / bn;
+    const int bn = column_tile(k), tiles = ncols / bn;
     *tslots = ws.get<int>("i8_tile_slots", (size_t)tiles * MAX_SLOTS);
     *tnact = ws.get<int>("i8_tile_nact", tiles);
     *tbelow = ws.get<int>("i8_tile_below", (size_t)tiles * (MAX_SLOTS + 1));
-    // per-tile masks [tiles][MAX_SLOTS] followed by the per-tile partial flags (int, see
-    // partial_flags)
-    uint8_t *hmask = mode >= 3 ? ws.get<uint8_t>("i8_tile_hmask", partial_offset(tiles) + (size_t)tiles * 4) : nullptr;
-    int *partial = mode >= 3 ? reinterpret_cast<int *>(hmask + partial_offset(tiles)) : nullptr;
+    // per-tile masks [tiles][MAX_SLOTS] followed by the per-tile partial flags (int)
+    uint8_t *hmask = masked(k) ? ws.get<uint8_t>("i8_tile_hmask", partial_offset(tiles) + (size_t)tiles * 4) : nullptr;
+    int *partial = masked(k) ? reinterpret_cast<int *>(hmask + partial_offset(tiles)) : nullptr;
     slot_scan_kernel<<<tiles, 1024, 0, st>>>(src, ld_src, nslots, bn, *tslots, *tnact, *tbelow, hmask, partial);
     if (thmask) *thmask = hmask;
     PK_CUDA(cudaGetLastError());
 }
 
+// dynamic shared memory opt-in, per device (the attribute is per device; one process may
+// drive several GPUs)
+template <class F> void ensure_smem(F *kernel, size_t bytes) {
+    static std::mutex mtx;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mtx);
+    size_t &d = done[{reinterpret_cast<const void *>(kernel), dev}];
+    if (d >= bytes) return;
+    PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    d = bytes;
+}
+
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
-                 const int *tnact, const int *tbelow, int mode, cudaStream_t st, bool direct = false,
+                 const int *tnact, const int *tbelow, I8Kernel kind, cudaStream_t st, bool direct = false,
                  const uint8_t *thmask = nullptr, int K = 0) {
-    if (mode >= 3 && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernel needs the half masks");
+    if (masked(kind) && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernels need the half masks");
     const int num_sms = sm_count();
-    const bool pair = mode != 0;
     Params p;
     std::memset(&p, 0, sizeof p);
     p.X = B;
@@ -1844,137 +1269,61 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.R = R;
     // instruction descriptor: D s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9 / 10-12 = 1),
     // both K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the CTA pair)
-    const int M = (mode == 1 || mode == 5) ? 2 * TBM : TBM;
+    const int M = kind == I8Kernel::pairdual ? 2 * TBM : TBM;
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.Nt >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-    static const int debug = std::getenv("PKGPU_I8_DEBUG") ? std::atoi(std::getenv("PKGPU_I8_DEBUG")) : 0;
-    p.debug = debug;
+    // chunks keep |int32 accumulator| <= slots * Ki * 128^2 < 2^31
     const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
     int nchunk = (int)((nslots + cmax - 1) / cmax);
-    static const int min_chunks = std::getenv("PKGPU_I8_CHUNKS") ? std::atoi(std::getenv("PKGPU_I8_CHUNKS")) : 0;
-    nchunk = std::max(nchunk, min_chunks);
-    const int64_t base = (int64_t)nmod * p.rowtiles * (mode >= 4 ? p.coltiles / 4 : pair ? p.coltiles / 2 : p.coltiles);
-    const int64_t resident = (mode == 1 || mode == 2 || mode >= 4) ? num_sms / 2 : num_sms;
+    const int64_t base = (int64_t)nmod * p.rowtiles * (ncols / column_tile(kind));
+    const int64_t resident = kind == I8Kernel::pairdual ? num_sms / 2 : num_sms;
     // enough units for ~4 per resident CTA (cfg2's small-level run: 3 -> 4 chunks, 2.57 -> 2.43 ms)
     while (base * nchunk < 4 * resident && nchunk * 16 < nslots) nchunk++;
     p.nchunk = nchunk;
     p.total_units = (int)(base * nchunk);
-    if (direct && (nchunk != 1 || mode != 0)) throw RuntimeError("i8 gemm: direct stores need one unit per tile");
+    if (direct && (nchunk != 1 || kind != I8Kernel::single))
+        throw RuntimeError("i8 gemm: direct stores need one unit per tile");
     p.direct = direct ? 1 : 0;
+    p.epi_transpose = 1;
     p.tile_slots = tslots;
     p.tile_nact = tnact;
     p.tile_below = tbelow;
     p.nslots = nslots;
     p.half_mask = thmask;
-    p.tile_partial = thmask ? reinterpret_cast<const int *>(thmask + partial_offset(ncols / column_tile(mode))) : nullptr;
-    // slot-index windows for the small-level run (operator reuse through L2 across its
-    // tiles); equal list shares for the dual-tile big levels (balanced static schedule)
-    static const int by_index_env = std::getenv("PKGPU_I8_BYINDEX") ? std::atoi(std::getenv("PKGPU_I8_BYINDEX")) : -1;
-    p.by_index = by_index_env >= 0 ? by_index_env : (mode >= 3 ? 0 : 1);
+    p.tile_partial = thmask ? reinterpret_cast<const int *>(thmask + partial_offset(ncols / column_tile(kind))) : nullptr;
+    // slot-index windows for the single-CTA kernel (operator reuse through L2 across its
+    // tiles); equal list shares for the dual-tile kernels (balanced static schedule)
+    p.by_index = masked(kind) ? 0 : 1;
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
-    // the CTA-pair variants stage half of the operator tile per CTA
-    const bool half_tile = mode == 1 || mode == 2 || mode >= 4;
-    const cuuint32_t box[3] = {BKI, (cuuint32_t)(half_tile ? p.Nt / 2 : p.Nt), 1};
+    // the CTA-pair kernel stages half of the operator tile per CTA
+    const cuuint32_t box[3] = {BKI, (cuuint32_t)(kind == I8Kernel::pairdual ? p.Nt / 2 : p.Nt), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    // L2 sector promotion of the operator rows (PKGPU_I8_L2PROMO = 0 / 64 / 128 / 256, default 256)
-    static const CUtensorMapL2promotion promo = [] {
-        const int v = std::getenv("PKGPU_I8_L2PROMO") ? std::atoi(std::getenv("PKGPU_I8_L2PROMO")) : 256;
-        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-               : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    }();
     const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
-                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
-    if (mode == 1) {
-        if (p.Nt % 32 != 0) throw RuntimeError("i8 pair kernel: Nt / 2 must be a multiple of 16");
-        const cuuint64_t xd[2] = {(cuuint64_t)Ki, (cuuint64_t)nmod * rows_per_mod};
-        const cuuint64_t xs[1] = {(cuuint64_t)Ki};
-        const cuuint32_t xb[2] = {BKI, 1};
-        const cuuint32_t xe[2] = {1, 1};
-        const CUresult rx = encode_fn()(&p.tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t *>(B), xd, xs, xb, xe,
-                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (rx != CUDA_SUCCESS)
-            throw CudaError("cuTensorMapEncodeTiled (int8 gather) failed (" + std::to_string((int)rx) + ")");
-    }
     const size_t epi = 4 * 32 * EPI_PITCH * sizeof(int) + 1024;
-    if (mode == 5) {
-        static const int prefetch = std::getenv("PKGPU_I8_PREFETCH") ? std::atoi(std::getenv("PKGPU_I8_PREFETCH")) : 0;
-        p.prefetch = prefetch;
+    if (kind == I8Kernel::pairdual) {
         if (ncols % (4 * TBM) != 0) throw RuntimeError("i8 gemm: the pair-dual kernel needs 512-column multiples");
         if (p.Nt % 32 != 0 || p.Nt / 2 > 128) throw RuntimeError("i8 pair-dual kernel: Nt / 2 must be a multiple of 16");
         const size_t smem = PD_RING_BYTES + epi;
-        static bool cfg = false;
-        if (!cfg) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_pairdual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
-        }
+        ensure_smem(m2l_i8_pairdual_kernel, smem);
         const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
         m2l_i8_pairdual_kernel<<<grid, PD_THREADS, smem, st>>>(p);
-    } else if (mode == 4) {
-        if (ncols % (4 * TBM) != 0) throw RuntimeError("i8 gemm: the multicast dual kernel needs 512-column multiples");
+    } else if (kind == I8Kernel::dual) {
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
-        static bool cfg = false;
-        if (!cfg) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_dualmc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
-        }
-        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
-        m2l_i8_dualmc_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
-    } else if (mode == 3) {
-        static const int prefetch = std::getenv("PKGPU_I8_DUALPF") ? std::atoi(std::getenv("PKGPU_I8_DUALPF")) : 0;
-        p.prefetch = prefetch;
-        const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
-        static bool cfg = false;
-        if (!cfg) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
-        }
+        ensure_smem(m2l_i8_dual_kernel, smem);
         const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
         m2l_i8_dual_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
-    } else if (mode == 2) {
-        const size_t smem = (size_t)NST * STAGE_BYTES + epi;
-        static bool cfg = false;
-        if (!cfg) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = true;
-        }
-        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
-        m2l_i8_mc_kernel<<<grid, NTHREADS, smem, st>>>(p);
-    } else if (pair) {
-        p.stage_bytes = A_BYTES + (p.Nt / 2 * BKI + 1023) / 1024 * 1024;
-        p.nst = (int)std::min<size_t>(NST_MAX, (227 * 1024 - epi) / p.stage_bytes);
-        const size_t smem = (size_t)p.nst * p.stage_bytes + epi;
-        static size_t cfg = 0;
-        if (cfg < smem) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = smem;
-        }
-        const unsigned grid = 2 * (unsigned)std::min<int64_t>(p.total_units, num_sms / 2);
-        m2l_i8_pair_kernel<<<grid, PAIR_THREADS, smem, st>>>(p);
     } else {
         // stage = 16 KB gathered rows + the operator tile rounded to 1 KB; as many stages as
         // the 227 KB of shared memory allow (the transposing epilogue costs 16.5 KB)
-        static const bool transpose = [] {
-            const char *e = std::getenv("PKGPU_I8_EPI");
-            return !(e && std::strcmp(e, "direct") == 0);
-        }();
-        p.epi_transpose = (transpose || direct) ? 1 : 0;
-        static const int prefetch = std::getenv("PKGPU_I8_PREFETCH") ? std::atoi(std::getenv("PKGPU_I8_PREFETCH")) : 0;
-        p.prefetch = prefetch;
         p.stage_bytes = A_BYTES + (p.Nt * BKI + 1023) / 1024 * 1024;
-        const size_t epi_bytes = transpose ? 4 * 32 * EPI_PITCH * sizeof(int) : 0;
+        const size_t epi_bytes = 4 * 32 * EPI_PITCH * sizeof(int);
         const size_t avail = 227 * 1024 - 1024 - 512 - epi_bytes;
         p.nst = (int)std::min<size_t>(NST_MAX, avail / p.stage_bytes);
         const size_t smem = (size_t)p.nst * p.stage_bytes + epi_bytes + 1024;
-        static size_t cfg = 0;
-        if (cfg < smem) {
-            PK_CUDA(cudaFuncSetAttribute(m2l_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cfg = smem;
-        }
+        ensure_smem(m2l_i8_kernel, smem);
         const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
         m2l_i8_kernel<<<grid, NTHREADS, smem, st>>>(p);
     }
@@ -1991,12 +1340,11 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
         throw RuntimeError("i8_gather_gemm: bad shape");
     upload_tables();
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
-    int mode = ncols >= 2048 ? select_mode(true) : 0;
-    mode = window_mode(mode, ncols, Ki);
+    const I8Kernel kind = window_kernel(ncols >= 2048 ? select_kernel(true) : I8Kernel::single, ncols, Ki);
     uint8_t *thmask = nullptr;
-    scan_tiles(src, ld_src, nslots, ncols, mode, ws, st, &tslots, &tnact, &tbelow, &thmask);
+    scan_tiles(src, ld_src, nslots, ncols, kind, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
-                tbelow, mode, st, false, thmask);
+                tbelow, kind, st, false, thmask);
     return 2;
 }
 
@@ -2021,7 +1369,7 @@ I8LevelWork m2l_i8_prepare(const I8Operators &o, const I8LevelArgs &a, int beta_
         a.X + box0 * a.Kp, nbox, a.K, a.Kp, Ki, nmod, beta_b, w.mx, a.lv, xres);
     w.xres = xres;
     upload_tables();
-    w.mode = select_mode(a.big);
+    w.kind = select_kernel(a.big);
     PK_CUDA(cudaGetLastError());
     if (launches) *launches += 1 + a.lv.n;
     return w;
@@ -2045,8 +1393,8 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
     // the multicast variant needs whole 512-column quads; other windows use the dual kernel
-    w.win_mode = window_mode(w.mode, ncols, o.K);
-    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.win_mode, ws, st, &w.tile_slots, &w.tile_nact,
+    w.win_kind = window_kernel(w.kind, ncols, o.K);
+    scan_tiles(a.src + c0, a.ld_src, a.nslots, ncols, w.win_kind, ws, st, &w.tile_slots, &w.tile_nact,
                &w.tile_below, &w.tile_hmask);
     if (a.mma_rows && w.tile_hmask) {
         mma_rows_kernel<<<ncols / (2 * TBM), 32, 0, st>>>(w.tile_hmask, a.nslots, a.mma_rows);
@@ -2062,7 +1410,7 @@ int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int6
     const int ncols = (int)(c1 - c0);
     if (ncols <= 0) return 0;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
-                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.win_mode, st, false,
+                a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.win_kind, st, false,
                 w.tile_hmask, o.K);
     return 1;
 }
@@ -2101,15 +1449,14 @@ int i8_translate(const I8Operators &o, const I8TransArgs &a, int beta_b, Workspa
     int *R = ws.get<int>("tr_R", (size_t)nmod * a.ncols * Ki);
     // <= 16 slots: one work unit per output tile (launch_gemm), whose epilogue stores the
     // partial residues directly -- no R zeroing, no atomics
-    static const bool chunks_forced = std::getenv("PKGPU_I8_CHUNKS") != nullptr;
-    const bool direct = a.nslots <= 16 && !chunks_forced;
+    const bool direct = a.nslots <= 16;
     tr_prepare_kernel<<<a.ncols, 256, 0, st>>>(a.src, a.ld_src, a.nslots, a.src_lo, nsrc, a.X, a.K, a.Kp, Ki, nmod,
                                                 beta_b, a.ncols, xres, ecol, R, direct ? 0 : 1);
     PK_CUDA(cudaGetLastError());
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
-    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, 0, ws, st, &tslots, &tnact, &tbelow);
+    scan_tiles(a.src, a.ld_src, a.nslots, a.ncols, I8Kernel::single, ws, st, &tslots, &tnact, &tbelow);
     launch_gemm(o.res, o.nmat, xres, (int)(nsrc + 1), (int)nsrc, Ki, nmod, a.src, a.ld_src, a.src_lo, a.nslots,
-                a.ncols, R, tslots, tnact, tbelow, 0, st, direct, nullptr, o.K);
+                a.ncols, R, tslots, tnact, tbelow, I8Kernel::single, st, direct, nullptr, o.K);
     const int64_t n = (int64_t)a.ncols * Ki;
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
     const int bs = o.beta_a + beta_b;

@@ -19,24 +19,16 @@
 #include <cstdlib>
 
 #include "common.h"
+#include "tuning.h"
 
 namespace pkgpu {
 
 constexpr int kI8MaxModuli = 20;
 constexpr int kI8Tile = 256; // columns per tile: level column counts are padded to this
 constexpr int64_t kI8Window = 65536; // columns per M2L gemm/finish window
-// columns per window (PKGPU_I8_WINDOW overrides): the int32 residue sums R stay small enough
-// for their atomics to hit L2 (one window of cfg4's 262k-box level: 85.8 ms, four: 82.5 ms)
-inline int64_t i8_window(int nmod, int Ki) {
-    (void)nmod;
-    (void)Ki;
-    static const int64_t w = [] {
-        const char *e = std::getenv("PKGPU_I8_WINDOW");
-        const int64_t v = e ? std::atoll(e) : kI8Window;
-        return std::max<int64_t>(kI8Tile, v / kI8Tile * kI8Tile);
-    }();
-    return w;
-}
+// columns per window (tuning().i8_window, default kI8Window): the int32 residue sums R stay
+// small enough for their atomics to hit L2 (one window of cfg4's 262k-box level: 85.8 ms, four: 82.5 ms)
+int64_t i8_window(int nmod, int Ki);
 
 struct I8Operators {          // residues of the stacked M2L operators (built once per KifmmOps)
     int nmod = 0, beta_a = 0, Ki = 0, nmat = 0, K = 0;
@@ -50,8 +42,12 @@ struct I8Settings {
     int nmod = 16, beta_a = 52, beta_b = 52; // accuracy study: profiles/r01_m2l_arith_study.md
     int64_t min_boxes = 1;    // levels with fewer boxes stay on the DMMA gather-GEMM
 };
-// PKGPU_M2L = i8 | dmma (default i8), PKGPU_M2L_I8 = "nmod,beta_a,beta_b", PKGPU_M2L_I8_MIN = boxes,
-// PKGPU_TRANS = i8 | dmma (default dmma; i8 requires PKGPU_M2L = i8)
+// the settings a call with nslots x K products per output actually uses: |S| <=
+// nslots K 2^(beta_a + beta_b) must stay below M / 2 (M = product of the moduli), so moduli
+// are added (up to kI8MaxModuli) while it does not; if even that is short, int8 is disabled
+// for the call (M2L on DMMA). Stokes p <= 16 fits the default 16 moduli.
+I8Settings i8_settings_for(const I8Settings &s, int64_t nslots, int K);
+// process defaults from tuning() (PKGPU_M2L, PKGPU_M2L_I8, PKGPU_M2L_I8_MIN, PKGPU_TRANS)
 const I8Settings &i8_settings();
 
 // `tag` names the operator set's workspace buffers (one I8Operators per matrix stack)
@@ -105,7 +101,7 @@ struct I8LevelArgs {
     I8Levels lv;                  // sources of a column are boxes of the column's own level
     const double *X = nullptr;    // [box][Kp]
     double *Y = nullptr;          // [box][Kp]: Y += alpha_l * sum_slot M X
-    bool big = false;             // one large level: the dual-tile kernel (see select_mode)
+    bool big = false;             // one large level: the pair-dual kernel (see select_kernel)
     unsigned long long *mma_rows = nullptr; // profiling: += 128 x active (pair tile, slot, half) triples
 };
 struct I8LevelWork {
@@ -116,8 +112,8 @@ struct I8LevelWork {
     int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile
     int *tile_below = nullptr;                       // per tile: active slots below each slot index
     uint8_t *tile_hmask = nullptr;                   // dual kernel: per (pair tile, slot) active halves
-    int mode = 0;                                    // kernel variant (select_mode)
-    int win_mode = 0;                                // variant of the current column window
+    I8Kernel kind = I8Kernel::automatic;             // kernel variant (select_kernel)
+    I8Kernel win_kind = I8Kernel::automatic;         // variant of the current column window
 };
 // The three steps of one level (separately timed by the stage profiler):
 //   prepare: level max, density residues

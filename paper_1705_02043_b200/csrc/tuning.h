@@ -1,0 +1,33 @@
+// Process-wide tuning knobs of libpkgpu, all read once from the environment here and
+// nowhere else. Every default is the measured best on B200; the knobs exist
+// for comparison runs and are documented in INTEGRATION.md ("Tuning knobs").
+#pragma once
+
+#include <cstdint>
+
+namespace pkgpu {
+
+enum class I8Kernel : int {
+    automatic = -1, // pair-dual for big levels, dual for the packed small-level runs
+    single = 0,     // m2l_i8_kernel: one CTA, 128-box tiles
+    dual = 1,       // m2l_i8_dual_kernel: one CTA, 256-box pair tiles
+    pairdual = 2,   // m2l_i8_pairdual_kernel: CTA pair (cta_group::2), 512-box quads
+};
+
+struct Tuning {
+    bool m2l_int8 = true;              // PKGPU_M2L = i8 | dmma: default M2L arithmetic of new contexts
+    bool trans_int8 = false;           // PKGPU_TRANS = i8 | dmma: M2M / L2L / pinv on the int8 pipe
+    int nmod = 16, beta_a = 52, beta_b = 52; // PKGPU_M2L_I8 = "nmod,beta_a,beta_b"
+    int64_t i8_min_boxes = 1;          // PKGPU_M2L_I8_MIN: levels with fewer boxes use DMMA
+    int64_t i8_small_boxes = 1024;     // PKGPU_I8_SMALL: levels up to this size share packed runs
+    int64_t i8_window = 65536;         // PKGPU_I8_WINDOW: columns per int8 M2L window (bounds R)
+    I8Kernel i8_kernel = I8Kernel::automatic; // PKGPU_I8_KERNEL = single | dual | pairdual
+    int64_t gemm_units_per_cta = 32;   // PKGPU_GEMM_UNITS: DMMA gather-GEMM work units per CTA
+    int64_t gemm_min_iters = 16;       // PKGPU_GEMM_MINIT: k-iterations per split-K unit
+    int64_t gemm_min_iters_small = 4;  // PKGPU_GEMM_MINIT_SMALL: same, latency-bound one-slot GEMMs
+    int64_t list_warp_max = 50000;     // PKGPU_LIST_WARP_MAX: trees up to this size list a warp per box
+};
+
+const Tuning &tuning();
+
+} // namespace pkgpu

@@ -170,6 +170,14 @@ EVAL_ADAPTIVE = [
 ]
 
 
+# p = 10 (K = 1464 for Stokes: BASELINE cfg3 / cfg5's order), ~4k points each
+EVAL_P10 = [
+    ("sto_tp_p10", "stokeslet", "tp", "", 2, 10, 40, 4000, "gated"),
+    ("sto_tp_p10_clu", "stokeslet", "tp", "", 2, 10, 30, 4000, "gated", 4, 0.02),
+    ("sto_dp_p10_clu", "stokeslet", "dp", "", 2, 10, 30, 4000, "standin", 8, 0.04),
+]
+
+
 def op_path(kernel, per, axes, ell, p, kind):
     tag = f"{kernel}_{per}{axes}_ell{ell}_p{p}_{kind}.pkm2l"
     return os.path.join(OPS, tag)
@@ -192,9 +200,9 @@ def make_op(kernel, per, axes, ell, p, kind):
     return path
 
 
-def golden_eval(tmp, cases=None):
+def golden_eval(tmp, cases=None, transform=None):
     for case in cases or EVAL_CASES:
-        (name, kernel, per, axes, ell, p, leaf, n, opk), extra = case[:9], case[9:]
+        (name, kernel, per, axes, ell, p, leaf, n, opk), extra = case[:9], case[9:11]
         ks = 1 if kernel == "laplace" else 3
         gaxes = {"none": "xyz", "sp": axes or "z", "dp": "xy", "tp": "xyz"}[per]
         if extra:
@@ -202,6 +210,8 @@ def golden_eval(tmp, cases=None):
                            nclusters=extra[0], sigma=extra[1])
         else:
             src, rho = gen(tmp, "e", n, kind="uniform", ks=ks, seed=1000 + n + len(name), axes=gaxes)
+        if transform:
+            rho = transform(case, rho)
         ps, pr = save_pts(tmp, "es", src), save_pts(tmp, "er", rho)
         args = ["eval", "--kernel", kernel, "--per", per, "--ell", ell, "--p", p, "--leaf", leaf, "--src", ps,
                 "--str", pr, "--out", os.path.join(tmp, "ev")]
@@ -232,6 +242,34 @@ def golden_eval(tmp, cases=None):
 
 def golden_eval_adaptive(tmp):
     golden_eval(tmp, EVAL_ADAPTIVE)
+
+
+# dynamic range of the strengths (the int8 M2L's fixed point is relative to each level's
+# max |phi|): two clusters, each made neutral on its own, cluster 0 scaled down by `scale`
+# (name, kernel, per, axes, ell, p, leaf, n, op-spec, nclusters, sigma, scale)
+EVAL_DYN = [
+    ("lap_sp_p8_dyn", "laplace", "sp", "", 2, 8, 30, 4000, "gated", 2, 0.03, 1e-6),
+    ("sto_tp_p8_dyn", "stokeslet", "tp", "", 2, 8, 30, 4000, "gated", 2, 0.03, 1e-8),
+]
+
+
+def dyn_strengths(case, rho):
+    ks = 1 if case[1] == "laplace" else 3
+    ncl, scale = case[9], case[11]
+    r = rho.reshape(-1, ks).copy()
+    member = np.arange(r.shape[0]) % ncl  # point i belongs to cluster i mod K
+    for k in range(ncl):
+        r[member == k] -= r[member == k].mean(axis=0)
+    r[member == 0] *= scale
+    return r.reshape(-1)
+
+
+def golden_eval_dyn(tmp):
+    golden_eval(tmp, [c[:11] + (c[11],) for c in EVAL_DYN], transform=dyn_strengths)
+
+
+def golden_eval_p10(tmp):
+    golden_eval(tmp, EVAL_P10)
 
 
 def golden_direct(tmp):
@@ -308,6 +346,8 @@ def main():
         golden_direct(tmp)
         golden_eval(tmp)
         golden_eval_adaptive(tmp)
+        golden_eval_p10(tmp)
+        golden_eval_dyn(tmp)
 
 
 if __name__ == "__main__":

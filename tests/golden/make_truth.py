@@ -22,7 +22,7 @@ REFDUMP = os.path.join(HERE, "..", "..", "oracle", "_ref", "refdump")
 # cases with a periodic truth evaluator: Laplace SP/DP/TP, Stokes TP
 # (Stokes DP has no K^P in the reference, src/refsum.cpp:620-622; cfg1 is SP-x)
 CASES = ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8", "lap_sp_p8_clu", "lap_dp_p6_clu",
-         "sto_tp_p6_clu"]
+         "sto_tp_p6_clu", "sto_tp_p10", "sto_tp_p10_clu"]
 
 
 def main():

@@ -58,11 +58,12 @@ def test_i8_gather_gemm_exact(Ki, nslots, ncols, nmod):
         assert np.abs(got[t]).max() <= 128 * nslots  # reduced per unit before the atomics
 
 
-@pytest.mark.parametrize("mode", [3, 4])
-def test_gather_gemm_exact_other_variants(mode):
-    """The exactness cases with every launch forced onto another kernel variant (3 dual tile,
-    4 dual tile + operator multicast); the variant is read once per process."""
-    env = dict(os.environ, PKGPU_I8_PAIR=str(mode))
+@pytest.mark.parametrize("kernel", ["dual", "pairdual"])
+def test_gather_gemm_exact_other_variants(kernel):
+    """The exactness cases with every launch forced onto another kernel variant
+    (PKGPU_I8_KERNEL: the dual-tile kernel; the pair-dual kernel wherever the columns form
+    whole 512-column quads); the variant is read once per process."""
+    env = dict(os.environ, PKGPU_I8_KERNEL=kernel)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__, "-k",
                         "test_i8_gather_gemm_exact"], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

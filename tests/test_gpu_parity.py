@@ -131,6 +131,8 @@ def test_lists_bit_exact(name, variant):
     ("c2", "uniform", 100000, 50, 3, {}, 0x6291641A7A150CB9),
     ("c3", "clusters", 1000000, 64, 3, dict(nclusters=8, sigma=0.04, periodic_axes=(True, True, False)),
      0x734159F57095BF50),
+    ("c4", "uniform", 8000000, 64, 1, {}, 0x04507BC8BCEB2641),
+    ("c5", "mixed", 32000000, 64, 3, dict(nclusters=64, sigma=0.02), 0x7908FA60CEF053F8),
 ])
 def test_structure_hash_at_baseline_sizes(cfg, kind, n, leaf, ks, kw, expect):
     """structure_hash of the BASELINE configs' trees, bit-exact."""
@@ -154,7 +156,9 @@ def test_tree_errors():
 EVAL_ALL = ["lap_none_p6", "lap_sp_p8", "lap_spx_p8", "lap_dp_p6", "lap_tp_p8", "lap_tp_p6_ell1", "sto_none_p6",
             "sto_tp_p6", "sto_tp_p8", "sto_dp_p6", "cfg1",
             # adaptive: clustered sources, depth 6-7 octrees with W and X lists (make_golden.py EVAL_ADAPTIVE)
-            "lap_none_p6_clu", "lap_sp_p8_clu", "lap_dp_p6_clu", "sto_tp_p6_clu"]
+            "lap_none_p6_clu", "lap_sp_p8_clu", "lap_dp_p6_clu", "sto_tp_p6_clu",
+            # p = 10 (K = 1464, the int8 Ki = 1536 tiling of BASELINE cfg3 / cfg5; make_golden.py EVAL_P10)
+            "sto_tp_p10", "sto_tp_p10_clu", "sto_dp_p10_clu"]
 
 
 def golden_request(g):

@@ -18,7 +18,7 @@ from test_gpu_parity import golden_request, load
 
 pytestmark = pytest.mark.gpu
 CASES = ["lap_sp_p8", "lap_dp_p6", "lap_tp_p8", "sto_tp_p6", "sto_tp_p8", "lap_sp_p8_clu", "lap_dp_p6_clu",
-         "sto_tp_p6_clu"]
+         "sto_tp_p6_clu", "sto_tp_p10", "sto_tp_p10_clu"]
 
 
 def truth_error(pot, truth, kt, tp):

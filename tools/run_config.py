@@ -5,9 +5,9 @@
 Inputs follow the SURVEY §8(d) protocol (pk.generate, mt19937_64 seed 12345). Operators:
   cfg1 Laplace SP-x p8  tests/golden/ops/laplace_spx_ell2_p8_spx.pkm2l (permuted SP-z, §8c)
   cfg2 Stokes TP p8     tests/golden/ops/stokeslet_tp_ell2_p8_gated.pkm2l
-  cfg3 Stokes DP p10    operators/stokeslet_tp_ell2_p10_gated.pkm2l relabelled DP (stand-in, §8c)
+  cfg3 Stokes DP p10    tests/golden/ops/stokeslet_tp_ell2_p10_gated.pkm2l relabelled DP (stand-in, §8c)
   cfg4 Laplace TP p8    tests/golden/ops/laplace_tp_ell2_p8_ungated.pkm2l (ungated, §8c)
-  cfg5 Stokes TP p10    operators/stokeslet_tp_ell2_p10_gated.pkm2l
+  cfg5 Stokes TP p10    tests/golden/ops/stokeslet_tp_ell2_p10_gated.pkm2l
 """
 import argparse
 import json
@@ -30,11 +30,11 @@ CONFIGS = {
     2: dict(kernel="stokeslet", per="tp", axes=None, n=100000, p=8, leaf=50, kind="uniform",
             op=os.path.join(G, "stokeslet_tp_ell2_p8_gated.pkm2l"), relabel=False),
     3: dict(kernel="stokeslet", per="dp", axes=None, n=1000000, p=10, leaf=64, kind="clusters", nclusters=8,
-            sigma=0.04, op=os.path.join(O, "stokeslet_tp_ell2_p10_gated.pkm2l"), relabel=True),
+            sigma=0.04, op=os.path.join(G, "stokeslet_tp_ell2_p10_gated.pkm2l"), relabel=True),
     4: dict(kernel="laplace", per="tp", axes=None, n=8000000, p=8, leaf=64, kind="uniform",
             op=os.path.join(G, "laplace_tp_ell2_p8_ungated.pkm2l"), relabel=False),
     5: dict(kernel="stokeslet", per="tp", axes=None, n=32000000, p=10, leaf=64, kind="mixed", nclusters=64,
-            sigma=0.02, op=os.path.join(O, "stokeslet_tp_ell2_p10_gated.pkm2l"), relabel=False),
+            sigma=0.02, op=os.path.join(G, "stokeslet_tp_ell2_p10_gated.pkm2l"), relabel=False),
 }
 
 
