@@ -153,8 +153,11 @@ def cpu_info():
 
 
 def reference_binary():
-    """refdump_native where it runs on this host, else the portable refdump."""
-    for b in (REFDUMP_NATIVE, REFDUMP):
+    """refdump_native where it runs on this host, else the portable refdump
+    (BENCH_REF_BINARY=refdump|refdump_native forces one, for comparisons)."""
+    force = os.environ.get("BENCH_REF_BINARY")
+    cands = [os.path.join(REPO, "oracle", "_ref", force)] if force else [REFDUMP_NATIVE, REFDUMP]
+    for b in cands:
         if os.path.exists(b):
             r = subprocess.run([b], capture_output=True, text=True)
             if "usage" in (r.stderr + r.stdout):

@@ -74,6 +74,7 @@ struct Params {
     int nmat, nmod, KC, Nt, rowtiles, coltiles, nchunk, total_units, ncols, Ki;
     uint32_t idesc;
     int nst, stage_bytes; // single-CTA kernel: stage ring depth and stride
+    int tile_fast;        // unit order: column tile fastest (decode_unit)
     int epi_transpose;    // epilogue atomics through a shared-memory transpose (coalesced)
     int *R; // [nmod][ncols][Ki]
 };
@@ -139,18 +140,34 @@ __device__ __forceinline__ void chunk_range(const Params &p, int tile, int chunk
     }
 }
 
+// unit index -> (modulus t, operator row tile rt, column tile ct, chunk). Default order:
+// row tile fastest (concurrent units share their gathered rows); tile_fast: column tile
+// fastest (the concurrent units of one (t, rt, chunk) walk the same operator tiles --
+// with slot-index chunks, one DRAM read of each tile serves them all through L2)
+__device__ __forceinline__ void decode_unit(const Params &p, int u, int ntiles, int &t, int &rt, int &ct, int &chunk) {
+    if (p.tile_fast) {
+        ct = u % ntiles;
+        u /= ntiles;
+        rt = u % p.rowtiles;
+        u /= p.rowtiles;
+    } else {
+        rt = u % p.rowtiles;
+        u /= p.rowtiles;
+        ct = u % ntiles;
+        u /= ntiles;
+    }
+    chunk = u % p.nchunk;
+    t = u / p.nchunk;
+}
+
 struct Unit {
     int t, rt, ct, s0, s1;
 };
 __device__ __forceinline__ Unit decode(const Params &p, int u) {
     // row tile fastest: consecutive units (running concurrently) share their gathered rows
     Unit x;
-    x.rt = u % p.rowtiles;
-    u /= p.rowtiles;
-    x.ct = u % p.coltiles;
-    u /= p.coltiles;
-    const int chunk = u % p.nchunk;
-    x.t = u / p.nchunk;
+    int chunk;
+    decode_unit(p, u, p.coltiles, x.t, x.rt, x.ct, chunk);
     chunk_range(p, x.ct, chunk, x.s0, x.s1);
     return x;
 }
@@ -379,13 +396,8 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
     int g = 0, jb = 0;
     const int npairs = p.coltiles / 2;
     for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
-        int v = u;
-        const int rt = v % p.rowtiles;
-        v /= p.rowtiles;
-        const int pr = v % npairs;
-        v /= npairs;
-        const int chunk = v % p.nchunk;
-        const int t = v / p.nchunk;
+        int t, rt, pr, chunk;
+        decode_unit(p, u, npairs, t, rt, pr, chunk);
         int s0, s1;
         chunk_range(p, pr, chunk, s0, s1);
         const int n = (s1 - s0) * p.KC;
@@ -613,13 +625,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
     int g = 0, jb = 0;
     const int nquads = p.coltiles / 4;
     for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
-        int v = u;
-        const int rt = v % p.rowtiles;
-        v /= p.rowtiles;
-        const int qd = v % nquads;
-        v /= nquads;
-        const int chunk = v % p.nchunk;
-        const int t = v / p.nchunk;
+        int t, rt, qd, chunk;
+        decode_unit(p, u, nquads, t, rt, qd, chunk);
         int s0, s1;
         chunk_range(p, qd, chunk, s0, s1);
         const int n = (s1 - s0) * p.KC;
@@ -1292,7 +1299,13 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     p.tile_partial = thmask ? reinterpret_cast<const int *>(thmask + partial_offset(ncols / column_tile(kind))) : nullptr;
     // slot-index windows for the single-CTA kernel (operator reuse through L2 across its
     // tiles); equal list shares for the dual-tile kernels (balanced static schedule)
-    p.by_index = masked(kind) ? 0 : 1;
+    const Tuning &tu = tuning();
+    p.by_index = tu.i8_by_index >= 0 ? tu.i8_by_index : (masked(kind) ? 0 : 1);
+    p.tile_fast = tu.i8_tile_fast >= 0 ? tu.i8_tile_fast : 0;
+    if (tu.i8_min_chunks > nchunk) {
+        p.nchunk = nchunk = tu.i8_min_chunks;
+        p.total_units = (int)(base * nchunk);
+    }
     const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
     const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
     // the CTA-pair kernel stages half of the operator tile per CTA

@@ -115,9 +115,42 @@ struct LeafParams {
     double *out;
 };
 
-template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafParams P) {
+// TT targets per thread (register tile: one shared-memory source read feeds TT independent
+// pair chains); the lane takes sources j, j + G, ... of every staged segment
+template <int KERNEL, int TT>
+__device__ __forceinline__ void accumulate_tt(const Stage<KERNEL> &S, const double (&tx)[TT], const double (&ty)[TT],
+                                              const double (&tz)[TT], int j, int G, double (&acc)[TT][3]) {
+    for (int s = 0; s < S.nseg; s++) {
+        double ux[TT], uy[TT], uz[TT];
+#pragma unroll
+        for (int k = 0; k < TT; k++) ux[k] = tx[k] - S.sx[s], uy[k] = ty[k] - S.sy[s], uz[k] = tz[k] - S.sz[s];
+        const int end = S.begin[s + 1];
+#pragma unroll 2
+        for (int q = S.begin[s] + j; q < end; q += G) {
+            const double sx = S.x[q], sy = S.y[q], sz = S.z[q];
+#pragma unroll
+            for (int k = 0; k < TT; k++) {
+                if (KERNEL == 0)
+                    pair_laplace(ux[k], uy[k], uz[k], sx, sy, sz, S.d[q], acc[k][0]);
+                else
+                    pair_stokes(ux[k], uy[k], uz[k], sx, sy, sz, S.d[3 * q], S.d[3 * q + 1], S.d[3 * q + 2], acc[k][0],
+                                acc[k][1], acc[k][2]);
+            }
+        }
+    }
+}
+
+// Leaf pass: one CTA per target leaf; targets in groups of TT, G = NT / groups lanes per
+// group (any G, so no lane idles for want of a power of two); sources staged in shared
+// memory per batch of segments; the G partial sums of a group are reduced in a fixed order
+// through shared memory (deterministic, each target written once).
+template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, 5) leaf_kernel(LeafParams P) {
     constexpr int KS = Stage<KERNEL>::KS;
-    __shared__ Stage<KERNEL> S;
+    __shared__ union {
+        Stage<KERNEL> S;
+        double red[NT][TT][KS];
+    } sm;
+    Stage<KERNEL> &S = sm.S;
     __shared__ int s_uc[MAXU], s_ucode[MAXU], s_ub[MAXU], s_ue[MAXU];
     __shared__ int s_segsrc[MAXSEG];
     __shared__ int s_pos, s_off;
@@ -129,18 +162,21 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
     double cx, cy, cz;
     box_center(bc, cx, cy, cz);
     const double scale = ldexp(1.0, bc.w);
-    const int G = lanes_per_target(ntg);
-    const int TPC = NT / G;
+    const int ngroups = (ntg + TT - 1) / TT;
+    const int G = max(1, min(32, NT / ngroups));
+    const int gpc = NT / G; // groups per pass
     const int tid = threadIdx.x, j = tid % G;
-    for (int t0 = 0; t0 < ntg; t0 += TPC) {
-        const int t = t0 + tid / G;
-        const bool active = t < ntg;
-        double tx = 0, ty = 0, tz = 0;
-        if (active) {
-            const double4 p = P.trg_pos[tr.x + t];
-            tx = p.x, ty = p.y, tz = p.z;
+    for (int g0 = 0; g0 < ngroups; g0 += gpc) {
+        const int grp = g0 + tid / G;
+        const bool active = tid / G < gpc && grp < ngroups;
+        double tx[TT], ty[TT], tz[TT], acc[TT][3];
+#pragma unroll
+        for (int k = 0; k < TT; k++) {
+            const int t = min(grp * TT + k, ntg - 1); // a missing target repeats the last one (not written)
+            const double4 p = P.trg_pos[tr.x + (active ? t : 0)];
+            tx[k] = p.x, ty[k] = p.y, tz[k] = p.z;
+            acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
         }
-        double acc[3] = {0.0, 0.0, 0.0};
         // L2T: outer (downward equivalent) surface of b, density phi_dn[b]
         {
             const double half = 0.5 * (kOuter / scale);
@@ -149,7 +185,7 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
                 stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), cx, cy, cz, half,
                                       P.phi_dn + (int64_t)b * P.Kp, 0.0, 0.0, 0.0);
                 __syncthreads();
-                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+                if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
             }
         }
         // W: inner (upward equivalent) surfaces of finer well-separated boxes
@@ -165,7 +201,7 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
                 stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), ccx, ccy, ccz, half,
                                       P.phi_up + (int64_t)en.x * P.Kp, shx, shy, shz);
                 __syncthreads();
-                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+                if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
             }
         }
         // U: adjacent source leaves, packed into batches of segments
@@ -178,12 +214,11 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
                 const int2 r = P.T.srng[en.x];
                 s_uc[k] = en.x, s_ucode[k] = en.y, s_ub[k] = r.x, s_ue[k] = r.y;
             }
+            __syncthreads();
             if (tid == 0) {
                 s_pos = 0;
-                s_off = ne > 0 ? 0 : 0;
+                s_off = ne > 0 ? s_ub[0] : 0;
             }
-            __syncthreads();
-            if (tid == 0 && ne > 0) s_off = s_ub[0];
             __syncthreads();
             while (s_pos < ne) {
                 if (tid == 0) {
@@ -215,7 +250,7 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
                     for (int q = tid; q < len; q += NT) stage_point<KERNEL>(S, beg + q, P.src_pos, P.src_f, src0 + q);
                 }
                 __syncthreads();
-                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+                if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
                 __syncthreads();
             }
         }
@@ -228,17 +263,29 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) leaf_kernel(LeafPara
                 stage_surface<KERNEL>(S, P.tmpl, i0, min(SB, P.n - i0), 0.5, 0.5, 0.5, half, P.phi_far, 0.0, 0.0,
                                       0.0);
                 __syncthreads();
-                if (active) accumulate<KERNEL>(S, tx, ty, tz, j, G, acc, nullptr);
+                if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
             }
         }
-        // combine the G lanes of each target
-        for (int o = G / 2; o > 0; o >>= 1)
+        // combine the G lanes of each group in a fixed order
+        __syncthreads();
 #pragma unroll
-            for (int a = 0; a < KS; a++) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
+        for (int k = 0; k < TT; k++)
+#pragma unroll
+            for (int a = 0; a < KS; a++) sm.red[tid][k][a] = acc[k][a];
+        __syncthreads();
         if (active && j == 0) {
-            const int64_t orig = P.trg_perm[tr.x + t];
 #pragma unroll
-            for (int a = 0; a < KS; a++) P.out[orig * KS + a] = KERNEL == 0 ? acc[a] : kOneOver8Pi * acc[a];
+            for (int k = 0; k < TT; k++) {
+                const int t = grp * TT + k;
+                if (t >= ntg) continue;
+                const int64_t orig = P.trg_perm[tr.x + t];
+#pragma unroll
+                for (int a = 0; a < KS; a++) {
+                    double v = 0.0;
+                    for (int l = 0; l < G; l++) v += sm.red[tid + l][k][a];
+                    P.out[orig * KS + a] = KERNEL == 0 ? v : kOneOver8Pi * v;
+                }
+            }
         }
     }
 }
@@ -444,9 +491,9 @@ void leaf_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, con
     LeafParams P{T.view(), g.n,         g.Kp,       g.tmpl,   T.src_pos, T.src_f, T.trg_pos, T.trg_perm, leaves,
                  L.u.off,  L.w.off,     L.u.ent,    L.w.ent,  phi_dn,    phi_up,  phi_far,   out};
     if (g.kernel == 0)
-        leaf_kernel<0><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        leaf_kernel<0, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
     else
-        leaf_kernel<1><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        leaf_kernel<1, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
     PK_CUDA(cudaGetLastError());
 }
 

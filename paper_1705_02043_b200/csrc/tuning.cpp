@@ -32,6 +32,9 @@ const Tuning &tuning() {
             else if (!std::strcmp(e, "dual")) r.i8_kernel = I8Kernel::dual;
             else if (!std::strcmp(e, "pairdual")) r.i8_kernel = I8Kernel::pairdual;
         }
+        r.i8_by_index = (int)env_int("PKGPU_I8_BYINDEX", r.i8_by_index, -1);
+        r.i8_tile_fast = (int)env_int("PKGPU_I8_TILEFAST", r.i8_tile_fast, -1);
+        r.i8_min_chunks = (int)env_int("PKGPU_I8_CHUNKS", r.i8_min_chunks, 0);
         r.gemm_units_per_cta = env_int("PKGPU_GEMM_UNITS", r.gemm_units_per_cta, 1);
         r.gemm_min_iters = env_int("PKGPU_GEMM_MINIT", r.gemm_min_iters, 1);
         r.gemm_min_iters_small = env_int("PKGPU_GEMM_MINIT_SMALL", r.gemm_min_iters_small, 1);

@@ -6,8 +6,12 @@
 // reference's fmm.o (whose evaluate symbol is weakened) makes every existing caller —
 // tools/pkifmm.cpp cmd_eval, src/experiments.cpp — run the GPU path unchanged.
 // Exceptions are rethrown with the reference's classes and messages.
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -17,17 +21,82 @@
 
 namespace {
 
-pkgpu_context *context() {
-    static std::once_flag once;
-    static pkgpu_context *ctx = nullptr;
-    std::call_once(once, [] {
+// ---- contexts: one per concurrently calling thread ----
+// The reference's evaluate is reentrant (per-call FmmTree, mutex-guarded static caches,
+// src/fmm.cpp:243-268). Here each call borrows a context from a pool -- its own CUDA stream
+// and workspaces -- so concurrent callers run concurrently on the device; a context is
+// created when every pooled one is busy and returned to the pool when the call ends.
+struct ContextPool {
+    std::mutex mtx;
+    std::vector<pkgpu_context *> free;
+    int device = 0;
+    ContextPool() {
+        if (const char *e = std::getenv("PKGPU_DEVICE")) device = std::atoi(e);
+    }
+    pkgpu_context *acquire() {
+        {
+            std::lock_guard<std::mutex> lk(mtx);
+            if (!free.empty()) {
+                pkgpu_context *c = free.back();
+                free.pop_back();
+                return c;
+            }
+        }
         char err[512];
-        int dev = 0;
-        if (const char *e = std::getenv("PKGPU_DEVICE")) dev = std::atoi(e);
-        if (pkgpu_context_create(dev, &ctx, err, sizeof err) != PKGPU_OK)
+        pkgpu_context *c = nullptr;
+        if (pkgpu_context_create(device, &c, err, sizeof err) != PKGPU_OK)
             throw std::runtime_error(std::string("pkgpu: ") + err);
-    });
-    return ctx;
+        return c;
+    }
+    void release(pkgpu_context *c) {
+        std::lock_guard<std::mutex> lk(mtx);
+        free.push_back(c);
+    }
+};
+ContextPool &pool() {
+    static ContextPool p;
+    return p;
+}
+struct ContextLease {
+    pkgpu_context *ctx;
+    ContextLease() : ctx(pool().acquire()) {}
+    ~ContextLease() { pool().release(ctx); }
+};
+
+// ---- periodizing operators: device-resident across calls ----
+// The caller's PeriodizingOperator is borrowed per call (include/pkifmm/fmm.hpp:120-131).
+// Its matrix is identified by a 64-bit content hash (plus provenance and size), so repeated
+// evaluates with the same operator reuse one pkgpu_operator -- and its device copy -- instead
+// of uploading T_M2L every call (the reference's static caches, src/fmm.cpp:238-283). The
+// hash reads the matrix once per call (~0.5 ms for the 6.3 MB Stokes p = 8 operator), so an
+// operator edited in place is still picked up. Small LRU, like the reference's.
+uint64_t content_hash(const double *d, size_t n) {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ n;
+    const auto *w = reinterpret_cast<const uint64_t *>(d);
+    for (size_t i = 0; i < n; i++) {
+        uint64_t x = w[i] + 0x9E3779B97F4A7C15ull * (i + 1);
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        h = (h ^ (x >> 31) ^ x) * 0x100000001B3ull;
+    }
+    return h;
+}
+
+struct OperatorCache {
+    struct Entry {
+        uint64_t key;
+        pkgpu_operator *op;
+    };
+    std::mutex mtx;
+    std::vector<Entry> lru; // most recent last
+    static constexpr size_t kCapacity = 4;
+    ~OperatorCache() {
+        for (auto &e : lru) pkgpu_operator_free(e.op);
+    }
+};
+OperatorCache &op_cache() {
+    static OperatorCache c;
+    return c;
 }
 
 pkgpu_setup to_setup(const pkifmm::PeriodicSetup &s) {
@@ -59,14 +128,32 @@ EvalResult evaluate(const EvalRequest &request) {
     if (request.op) {
         const PeriodizingOperator &p = *request.op;
         const pkgpu_setup s = to_setup(p.setup);
-        const pkgpu_status st = pkgpu_operator_create(static_cast<int>(p.kernel.type), &s, p.p, p.matrix.data.data(),
-                                                      p.matrix.rows, &op, err, sizeof err);
-        if (st != PKGPU_OK) rethrow(st, err);
+        uint64_t key = content_hash(p.matrix.data.data(), p.matrix.data.size());
+        key = (key ^ static_cast<uint64_t>(p.kernel.type)) * 0x100000001B3ull ^ static_cast<uint64_t>(p.p);
+        key = (key ^ static_cast<uint64_t>(s.periodicity * 64 + s.axes[0] * 4 + s.axes[1] * 2 + s.axes[2])) *
+              0x100000001B3ull ^ static_cast<uint64_t>(s.ell);
+        OperatorCache &cache = op_cache();
+        std::lock_guard<std::mutex> lk(cache.mtx);
+        for (size_t i = 0; i < cache.lru.size(); i++)
+            if (cache.lru[i].key == key) {
+                op = cache.lru[i].op;
+                std::rotate(cache.lru.begin() + i, cache.lru.begin() + i + 1, cache.lru.end());
+                break;
+            }
+        if (!op) {
+            const pkgpu_status st = pkgpu_operator_create(static_cast<int>(p.kernel.type), &s, p.p,
+                                                          p.matrix.data.data(), p.matrix.rows, &op, err, sizeof err);
+            if (st != PKGPU_OK) rethrow(st, err);
+            if (cache.lru.size() == OperatorCache::kCapacity) {
+                // the evicted operator may still be in use by a concurrent call: keep it alive
+                // until process exit rather than free it under that call
+                static std::vector<pkgpu_operator *> retired;
+                retired.push_back(cache.lru.front().op);
+                cache.lru.erase(cache.lru.begin());
+            }
+            cache.lru.push_back({key, op});
+        }
     }
-    struct OpGuard {
-        pkgpu_operator *p;
-        ~OpGuard() { pkgpu_operator_free(p); }
-    } guard{op};
 
     pkgpu_request r{};
     r.kernel = static_cast<int>(kernel.type);
@@ -88,7 +175,8 @@ EvalResult evaluate(const EvalRequest &request) {
     result.potentials.assign(static_cast<size_t>(kernel.kt) * request.targets.size(), 0.0);
     pkgpu_timings tm{};
     pkgpu_compat cp{};
-    const pkgpu_status st = pkgpu_evaluate(context(), &r, result.potentials.data(), &tm, &cp, err, sizeof err);
+    ContextLease lease;
+    const pkgpu_status st = pkgpu_evaluate(lease.ctx, &r, result.potentials.data(), &tm, &cp, err, sizeof err);
     if (st != PKGPU_OK) rethrow(st, err);
     result.timings.tree = tm.tree;
     result.timings.near = tm.near;
@@ -110,8 +198,9 @@ PeriodizingOperator solve_on_gpu(const PeriodicKernelSpec &spec, int p) {
     const pkgpu_ewald e{spec.params.xi, spec.params.real_shells, spec.params.wave_cutoff, spec.params.n_images};
     pkgpu_operator *op = nullptr;
     char err[2048] = {0};
+    ContextLease lease;
     const pkgpu_status st =
-        pkgpu_operator_solve(context(), static_cast<int>(spec.kernel.type), &s, p, &e, 1, &op, err, sizeof err);
+        pkgpu_operator_solve(lease.ctx, static_cast<int>(spec.kernel.type), &s, p, &e, 1, &op, err, sizeof err);
     if (st != PKGPU_OK) rethrow(st, err);
     int64_t dim = 0;
     double residual = 0.0;
