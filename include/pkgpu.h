@@ -126,22 +126,40 @@ pkgpu_status pkgpu_evaluate(pkgpu_context *ctx, const pkgpu_request *req, double
 /* ---- multi-GPU: Morton-range partition ---------------------------- */
 /* Every rank receives the full request (inputs replicated, so the near-field source halo
  * is implicit) and builds the same tree. Rank r owns a contiguous Morton range of leaves
- * (its targets). It runs the upward pass over its own leaves only; because the upward
- * chain is linear in the sources, the complete equivalent densities (root density
- * included) are the SUM over ranks, exchanged with one allreduce. The downward pass and
- * the leaf pass then run for the boxes intersecting the rank's range; the outputs
- * (each target written by exactly one rank, zeros elsewhere) are summed by a second
- * allreduce so every rank returns the full potentials.
- *   alloc     : device memory the collective can operate on (e.g. a torch tensor)
- *   allreduce : in-place elementwise sum over ranks of count doubles; the work stream
- *               is synchronised before the call and must be safe to use after return. */
+ * (equal leaf counts; its targets). The upward pass runs over the rank's own leaves; a box
+ * whose leaves all belong to one rank (its owner) is then complete there, a box spanning
+ * several ranks (a "straddler": the ancestors of the range boundaries, root included) holds
+ * a partial sum on each -- the upward chain is linear in the sources.
+ * Equivalent-density exchange (with `alltoallv`): one allreduce over the straddlers only,
+ * then a halo exchange -- every rank receives, from their owners, the densities of the V-
+ * and W-list sources of its own target boxes (need masks from the replicated tree). Without
+ * `alltoallv` (NULL): one allreduce of all boxes' densities (round 1's scheme).
+ * The small-level int8 M2L run (levels streamed as one launch) is split by modulus when
+ * `allgather` is given: each rank computes ceil(nmod / R) moduli of the residue sums for all
+ * of the run's columns, gathered before the CRT rebuild.
+ * The downward and leaf passes run for the boxes meeting the rank's range; the outputs
+ * (each target written by one rank, zeros elsewhere) are summed by a final allreduce so
+ * every rank returns the full potentials.
+ *   alloc     : device memory the collectives can operate on (e.g. a torch tensor)
+ *   allreduce : in-place elementwise sum over ranks of count doubles
+ *   alltoallv : send[...] holds nranks consecutive blocks (send_counts[q] doubles for rank q,
+ *               q = rank included, count 0); recv receives recv_counts[q] doubles from each q
+ *   allgather : buf holds nranks blocks of bytes_per_rank; block `rank` is filled, all are
+ *               filled on return
+ * The work stream is synchronised before each callback, which must complete (or order its
+ * work before any later use of the buffers) before returning. */
 typedef void *(*pkgpu_alloc_fn)(void *user, size_t bytes);
 typedef int (*pkgpu_allreduce_fn)(void *user, double *device_buf, int64_t count, void *stream);
+typedef int (*pkgpu_alltoallv_fn)(void *user, const double *send, const int64_t *send_counts, double *recv,
+                                  const int64_t *recv_counts, void *stream);
+typedef int (*pkgpu_allgather_fn)(void *user, void *device_buf, int64_t bytes_per_rank, void *stream);
 typedef struct {
     int rank, nranks;
     pkgpu_alloc_fn alloc;
     pkgpu_allreduce_fn allreduce;
     void *user;
+    pkgpu_alltoallv_fn alltoallv; /* optional */
+    pkgpu_allgather_fn allgather; /* optional */
 } pkgpu_partition;
 
 pkgpu_status pkgpu_evaluate_partitioned(pkgpu_context *ctx, const pkgpu_request *req, const pkgpu_partition *part,

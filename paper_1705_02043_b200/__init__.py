@@ -59,11 +59,17 @@ class _Request(ctypes.Structure):
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
 _ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+_ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                 ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
+_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
 
 
 class _Partition(ctypes.Structure):
+    """pkgpu_partition (include/pkgpu.h): rank, nranks, alloc, allreduce, user, and the
+    optional alltoallv (halo exchange) and allgather (small-level int8 run by modulus)."""
     _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("alloc", _ALLOC_FN),
-                ("allreduce", _ALLREDUCE_FN), ("user", ctypes.c_void_p)]
+                ("allreduce", _ALLREDUCE_FN), ("user", ctypes.c_void_p), ("alltoallv", _ALLTOALLV_FN),
+                ("allgather", _ALLGATHER_FN)]
 
 
 class _Timings(ctypes.Structure):
@@ -586,7 +592,8 @@ def evaluate(request: EvalRequest, context: Optional[Context] = None, out=None, 
     tm, cp, err = _Timings(), _Compat(), _errbuf()
     if comm is not None and comm.nranks > 1:
         comm.begin_call()
-        part = _Partition(comm.rank, comm.nranks, comm.c_alloc, comm.c_allreduce, None)
+        part = _Partition(comm.rank, comm.nranks, comm.c_alloc, comm.c_allreduce, None, comm.c_alltoallv,
+                          comm.c_allgather)
         try:
             st = lib().pkgpu_evaluate_partitioned(ctx._h, ctypes.byref(r), ctypes.byref(part), ctypes.c_void_p(optr),
                                                   ctypes.byref(tm), ctypes.byref(cp), err, 1024)
@@ -615,10 +622,21 @@ class _CommBase:
         self.error = None
         self.c_alloc = _ALLOC_FN(self._alloc)
         self.c_allreduce = _ALLREDUCE_FN(self._allreduce)
+        # the halo / modulus-split collectives; set_v1() reverts to round 1's single allreduce
+        self.c_alltoallv = _ALLTOALLV_FN(self._alltoallv)
+        self.c_allgather = _ALLGATHER_FN(self._allgather)
+        self.moved = 0  # doubles this rank received through the collectives (last call)
+
+    def set_v1(self):
+        """Exchange every box's equivalent density with one allreduce (no halo exchange,
+        no modulus split): the library falls back when the optional callbacks are NULL."""
+        self.c_alltoallv = _ALLTOALLV_FN()
+        self.c_allgather = _ALLGATHER_FN()
 
     def begin_call(self):
         self._bufs.clear()
         self.error = None
+        self.moved = 0
 
     def end_call(self):
         self._bufs.clear()
@@ -634,15 +652,52 @@ class _CommBase:
             self.error = e
             return None
 
+    def _find(self, ptr, count):
+        """The allocated tensor holding [ptr, ptr + count doubles) as a view."""
+        for base, t in self._bufs.items():
+            if base <= ptr and ptr + 8 * count <= base + 8 * t.numel():
+                o = (ptr - base) // 8
+                return t[o:o + count]
+        raise KeyError("pkgpu: collective on memory not from the alloc callback")
+
     def _allreduce(self, user, ptr, count, stream):
         try:
-            self.allreduce(self._bufs[ptr][:count])
+            self.allreduce(self._find(ptr, count))
+            self.moved += count
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+    def _alltoallv(self, user, sptr, scounts, rptr, rcounts, stream):
+        try:
+            sc = [int(scounts[q]) for q in range(self.nranks)]
+            rc = [int(rcounts[q]) for q in range(self.nranks)]
+            self.alltoallv(self._find(sptr, max(1, sum(sc)))[:sum(sc)], sc, self._find(rptr, max(1, sum(rc)))[:sum(rc)],
+                           rc)
+            self.moved += sum(rc)
+            return 0
+        except Exception as e:
+            self.error = e
+            return 1
+
+    def _allgather(self, user, ptr, nbytes, stream):
+        try:
+            n = (nbytes + 7) // 8
+            self.allgather(self._find(ptr, n * self.nranks), n)
+            self.moved += n * (self.nranks - 1)
             return 0
         except Exception as e:
             self.error = e
             return 1
 
     def allreduce(self, t):
+        raise NotImplementedError
+
+    def alltoallv(self, send, send_counts, recv, recv_counts):
+        raise NotImplementedError
+
+    def allgather(self, buf, n):
         raise NotImplementedError
 
 
@@ -661,6 +716,22 @@ class TorchDistComm(_CommBase):
         dist.all_reduce(t, group=self.group)
         if t.is_cuda:
             torch.cuda.synchronize(t.device)
+
+    def alltoallv(self, send, send_counts, recv, recv_counts):
+        import torch
+        import torch.distributed as dist
+        dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                               group=self.group)
+        if recv.is_cuda:
+            torch.cuda.synchronize(recv.device)
+
+    def allgather(self, buf, n):
+        import torch
+        import torch.distributed as dist
+        mine = buf[self.rank * n:(self.rank + 1) * n].clone()
+        dist.all_gather_into_tensor(buf, mine, group=self.group)
+        if buf.is_cuda:
+            torch.cuda.synchronize(buf.device)
 
 
 class ThreadComm:
@@ -691,6 +762,32 @@ class ThreadComm:
                     torch.cuda.synchronize()
                 outer.barrier.wait()
                 t.copy_(outer.result)
+                torch.cuda.synchronize()
+                outer.barrier.wait()
+
+            def alltoallv(self, send, send_counts, recv, recv_counts):
+                import torch
+                torch.cuda.synchronize()
+                outer.slots[r] = (send, send_counts)
+                outer.barrier.wait()
+                o = 0
+                for q in range(outer.nranks):
+                    s_q, c_q = outer.slots[q]
+                    off = sum(c_q[:r])
+                    assert c_q[r] == recv_counts[q]
+                    recv[o:o + recv_counts[q]].copy_(s_q[off:off + c_q[r]])
+                    o += recv_counts[q]
+                torch.cuda.synchronize()
+                outer.barrier.wait()
+
+            def allgather(self, buf, n):
+                import torch
+                torch.cuda.synchronize()
+                outer.slots[r] = buf
+                outer.barrier.wait()
+                for q in range(outer.nranks):
+                    if q != r:
+                        buf[q * n:(q + 1) * n].copy_(outer.slots[q][q * n:(q + 1) * n])
                 torch.cuda.synchronize()
                 outer.barrier.wait()
 

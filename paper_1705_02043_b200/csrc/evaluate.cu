@@ -109,7 +109,7 @@ __global__ void leaf_key_kernel(TreeView T, const int *__restrict__ leaves, int 
 
 // box -> does its DFS leaf interval meet [lo, hi)?  own[b]: leaf owned by this rank
 __global__ void part_mask_kernel(TreeView T, const unsigned long long *__restrict__ lkeys, int nleaves, int lo, int hi,
-                                 int *in, int *own) {
+                                 int nranks, int *in, int *own, int *rlo, int *rhi) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= T.nboxes) return;
     const int sh = 3 * (kMaxDepth - T.cell[b].w);
@@ -132,6 +132,54 @@ __global__ void part_mask_kernel(TreeView T, const unsigned long long *__restric
     }
     in[b] = (a < hi && c > lo) ? 1 : 0;
     own[b] = (T.isleaf[b] && a >= lo && a < hi) ? 1 : 0;
+    // ranks of the box's first and last leaf: rank(i) = ceil((i + 1) R / L) - 1 for the
+    // equal split lo_r = floor(L r / R)
+    auto rank_of = [&](int i) { return (int)((((int64_t)i + 1) * nranks + nleaves - 1) / nleaves) - 1; };
+    rlo[b] = rank_of(min(a, nleaves - 1));
+    rhi[b] = rank_of(max(a, c - 1));
+}
+
+// boxes of the small levels (the packed int8 run) join every rank's mask when that run is
+// split by modulus: all ranks then lay out and compute the same columns
+__global__ void small_or_kernel(TreeView T, const int *__restrict__ in, int64_t small_max, int *out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int l = T.cell[b].w;
+    out[b] = in[b] || (l >= 1 && T.level_off[l + 1] - T.level_off[l] <= small_max);
+}
+__global__ void need_small_kernel(TreeView T, int64_t small_max, unsigned long long all, unsigned long long *need) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int l = T.cell[b].w;
+    if (l >= 1 && T.level_off[l + 1] - T.level_off[l] <= small_max) need[b] |= all;
+}
+
+// ---- equivalent-density exchange of the partitioned run ----
+__global__ void strad_flags_kernel(const int *__restrict__ rlo, const int *__restrict__ rhi, int n, int *flags) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < n) flags[b] = rlo[b] != rhi[b];
+}
+// send (dir 0): boxes this rank owns that rank q needs; recv (dir 1): boxes rank q owns that this rank needs
+__global__ void halo_flags_kernel(const int *__restrict__ rlo, const int *__restrict__ rhi,
+                                  const unsigned long long *__restrict__ need, int n, int me, int q, int dir,
+                                  int *flags) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const int o = rlo[b];
+    const bool single = o == rhi[b];
+    flags[b] = dir == 0 ? (single && o == me && ((need[b] >> q) & 1ull)) : (single && o == q && ((need[b] >> me) & 1ull));
+}
+__global__ void rows_pack_kernel(const double *__restrict__ X, const int *__restrict__ list, int n, int Kp,
+                                 double *__restrict__ buf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * Kp) return;
+    buf[i] = X[(int64_t)list[i / Kp] * Kp + i % Kp];
+}
+__global__ void rows_unpack_kernel(const double *__restrict__ buf, const int *__restrict__ list, int n, int Kp,
+                                   double *__restrict__ X) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)n * Kp) return;
+    X[(int64_t)list[i / Kp] * Kp + i % Kp] = buf[i];
 }
 
 __global__ void flags_by_level_kernel(TreeView T, const int *__restrict__ mask, int *level_count) {
@@ -489,6 +537,7 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
 struct Partition {
     bool on = false;
     int *in = nullptr, *own = nullptr;
+    int *rlo = nullptr, *rhi = nullptr; // ranks of each box's first and last leaf
     int *act = nullptr;
     std::vector<int64_t> actbase; // per level column base into act
     int *leaves = nullptr;
@@ -520,7 +569,9 @@ Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int
     const int lo = (int)((int64_t)nl * rank / nranks), hi = (int)((int64_t)nl * (rank + 1) / nranks);
     P.in = ws.get<int>("pt_in", nb);
     P.own = ws.get<int>("pt_own", nb);
-    part_mask_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, k_out, nl, lo, hi, P.in, P.own);
+    P.rlo = ws.get<int>("pt_rlo", nb);
+    P.rhi = ws.get<int>("pt_rhi", nb);
+    part_mask_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, k_out, nl, lo, hi, nranks, P.in, P.own, P.rlo, P.rhi);
     // owned leaves
     P.leaves = ws.get<int>("pt_leaves", std::max(nl, 1));
     int *cnt = ws.get<int>("pt_cnt", 2);
@@ -558,6 +609,86 @@ Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int
     ctx.launches += 6;
     PK_CUDA(cudaStreamSynchronize(st));
     return P;
+}
+
+// Equivalent-density exchange after the upward pass (pkgpu_partition, include/pkgpu.h):
+// straddling boxes summed by one allreduce, then the halo -- each rank receives from their
+// owners the densities of the V / W sources of its own target boxes (alltoallv). Returns
+// the doubles this rank received (the bytes-moved statistic of the stage profiler).
+int64_t exchange_up(pkgpu_context &ctx, const DeviceTree &T, const Partition &P, const ListSetup &ls, double *Pup,
+                    int Kp, const pkgpu_partition *part, int64_t small_all, cudaStream_t st) {
+    Workspace &ws = ctx.ws;
+    const int nb = (int)T.nboxes, R = part->nranks, me = part->rank;
+    if (R > 64) throw InvalidArgument("evaluate_partitioned: at most 64 ranks");
+    int *flags = ws.get<int>("ex_flags", nb), *cnt = ws.get<int>("ex_cnt", 2 * R + 1);
+    int64_t moved = 0;
+    // 1. straddlers (identical list on every rank)
+    int *slist = ws.get<int>("ex_slist", nb);
+    strad_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(P.rlo, P.rhi, nb, flags);
+    compact(ctx, flags, nb, slist, cnt + 2 * R, "exs", st);
+    // 2. who needs what, from the replicated tree
+    unsigned long long *need = ws.get<unsigned long long>("ex_need", nb);
+    need_masks(T, ls, P.rlo, P.rhi, need, st);
+    if (small_all > 0) // modulus-split small-level run: every rank computes every small-level column
+        need_small_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(T.view(), small_all,
+                                                                R == 64 ? ~0ull : (1ull << R) - 1ull, need);
+    std::vector<int *> lists(2 * R, nullptr);
+    for (int q = 0; q < R; q++)
+        for (int dir = 0; dir < 2; dir++) {
+            int *l = lists[2 * q + dir] = ws.get<int>("ex_l" + std::to_string(2 * q + dir), nb);
+            if (q == me) {
+                PK_CUDA(cudaMemsetAsync(cnt + 2 * q + dir, 0, sizeof(int), st));
+                continue;
+            }
+            halo_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(P.rlo, P.rhi, need, nb, me, q, dir, flags);
+            compact(ctx, flags, nb, l, cnt + 2 * q + dir, ("exh" + std::to_string(2 * q + dir)).c_str(), st);
+        }
+    ctx.launches += 2 + 2 * (R - 1);
+    std::vector<int> h(2 * R + 1);
+    PK_CUDA(cudaMemcpyAsync(h.data(), cnt, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    const int ns = h[2 * R];
+    if (ns > 0) {
+        double *buf = static_cast<double *>(part->alloc(part->user, (size_t)ns * Kp * sizeof(double)));
+        if (!buf) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+        const int64_t n = (int64_t)ns * Kp;
+        rows_pack_kernel<<<blocks_for(n, 256), 256, 0, st>>>(Pup, slist, ns, Kp, buf);
+        PK_CUDA(cudaStreamSynchronize(st));
+        if (part->allreduce(part->user, buf, n, st) != 0)
+            throw RuntimeError("evaluate_partitioned: allreduce of straddling equivalent densities failed");
+        rows_unpack_kernel<<<blocks_for(n, 256), 256, 0, st>>>(buf, slist, ns, Kp, Pup);
+        ctx.launches += 2;
+        moved += n;
+    }
+    std::vector<int64_t> sc(R), rc(R);
+    int64_t st_tot = 0, rt_tot = 0;
+    for (int q = 0; q < R; q++) {
+        sc[q] = (int64_t)h[2 * q] * Kp, rc[q] = (int64_t)h[2 * q + 1] * Kp;
+        st_tot += sc[q], rt_tot += rc[q];
+    }
+    double *sbuf = static_cast<double *>(part->alloc(part->user, (size_t)std::max<int64_t>(st_tot, 1) * sizeof(double)));
+    double *rbuf = static_cast<double *>(part->alloc(part->user, (size_t)std::max<int64_t>(rt_tot, 1) * sizeof(double)));
+    if (!sbuf || !rbuf) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+    for (int q = 0, o = 0; q < R; q++) {
+        if (h[2 * q]) {
+            rows_pack_kernel<<<blocks_for(sc[q], 256), 256, 0, st>>>(Pup, lists[2 * q], h[2 * q], Kp, sbuf + o);
+            ctx.launches++;
+        }
+        o += (int)sc[q];
+    }
+    PK_CUDA(cudaStreamSynchronize(st));
+    if (part->alltoallv(part->user, sbuf, sc.data(), rbuf, rc.data(), st) != 0)
+        throw RuntimeError("evaluate_partitioned: halo exchange of equivalent densities failed");
+    for (int q = 0; q < R; q++) {
+        int64_t o = 0;
+        for (int k = 0; k < q; k++) o += rc[k];
+        if (h[2 * q + 1]) {
+            rows_unpack_kernel<<<blocks_for(rc[q], 256), 256, 0, st>>>(rbuf + o, lists[2 * q + 1], h[2 * q + 1], Kp,
+                                                                       Pup);
+            ctx.launches++;
+        }
+    }
+    return moved + rt_tot;
 }
 
 // int8 operator sets for i8_translate, built on first use
@@ -801,21 +932,33 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         Partition Part;
         if (partitioned) Part = build_partition(ctx, T, part->rank, part->nranks, st);
         const Partition *PP = partitioned ? &Part : nullptr;
-        Layout Lay = build_layout(ctx, T, partitioned ? Part.in : nullptr, st);
+        // the small-level int8 run split by modulus across ranks (allgather given): every
+        // rank lays out all of that run's columns
+        const bool msplit = partitioned && part->allgather && ctx.i8.enabled;
+        const int64_t small_max = tuning().i8_small_boxes;
+        int *lmask = partitioned ? Part.in : nullptr;
+        if (msplit) {
+            lmask = ws.get<int>("pt_in_small", nb);
+            small_or_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(T.view(), Part.in, small_max, lmask);
+            ctx.launches++;
+        }
+        Layout Lay = build_layout(ctx, T, lmask, st);
         ListSetup ls{};
         if (periodic && ell >= 1)
             for (int a = 0; a < 3; a++) ls.periodic[a] = axes[a];
         build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
-                         &ctx.launches, partitioned ? Part.in : nullptr);
+                         &ctx.launches, lmask);
         prof.end(pm);
         // pseudo-inverse scratch: one level at a time (indexed by box id through a level offset)
         int64_t maxlev = 1;
         for (int l = 0; l <= T.depth; l++) maxlev = std::max<int64_t>(maxlev, T.level_off[l + 1] - T.level_off[l]);
         double *Q = ws.get<double>("Q", nb * Kp), *Tm = ws.get<double>("Tmp", maxlev * Kp),
                *Pdn = ws.get<double>("phi_dn", nb * Kp);
-        // phi_up lives in collective-visible memory when partitioned (summed over ranks)
-        double *Pup = partitioned ? static_cast<double *>(part->alloc(part->user, nb * Kp * sizeof(double)))
-                                  : ws.get<double>("phi_up", nb * Kp);
+        // phi_up lives in collective-visible memory when partitioned without a halo exchange
+        // (then summed over ranks in one allreduce)
+        const bool halo = partitioned && part->alltoallv;
+        double *Pup = partitioned && !halo ? static_cast<double *>(part->alloc(part->user, nb * Kp * sizeof(double)))
+                                           : ws.get<double>("phi_up", nb * Kp);
         if (!Pup) throw RuntimeError("evaluate_partitioned: allocation callback failed");
         if (partitioned) PK_CUDA(cudaMemsetAsync(Pup, 0, nb * Kp * sizeof(double), st));
         // ---- upward pass (src/fmm.cpp:532-553) ----
@@ -867,7 +1010,13 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             pinv_level(ctx, ops, true, lo, hi, l, Q, Tm - lo * Kp, Pup, st, PP, Lay);
             prof.end(pm);
         }
-        if (partitioned) {
+        if (halo) {
+            // straddlers summed, then the halo of V / W sources from their owners
+            pm = prof.begin("comm");
+            const int64_t moved = exchange_up(ctx, T, Part, ls, Pup, Kp, part, msplit ? small_max : 0, st);
+            prof.end(pm);
+            prof.work("comm", 8.0 * moved, 0.0);
+        } else if (partitioned) {
             // the upward chain is linear in the sources: the complete equivalent densities
             // (root included, feeding the periodizing step) are the sum over ranks
             pm = prof.begin("comm");
@@ -875,6 +1024,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             if (part->allreduce(part->user, Pup, nb * Kp, st) != 0)
                 throw RuntimeError("evaluate_partitioned: allreduce of equivalent densities failed");
             prof.end(pm);
+            prof.work("comm", 8.0 * nb * Kp, 0.0);
         }
         // ---- downward pass (src/fmm.cpp:557-601) ----
         PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));
@@ -928,14 +1078,34 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             I8LevelWork w = m2l_i8_prepare(ops.i8, a, is.beta_b, ws, st, &ctx.launches);
             prof.end(ps);
             const int64_t win = i8_window(ops.i8.nmod, ops.i8.Ki);
+            // split by modulus across ranks: ceil(nmod / R) moduli here, the residue sums of
+            // all columns gathered before the CRT (the run streams 1 / R of the operators)
+            const bool split_run = msplit && !a.big && a.ncols <= win;
+            int64_t split_block = 0;
+            if (split_run) {
+                const int R = part->nranks, B = (ops.i8.nmod + R - 1) / R;
+                split_block = (int64_t)B * a.ncols * ops.i8.Ki * (int64_t)sizeof(int);
+                w.R_ext = static_cast<int *>(part->alloc(part->user, (size_t)split_block * R));
+                if (!w.R_ext) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+                w.t0 = std::min(ops.i8.nmod, part->rank * B);
+                w.t1 = std::min(ops.i8.nmod, (part->rank + 1) * B);
+            }
             for (int64_t w0 = 0; w0 < a.ncols; w0 += win) { // column windows bound the residue sums
                 const int64_t w1 = std::min<int64_t>(a.ncols, w0 + win);
                 ps = prof.begin("m2l_prep");
                 ctx.launches += m2l_i8_window(ops.i8, a, w, w0, w1, ws, st);
                 prof.end(ps);
                 ps = prof.begin("m2l_i8");
-                ctx.launches += m2l_i8_gemm(ops.i8, a, w, w0, w1, ws, st);
+                if (!split_run || w.t1 > w.t0) ctx.launches += m2l_i8_gemm(ops.i8, a, w, w0, w1, ws, st);
                 prof.end(ps);
+                if (split_run) {
+                    ps = prof.begin("comm");
+                    PK_CUDA(cudaStreamSynchronize(st));
+                    if (part->allgather(part->user, w.R_ext, split_block, st) != 0)
+                        throw RuntimeError("evaluate_partitioned: allgather of residue sums failed");
+                    prof.end(ps);
+                    prof.work("comm", (double)split_block * (part->nranks - 1), 0.0);
+                }
                 ps = prof.begin("m2l_crt");
                 ctx.launches += m2l_i8_finish(ops.i8, a, w, w0, w1, is.beta_b, st);
                 prof.end(ps);

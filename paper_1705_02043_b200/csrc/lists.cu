@@ -414,6 +414,26 @@ struct EvalFillSink {
     __device__ void x(int c, int code) { ex[nx++] = make_int2(c, code); }
 };
 
+// which ranks need a box's equivalent density (partitioned runs): every target box c with
+// V or W entries marks its sources with the ranks whose leaf ranges c meets
+struct NeedSink {
+    unsigned long long *need;
+    unsigned long long m;
+    __device__ void u(int, int) {}
+    __device__ void v(int c, int) { atomicOr(need + c, m); }
+    __device__ void w(int c, int) { atomicOr(need + c, m); }
+    __device__ void x(int, int) {}
+};
+
+__global__ void need_kernel(TreeView T, Params P, const int *__restrict__ rlo, const int *__restrict__ rhi,
+                            unsigned long long *need) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= T.nboxes) return;
+    const int lo = rlo[b], hi = rhi[b];
+    NeedSink s{need, ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1ull)) >> lo) << lo};
+    enumerate_box(T, P, b, s);
+}
+
 __global__ void count_kernel(TreeView T, Params P, int64_t *cu, int64_t *cv, int64_t *cw, int64_t *cx) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= T.nboxes) return;
@@ -486,6 +506,14 @@ void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cu
                                                    L.x.ent);
     PK_CUDA(cudaStreamSynchronize(st));
     *launches += 6;
+}
+
+void need_masks(const DeviceTree &T, const ListSetup &S, const int *rlo, const int *rhi, unsigned long long *need,
+                cudaStream_t st) {
+    const int nb = (int)T.nboxes;
+    PK_CUDA(cudaMemsetAsync(need, 0, nb * sizeof(unsigned long long), st));
+    need_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(T.view(), make_params(S, 1), rlo, rhi, need);
+    PK_CUDA(cudaGetLastError());
 }
 
 void build_lists_eval(const DeviceTree &T, const ListSetup &S, DeviceLists &L, int *m2l_table, int64_t ld,

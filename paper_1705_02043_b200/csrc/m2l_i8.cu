@@ -75,6 +75,8 @@ struct Params {
     uint32_t idesc;
     int nst, stage_bytes; // single-CTA kernel: stage ring depth and stride
     int tile_fast;        // unit order: column tile fastest (decode_unit)
+    int *sched;           // dynamic schedule: global unit counter (zeroed per launch), or null
+    int t_base;           // first modulus of this launch (the small-level run split by modulus across ranks)
     int epi_transpose;    // epilogue atomics through a shared-memory transpose (coalesced)
     int *R; // [nmod][ncols][Ki]
 };
@@ -157,7 +159,7 @@ __device__ __forceinline__ void decode_unit(const Params &p, int u, int ntiles, 
         u /= ntiles;
     }
     chunk = u % p.nchunk;
-    t = u / p.nchunk;
+    t = p.t_base + u / p.nchunk;
 }
 
 struct Unit {
@@ -349,6 +351,60 @@ __device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
 __device__ __forceinline__ void remote_arrive_cta(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
+
+// ---------------------------------------------------------------------------
+// Dynamic unit schedule (p.sched != null): one scheduler warp per CTA / CTA pair hands out
+// unit indices from a global counter in increasing order, so the concurrently running units
+// always form one contiguous window of the unit order -- with the column-tile-fastest order
+// and slot-index chunks, the operator tiles of that window are read from DRAM once and
+// served from L2 to every tile (the static round robin lets CTAs drift apart on adaptive
+// levels, whose tiles have very different slot counts). Every role warp of both CTAs pops
+// the same sequence from a small queue in its own shared memory; slots are released on the
+// leader's "empty" barrier (remote arrivals from the peer).
+constexpr int UQ = 4;
+struct UnitQueue {
+    int u[UQ];
+    uint64_t full[UQ], empty[UQ];
+};
+__device__ __forceinline__ void uq_init(UnitQueue &q, unsigned consumers) {
+    for (int s = 0; s < UQ; s++) {
+        tma::mbar_init(&q.full[s], 1);
+        tma::mbar_init(&q.empty[s], consumers);
+    }
+}
+// k-th unit of the sequence (whole warp); `remote`: this CTA is the pair's peer
+__device__ __forceinline__ int uq_pop(UnitQueue &q, int k, bool remote) {
+    const int s = k % UQ;
+    tma::mbar_wait(&q.full[s], (k / UQ) & 1);
+    const int u = *reinterpret_cast<volatile int *>(&q.u[s]);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        if (remote)
+            remote_arrive(map_to_rank(&q.empty[s], 0));
+        else
+            tma::mbar_arrive(&q.empty[s]);
+    }
+    return u;
+}
+// the scheduler warp (leader CTA): pushes units until it has pushed one >= total
+__device__ __forceinline__ void uq_schedule(UnitQueue &q, int *counter, int total, bool pair) {
+    for (int k = 0;; k++) {
+        const int s = k % UQ;
+        tma::mbar_wait(&q.empty[s], ((k / UQ) & 1) ^ 1);
+        int u = 0;
+        if ((threadIdx.x & 31) == 0) {
+            u = min(atomicAdd(counter, 1), total);
+            q.u[s] = u;
+            tma::mbar_arrive(&q.full[s]);
+            if (pair) {
+                asm volatile("st.shared::cluster.b32 [%0], %1;\n" ::"r"(map_to_rank(&q.u[s], 1)), "r"(u) : "memory");
+                remote_arrive(map_to_rank(&q.full[s], 1));
+            }
+        }
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= total) break;
+    }
+}
 // ---------------------------------------------------------------------------
 // Dual-tile variant (one CTA per SM): a unit covers TWO 128-box column tiles (a 256-column
 // pair tile with one slot list) and one operator row tile. Per stage: 2 x 16 KB gathered
@@ -360,19 +416,23 @@ __device__ __forceinline__ void remote_arrive_cta(uint32_t cluster_addr) {
 constexpr int DUAL_NPROD = 4;
 constexpr int DUAL_MMA_WARP = DUAL_NPROD;
 constexpr int DUAL_THREADS = (DUAL_NPROD + 1 + 4) * 32;
+constexpr int DUAL_SCHED_WARP = DUAL_THREADS / 32;    // warp 9: unit scheduler (dynamic schedule)
+constexpr int DUAL_THREADS_DYN = DUAL_THREADS + 32;
 constexpr int DUAL_A_BYTES = 2 * A_BYTES;
 constexpr int DUAL_STAGE = DUAL_A_BYTES + B_BYTES;
 constexpr int DUAL_NST = 3;
 
-__global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(DUAL_THREADS_DYN, 1) m2l_i8_dual_kernel(const __grid_constant__ Params p) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     int *s_epi = reinterpret_cast<int *>(smem + DUAL_NST * DUAL_STAGE); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t full[DUAL_NST], empty[DUAL_NST], tfull, tempty;
+    __shared__ UnitQueue uq;
     __shared__ uint32_t s_tmem;
     const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     constexpr int NPT = DUAL_NPROD * 32;
+    const bool dyn = p.sched != nullptr;
     if (tid == 0) {
         for (int s = 0; s < DUAL_NST; s++) {
             tma::mbar_init(&full[s], NPT + 1);
@@ -380,6 +440,7 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
         }
         tma::mbar_init(&tfull, 1);
         tma::mbar_init(&tempty, 4);
+        uq_init(uq, DUAL_THREADS / 32);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == DUAL_MMA_WARP) {
@@ -395,7 +456,12 @@ __global__ void __launch_bounds__(DUAL_THREADS, 1) m2l_i8_dual_kernel(const __gr
 
     int g = 0, jb = 0;
     const int npairs = p.coltiles / 2;
-    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+    if (warp == DUAL_SCHED_WARP) {
+        if (dyn) uq_schedule(uq, p.sched, p.total_units, false);
+    } else
+    for (int k = 0, us = blockIdx.x;; k++, us += gridDim.x) {
+        const int u = dyn ? uq_pop(uq, k, false) : us;
+        if (u >= p.total_units) break;
         int t, rt, pr, chunk;
         decode_unit(p, u, npairs, t, rt, pr, chunk);
         int s0, s1;
@@ -579,7 +645,8 @@ constexpr int PD_B_BYTES = 128 * BKI; // half operator tile, Nt / 2 <= 128 rows
 constexpr int PD_NA = 4;               // gathered-row ring (32 KB stages)
 constexpr int PD_NB = 5;               // operator ring (16 KB stages): runs further ahead
 constexpr int PD_OPER_WARP = DUAL_THREADS / 32; // warp 9: operator TMA producer
-constexpr int PD_THREADS = DUAL_THREADS + 32;
+constexpr int PD_SCHED_WARP = PD_OPER_WARP + 1;         // warp 10: unit scheduler (leader, dynamic schedule)
+constexpr int PD_THREADS = DUAL_THREADS + 64;
 constexpr size_t PD_RING_BYTES = (size_t)PD_NA * DUAL_A_BYTES + (size_t)PD_NB * PD_B_BYTES;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
@@ -591,6 +658,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
     int *s_epi = reinterpret_cast<int *>(smem + PD_RING_BYTES); // [4 warps][32][33]
     __shared__ __align__(8) uint64_t fullA[PD_NA], pfullA[PD_NA], emptyA[PD_NA], fullB[PD_NB], emptyB[PD_NB], tfull,
         tempty;
+    __shared__ UnitQueue uq;
     __shared__ uint32_t s_tmem;
     const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -609,6 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
         }
         tma::mbar_init(&tfull, 1);
         tma::mbar_init(&tempty, 8); // leader: 4 local + 4 remote epilogue warps
+        uq_init(uq, 2 * (PD_OPER_WARP + 1)); // leader: the role warps of both CTAs
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == DUAL_MMA_WARP) {
@@ -624,7 +693,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
 
     int g = 0, jb = 0;
     const int nquads = p.coltiles / 4;
-    for (int u = blockIdx.x / 2; u < p.total_units; u += gridDim.x / 2) {
+    const bool dyn = p.sched != nullptr;
+    if (warp == PD_SCHED_WARP) {
+        if (dyn && leader) uq_schedule(uq, p.sched, p.total_units, true);
+    } else
+    for (int k = 0, us = blockIdx.x / 2;; k++, us += gridDim.x / 2) {
+        const int u = dyn ? uq_pop(uq, k, !leader) : us;
+        if (u >= p.total_units) break;
         int t, rt, qd, chunk;
         decode_unit(p, u, nquads, t, rt, qd, chunk);
         int s0, s1;
@@ -1253,7 +1328,7 @@ template <class F> void ensure_smem(F *kernel, size_t bytes) {
 void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, int zero_row, int Ki, int nmod,
                  const int *src, int64_t ld_src, int64_t box0, int nslots, int ncols, int *R, const int *tslots,
                  const int *tnact, const int *tbelow, I8Kernel kind, cudaStream_t st, bool direct = false,
-                 const uint8_t *thmask = nullptr, int K = 0) {
+                 const uint8_t *thmask = nullptr, int K = 0, int *sched = nullptr, int t0 = 0, int t1 = -1) {
     if (masked(kind) && !thmask) throw RuntimeError("i8 gemm: the dual-tile kernels need the half masks");
     const int num_sms = sm_count();
     Params p;
@@ -1281,7 +1356,9 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     // chunks keep |int32 accumulator| <= slots * Ki * 128^2 < 2^31
     const int64_t cmax = std::max<int64_t>(1, 2147483647LL / ((int64_t)Ki * 16384));
     int nchunk = (int)((nslots + cmax - 1) / cmax);
-    const int64_t base = (int64_t)nmod * p.rowtiles * (ncols / column_tile(kind));
+    if (t1 < 0) t1 = nmod;
+    p.t_base = t0;
+    const int64_t base = (int64_t)(t1 - t0) * p.rowtiles * (ncols / column_tile(kind));
     const int64_t resident = kind == I8Kernel::pairdual ? num_sms / 2 : num_sms;
     // enough units for ~4 per resident CTA (cfg2's small-level run: 3 -> 4 chunks, 2.57 -> 2.43 ms)
     while (base * nchunk < 4 * resident && nchunk * 16 < nslots) nchunk++;
@@ -1302,6 +1379,11 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
     const Tuning &tu = tuning();
     p.by_index = tu.i8_by_index >= 0 ? tu.i8_by_index : (masked(kind) ? 0 : 1);
     p.tile_fast = tu.i8_tile_fast >= 0 ? tu.i8_tile_fast : 0;
+    // dynamic unit schedule (dual-tile kernels): the caller's zeroed counter
+    if (sched && kind != I8Kernel::single) {
+        PK_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), st));
+        p.sched = sched;
+    }
     if (tu.i8_min_chunks > nchunk) {
         p.nchunk = nchunk = tu.i8_min_chunks;
         p.total_units = (int)(base * nchunk);
@@ -1327,7 +1409,7 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         const size_t smem = (size_t)DUAL_NST * DUAL_STAGE + epi;
         ensure_smem(m2l_i8_dual_kernel, smem);
         const unsigned grid = (unsigned)std::min<int64_t>(p.total_units, num_sms);
-        m2l_i8_dual_kernel<<<grid, DUAL_THREADS, smem, st>>>(p);
+        m2l_i8_dual_kernel<<<grid, DUAL_THREADS_DYN, smem, st>>>(p);
     } else {
         // stage = 16 KB gathered rows + the operator tile rounded to 1 KB; as many stages as
         // the 227 KB of shared memory allow (the transposing epilogue costs 16.5 KB)
@@ -1357,7 +1439,7 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     uint8_t *thmask = nullptr;
     scan_tiles(src, ld_src, nslots, ncols, kind, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,
-                tbelow, kind, st, false, thmask);
+                tbelow, kind, st, false, thmask, 0, tuning().i8_dynamic > 0 ? ws.get<int>("i8_sched", 1) : nullptr);
     return 2;
 }
 
@@ -1402,8 +1484,9 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
     const int ncols = (int)(c1 - c0);
     if (ncols <= 0) return 0;
     if (c0 % kI8Tile != 0 || ncols % kI8Tile != 0) throw RuntimeError("m2l_i8: column window not tile aligned");
-    // residue sums of this column window only (the window bounds R: 4 nmod Ki bytes per column)
-    w.R = ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
+    // residue sums of this column window only (the window bounds R: 4 nmod Ki bytes per column);
+    // a modulus-split run (partitioned) sums into the caller's collective-visible buffer
+    w.R = w.R_ext ? w.R_ext : ws.get<int>("i8_R", (size_t)o.nmod * ncols * o.Ki);
     PK_CUDA(cudaMemsetAsync(w.R, 0, (size_t)o.nmod * ncols * o.Ki * sizeof(int), st));
     // the multicast variant needs whole 512-column quads; other windows use the dual kernel
     w.win_kind = window_kernel(w.kind, ncols, o.K);
@@ -1419,12 +1502,12 @@ int m2l_i8_window(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, in
 
 int m2l_i8_gemm(const I8Operators &o, const I8LevelArgs &a, I8LevelWork &w, int64_t c0, int64_t c1, Workspace &ws,
                 cudaStream_t st) {
-    (void)ws;
     const int ncols = (int)(c1 - c0);
     if (ncols <= 0) return 0;
+    const int dyn = tuning().i8_dynamic;
     launch_gemm(o.res, o.nmat, w.xres, (int)w.rows, (int)(w.rows - 1), o.Ki, o.nmod, a.src + c0, a.ld_src,
                 a.lv.box0[0], a.nslots, ncols, w.R, w.tile_slots, w.tile_nact, w.tile_below, w.win_kind, st, false,
-                w.tile_hmask, o.K);
+                w.tile_hmask, o.K, dyn > 0 ? ws.get<int>("i8_sched", 1) : nullptr, w.t0, w.t1 < 0 ? o.nmod : w.t1);
     return 1;
 }
 

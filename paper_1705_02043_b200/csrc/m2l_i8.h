@@ -107,6 +107,8 @@ struct I8LevelArgs {
 struct I8LevelWork {
     const int8_t *xres = nullptr;     // [nmod][nbox + 1][Ki] density residues (last row zero)
     int *R = nullptr;                 // [nmod][ncols][Ki] residue sums
+    int *R_ext = nullptr;             // caller-provided R (modulus split across ranks), or null
+    int t0 = 0, t1 = -1;              // moduli this launch computes (-1: all)
     unsigned long long *mx = nullptr; // per-level max |phi| (bit patterns)
     int64_t rows = 0;
     int *tile_slots = nullptr, *tile_nact = nullptr; // active V slots per column tile

@@ -84,6 +84,12 @@ struct DeviceLists {
     int64_t v_total = 0; // V applications (evaluate path: entries written to the M2L table)
 };
 
+// Partitioned runs: need[b] = bit mask of the ranks that read box b's equivalent density
+// (V / W sources of target boxes meeting rank r's leaf range [rlo[c], rhi[c]]); all boxes
+// enumerated, nothing stored but the masks (ranks < 64).
+void need_masks(const DeviceTree &T, const ListSetup &S, const int *rlo, const int *rhi, unsigned long long *need,
+                cudaStream_t st);
+
 // Full CSR lists for all four types (export / tests).
 void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cudaStream_t stream,
                      int64_t *launches);

@@ -35,6 +35,7 @@ const Tuning &tuning() {
         r.i8_by_index = (int)env_int("PKGPU_I8_BYINDEX", r.i8_by_index, -1);
         r.i8_tile_fast = (int)env_int("PKGPU_I8_TILEFAST", r.i8_tile_fast, -1);
         r.i8_min_chunks = (int)env_int("PKGPU_I8_CHUNKS", r.i8_min_chunks, 0);
+        r.i8_dynamic = (int)env_int("PKGPU_I8_DYNAMIC", r.i8_dynamic, 0);
         r.gemm_units_per_cta = env_int("PKGPU_GEMM_UNITS", r.gemm_units_per_cta, 1);
         r.gemm_min_iters = env_int("PKGPU_GEMM_MINIT", r.gemm_min_iters, 1);
         r.gemm_min_iters_small = env_int("PKGPU_GEMM_MINIT_SMALL", r.gemm_min_iters_small, 1);

@@ -24,7 +24,8 @@ struct Tuning {
     I8Kernel i8_kernel = I8Kernel::automatic; // PKGPU_I8_KERNEL = single | dual | pairdual
     int i8_by_index = -1;              // PKGPU_I8_BYINDEX = 0 | 1: chunks as slot-index windows (-1: per kernel)
     int i8_tile_fast = -1;             // PKGPU_I8_TILEFAST = 0 | 1: unit order, column tile fastest
-    int i8_min_chunks = 0;             // PKGPU_I8_CHUNKS: at least this many slot chunks per tile
+    int i8_min_chunks = 0;
+    int i8_dynamic = 0;                // PKGPU_I8_DYNAMIC = 0 | 1: dynamic unit schedule (dual-tile kernels)             // PKGPU_I8_CHUNKS: at least this many slot chunks per tile
     int64_t gemm_units_per_cta = 32;   // PKGPU_GEMM_UNITS: DMMA gather-GEMM work units per CTA
     int64_t gemm_min_iters = 16;       // PKGPU_GEMM_MINIT: k-iterations per split-K unit
     int64_t gemm_min_iters_small = 4;  // PKGPU_GEMM_MINIT_SMALL: same, latency-bound one-slot GEMMs

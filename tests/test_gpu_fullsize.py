@@ -42,3 +42,46 @@ def test_cfg2_full_size_vs_reference():
     print(f"cfg2 full size: rel-L2 vs reference {rel:.3e}; ref wall {json.loads(r.stdout)['runs'][0]['wall']:.2f} s")
     assert rel <= 1.4e-7
     assert ref_up.shape == (3 * 296,)
+
+
+def _fixture_request(name):
+    import torch
+
+    f = np.load(os.path.join(GOLDEN, f"full_{name}.npz"))
+    c = json.loads(str(f["meta"]))
+    k = pk.KernelSpec.from_name(c["kernel"])
+    setup = pk.PeriodicSetup.make(pk.Periodicity.from_name(c["per"]))
+    axes = tuple(a in c["axes"] for a in "xyz")
+    pts, q = pk.generate(c["kind"], c["n"], c["ks"], seed=12345, nclusters=c["nclusters"], sigma=c["sigma"],
+                         periodic_axes=axes)
+    assert np.array_equal(np.array([pts.sum(), q.sum()]), f["fp"])  # the reference's inputs, bit for bit
+    op = pk.load_operator(os.path.join(GOLDEN, "ops", c["op"]))
+    if c["relabel"]:
+        op.relabel(k, setup)
+    dev = torch.device("cuda", 0)
+    d_pts = torch.from_numpy(pts).to(dev).reshape(-1).contiguous()
+    req = pk.EvalRequest(kernel=k, sources=d_pts, strengths=torch.from_numpy(q).to(dev), targets=d_pts, setup=setup,
+                         p=c["p"], op=op, leaf_capacity=c["leaf"])
+    return f, c, k, pts, req
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_full_size_vs_reference_fixture(name):
+    if not os.path.exists(os.path.join(GOLDEN, f"full_{name}.npz")):
+        pytest.skip(f"tests/golden/full_{name}.npz not generated")
+    """BASELINE cfg3 (Stokes DP p = 10, 1M clustered, stand-in operator) and cfg4 (Laplace TP
+    p = 8, 8M uniform, ungated operator) at full size against the unmodified reference run
+    once in the build container (tests/golden/make_fullsize.py: 65,536 strided targets).
+    Bar (SURVEY §8c): rel-L2 <= max(1e-10, 10 x the reference's 8-vs-4-thread spread)."""
+    f, c, k, pts, req = _fixture_request(name)
+    t = pk.FmmTree(pts, pts, c["leaf"])
+    assert t.structure_hash() == int(f["hash"])
+    del t
+    res = pk.evaluate(req)
+    got = res.potentials.cpu().numpy().reshape(-1, k.kt)[f["idx"]].reshape(-1)
+    ref = f["pot"]
+    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    tol = max(1e-10, 10 * float(f["spread"]))
+    print(f"{name} full size ({c['n']} points): rel-L2 vs reference {rel:.3e} on {len(f['idx'])} targets "
+          f"(reference spread {float(f['spread']):.1e}, tol {tol:.1e}); reference wall {c['wall_s']}")
+    assert rel <= tol

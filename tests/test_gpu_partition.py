@@ -15,14 +15,19 @@ from conftest import GOLDEN
 pytestmark = pytest.mark.gpu
 
 
-def run_ranks(req, nranks):
+def run_ranks(req, nranks, v1=False, moved=None):
     tc = pk.ThreadComm(nranks)
     outs, errs = [None] * nranks, []
 
     def body(r):
         try:
             ctx = pk.Context(0)
-            outs[r] = pk.evaluate(req, context=ctx, comm=tc.rank(r)).potentials.copy()
+            comm = tc.rank(r)
+            if v1:
+                comm.set_v1()
+            outs[r] = pk.evaluate(req, context=ctx, comm=comm).potentials.copy()
+            if moved is not None:
+                moved[r] = comm.moved
             ctx.close()
         except Exception as e:  # pragma: no cover - surfaced below
             errs.append(e)
@@ -60,16 +65,21 @@ def golden_req(name):
     return req, float(g["self_spread"])
 
 
+@pytest.mark.parametrize("scheme", ["halo", "v1"])
 @pytest.mark.parametrize("name,nranks", [("lap_sp_p8", 2), ("lap_sp_p8", 3), ("lap_none_p6", 4), ("cfg1", 4),
-                                         ("sto_tp_p6", 2), ("sto_dp_p6", 3)])
-def test_partitioned_matches_single(name, nranks):
+                                         ("sto_tp_p6", 2), ("sto_dp_p6", 3), ("lap_sp_p8_clu", 5),
+                                         ("sto_tp_p6_clu", 3)])
+def test_partitioned_matches_single(name, nranks, scheme):
+    """halo: straddler allreduce + halo alltoallv of equivalent densities, small-level int8
+    run split by modulus (allgather); v1: one allreduce of every box's density."""
     req, spread = golden_req(name)
     single = pk.evaluate(req).potentials
-    outs = run_ranks(req, nranks)
+    moved = [0] * nranks
+    outs = run_ranks(req, nranks, v1=scheme == "v1", moved=moved)
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])  # every rank holds the full, identical result
     err = rel(outs[0], single)
-    print(f"{name} R={nranks}: rel-L2 vs single rank {err:.3e}")
+    print(f"{name} R={nranks} [{scheme}]: rel-L2 vs single rank {err:.3e}; doubles received per rank {moved}")
     assert err <= max(1e-13, 3 * spread)
 
 
