@@ -274,9 +274,16 @@ def run_ours(args):
     import paper_1705_02043_b200 as pk
 
     ws, rank, local = dist_env()
+    # one process per GPU; BENCH_DIST_BACKEND=gloo (host collectives) lets ranks share a GPU
+    # for a plumbing check on a one-GPU box -- never a measurement
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = pk.Context(local)
@@ -389,8 +396,10 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "N": N_POINTS, "p": P_ORDER, "leaf": LEAF, "kernel": "stokeslet",
                        "periodicity": "tp", "ell": 2,
                        "l2": "flushed between timed steps (256 MiB write, outside the step events)",
-                       "parallelism": (f"dp{ws}: Morton-range partition of the leaves, NCCL allreduce of "
-                                       "equivalent densities + potentials") if ws > 1 else "single GPU"},
+                       "parallelism": (f"dp{ws}: Morton-range partition of the leaves; straddler allreduce + "
+                                       "halo alltoallv of equivalent densities, small-level int8 run split by "
+                                       f"modulus (allgather), allreduce of potentials ({backend})") if ws > 1
+                       else "single GPU"},
             "e2e": {"value": N_POINTS / (e2e_max * 1e-3), "unit": UNIT,
                     # positions + forces; the targets are the sources' own buffer, which the
                     # API copies once (csrc/evaluate.cu input staging)
@@ -398,6 +407,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(3 * N_POINTS * 8), "matches_device_result": same},
             "gpu_launches": int(round(launches)),
             "roofline": roofline,
+            "comm": ({"bytes_received_per_rank_per_step": 8 * comm.moved,
+                      "note": "rank 0, last step: straddler allreduce + halo alltoallv + residue-sum allgather + "
+                              "potentials allreduce (doubles received x 8)"} if comm is not None else None),
             "stages": stage_tab,
             "stages_note": "profiled pass (not the timed region)",
             "clocks": clk,

@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) m2l_i8_kernel(const __grid_consta
                     unsigned char *as = smem + st * SB;
                     if (tid == 0) {
                         tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        tma::tma_load_3d(as + A_BYTES, &p.tmB, kc * BKI, x.rt * p.Nt, x.t * p.nmat + slot, &full[st]);
+                        tma::tma_load_4d(as + A_BYTES, &p.tmB, 0, 0, kc, (x.t * p.nmat + slot) * p.rowtiles + x.rt,
+                                         &full[st]);
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
@@ -492,7 +493,8 @@ __global__ void __launch_bounds__(DUAL_THREADS_DYN, 1) m2l_i8_dual_kernel(const 
                     unsigned char *as = smem + st * DUAL_STAGE;
                     if (tid == 0) {
                         tma::mbar_expect_tx(&full[st], p.Nt * BKI);
-                        tma::tma_load_3d(as + DUAL_A_BYTES, &p.tmB, kc * BKI, rt * p.Nt, t * p.nmat + slot, &full[st]);
+                        tma::tma_load_4d(as + DUAL_A_BYTES, &p.tmB, 0, 0, kc, (t * p.nmat + slot) * p.rowtiles + rt,
+                                         &full[st]);
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) {
@@ -754,10 +756,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PD_THREADS, 1)
                         asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(bar),
                                      "r"(2 * half * BKI)
                                      : "memory");
-                    asm volatile("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
-                                 "bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tma::smem_u32(ringB + st * PD_B_BYTES)),
-                                 "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(kc * BKI),
-                                 "r"(rt * p.Nt + (int)rank * half), "r"(t * p.nmat + slot), "r"(bar)
+                    asm volatile("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+                                 "bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(tma::smem_u32(ringB + st * PD_B_BYTES)),
+                                 "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(0), "r"((int)rank * half), "r"(kc),
+                                 "r"((t * p.nmat + slot) * p.rowtiles + rt), "r"(bar)
                                  : "memory");
                 }
                 __syncwarp();
@@ -970,15 +972,31 @@ __global__ void rowexp_kernel(const unsigned long long *__restrict__ mx, int K, 
     rowexp[r] = m > 0 ? ilogb(m) + 1 : 0;
 }
 
+// operator residues, tile-contiguous: [t][mat][row tile][k chunk][Nt rows][128 B], so every
+// TMA box (an Nt x 128 B operator tile, or half of it) is one contiguous range
 __global__ void op_residue_kernel(const double *__restrict__ A, int nmat, int K, int Kp, int Ki, int nmod, int beta,
-                                  const int *__restrict__ rowexp, int8_t *__restrict__ res) {
-    const int r = blockIdx.x, o = blockIdx.y;
-    const int64_t stride = (int64_t)nmat * Ki * Ki;
-    int8_t *out = res + ((int64_t)o * Ki + r) * Ki;
+                                  const int *__restrict__ rowexp, int Nt, int rowtiles, int8_t *__restrict__ res) {
+    const int r = blockIdx.x, o = blockIdx.y; // r < rowtiles * Nt
+    const int KC = Ki / 128;
+    const int64_t stride = (int64_t)nmat * rowtiles * KC * Nt * 128;
+    const int rt = r / Nt, rr = r % Nt;
+    int8_t *out = res + (((int64_t)o * rowtiles + rt) * KC * Nt + rr) * 128;
     for (int k = threadIdx.x; k < Ki; k += blockDim.x) {
         const double a = (r < K && k < K) ? A[((size_t)o * Kp + r) * Kp + k] : 0.0;
-        residues(llrint(ldexp(a, beta - rowexp[r])), nmod, out + k, stride);
+        residues(llrint(ldexp(a, beta - (r < K ? rowexp[r] : 0))), nmod, out + (int64_t)(k / 128) * Nt * 128 + (k % 128),
+                 stride);
     }
+}
+
+// plain [t][mat][Ki][Ki] int8 -> the tile-contiguous layout (the i8_gather_gemm test entry)
+__global__ void op_tile_kernel(const int8_t *__restrict__ A, int nmm, int Ki, int Nt, int rowtiles,
+                               int8_t *__restrict__ out) {
+    const int r = blockIdx.x, o = blockIdx.y; // o < nmod * nmat
+    const int KC = Ki / 128, rt = r / Nt, rr = r % Nt;
+    (void)nmm;
+    for (int k = threadIdx.x; k < Ki; k += blockDim.x)
+        out[(((int64_t)o * rowtiles + rt) * KC + k / 128) * Nt * 128 + (int64_t)rr * 128 + k % 128] =
+            r < Ki ? A[((int64_t)o * Ki + r) * Ki + k] : 0;
 }
 
 __global__ void level_absmax_kernel(const double *__restrict__ X, int64_t nbox, int K, int Kp,
@@ -1263,8 +1281,10 @@ void i8_build_operators(I8Operators &o, Workspace &ws, const double *A, int nmat
     rowmax_kernel<<<dim3(K, nmat), 32, 0, st>>>(A, nmat, K, Kp, mx);
     o.rowexp = ws.get<int>(pre + "rowexp", o.Ki);
     rowexp_kernel<<<(o.Ki + 127) / 128, 128, 0, st>>>(mx, K, o.Ki, o.rowexp);
-    o.res = ws.get<int8_t>(pre + "res", (size_t)nmod * nmat * o.Ki * o.Ki);
-    op_residue_kernel<<<dim3(o.Ki, nmat), 128, 0, st>>>(A, nmat, K, Kp, o.Ki, nmod, beta_a, o.rowexp, o.res);
+    const int nt = nt_of(K), rtl = rowtiles_of(K);
+    o.res = ws.get<int8_t>(pre + "res", (size_t)nmod * nmat * rtl * nt * o.Ki);
+    op_residue_kernel<<<dim3(rtl * nt, nmat), 128, 0, st>>>(A, nmat, K, Kp, o.Ki, nmod, beta_a, o.rowexp, nt, rtl,
+                                                             o.res);
     PK_CUDA(cudaGetLastError());
 }
 
@@ -1282,10 +1302,6 @@ I8Kernel select_kernel(bool big) {
     if (forced != I8Kernel::automatic) return forced;
     return big ? I8Kernel::pairdual : I8Kernel::dual;
 }
-// operator rows per tile: as few tiles as possible, N a multiple of 16 (<= 256)
-// (from the true K: operator rows past K inside the 128-padded Ki are never computed)
-int rowtiles_of(int K) { return (K + 255) / 256; }
-int nt_of(int K) { return ((K + rowtiles_of(K) - 1) / rowtiles_of(K) + 31) / 32 * 32; }
 // the pair-dual kernel needs whole 512-column quads and Nt / 2 a multiple of 16
 I8Kernel window_kernel(I8Kernel k, int ncols, int K) {
     if (k == I8Kernel::pairdual && (ncols % (4 * TBM) != 0 || nt_of(K) % 32 != 0)) return I8Kernel::dual;
@@ -1388,12 +1404,14 @@ void launch_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod, i
         p.nchunk = nchunk = tu.i8_min_chunks;
         p.total_units = (int)(base * nchunk);
     }
-    const cuuint64_t dims[3] = {(cuuint64_t)Ki, (cuuint64_t)Ki, (cuuint64_t)nmod * nmat};
-    const cuuint64_t strides[2] = {(cuuint64_t)Ki, (cuuint64_t)Ki * Ki};
+    // operator residues, tile-contiguous [t][mat][row tile][k chunk][Nt][128 B] (op_residue_kernel)
+    const cuuint64_t dims[4] = {(cuuint64_t)BKI, (cuuint64_t)p.Nt, (cuuint64_t)p.KC,
+                                (cuuint64_t)nmod * nmat * p.rowtiles};
+    const cuuint64_t strides[3] = {(cuuint64_t)BKI, (cuuint64_t)BKI * p.Nt, (cuuint64_t)BKI * p.Nt * p.KC};
     // the CTA-pair kernel stages half of the operator tile per CTA
-    const cuuint32_t box[3] = {BKI, (cuuint32_t)(kind == I8Kernel::pairdual ? p.Nt / 2 : p.Nt), 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(A), dims, strides,
+    const cuuint32_t box[4] = {BKI, (cuuint32_t)(kind == I8Kernel::pairdual ? p.Nt / 2 : p.Nt), 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t *>(A), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (int8) failed (" + std::to_string((int)r) + ")");
@@ -1436,6 +1454,12 @@ int i8_gather_gemm(const int8_t *A, int nmat, const int8_t *B, int rows_per_mod,
     upload_tables();
     int *tslots = nullptr, *tnact = nullptr, *tbelow = nullptr;
     const I8Kernel kind = window_kernel(ncols >= 2048 ? select_kernel(true) : I8Kernel::single, ncols, Ki);
+    // the kernels read operator residues tile-contiguous; the test input is [t][slot][Ki][Ki]
+    const int nt = nt_of(Ki), rtl = rowtiles_of(Ki);
+    int8_t *At = ws.get<int8_t>("i8_gg_tiled", (size_t)nmod * nmat * rtl * nt * Ki);
+    op_tile_kernel<<<dim3(rtl * nt, nmod * nmat), 128, 0, st>>>(A, nmod * nmat, Ki, nt, rtl, At);
+    PK_CUDA(cudaGetLastError());
+    A = At;
     uint8_t *thmask = nullptr;
     scan_tiles(src, ld_src, nslots, ncols, kind, ws, st, &tslots, &tnact, &tbelow, &thmask);
     launch_gemm(A, nmat, B, rows_per_mod, zero_row, Ki, nmod, src, ld_src, box0, nslots, ncols, R, tslots, tnact,

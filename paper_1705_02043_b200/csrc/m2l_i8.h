@@ -30,9 +30,14 @@ constexpr int64_t kI8Window = 65536; // columns per M2L gemm/finish window
 // small enough for their atomics to hit L2 (one window of cfg4's 262k-box level: 85.8 ms, four: 82.5 ms)
 int64_t i8_window(int nmod, int Ki);
 
+// operator rows per tile: as few tiles as possible, N a multiple of 32 (<= 256), from the
+// true K (operator rows past K inside the 128-padded Ki are never computed)
+inline int rowtiles_of(int K) { return (K + 255) / 256; }
+inline int nt_of(int K) { return ((K + rowtiles_of(K) - 1) / rowtiles_of(K) + 31) / 32 * 32; }
+
 struct I8Operators {          // residues of the stacked M2L operators (built once per KifmmOps)
     int nmod = 0, beta_a = 0, Ki = 0, nmat = 0, K = 0;
-    int8_t *res = nullptr;    // [nmod][nmat][Ki][Ki], Ki = roundup(K, 128)
+    int8_t *res = nullptr;    // [nmod][nmat][rowtiles][Ki / 128][Nt][128] (tile-contiguous), Ki = roundup(K, 128)
     int *rowexp = nullptr;    // [Ki] e_r
 };
 
