@@ -7,6 +7,7 @@
 
 #include "kernels.cuh"
 #include "pairs.h"
+#include "tuning.h"
 
 namespace pkgpu {
 
@@ -490,10 +491,17 @@ void leaf_pass(const PairGeom &g, const DeviceTree &T, const DeviceLists &L, con
     if (nleaves == 0) return;
     LeafParams P{T.view(), g.n,         g.Kp,       g.tmpl,   T.src_pos, T.src_f, T.trg_pos, T.trg_perm, leaves,
                  L.u.off,  L.w.off,     L.u.ent,    L.w.ent,  phi_dn,    phi_up,  phi_far,   out};
-    if (g.kernel == 0)
-        leaf_kernel<0, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
-    else
-        leaf_kernel<1, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
+    // targets per thread (register tile): PKGPU_LEAF_TT = 1 | 2 | 4, default 2
+    const int tt = tuning().leaf_tt;
+    if (g.kernel == 0) {
+        if (tt == 1) leaf_kernel<0, 1><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        else if (tt == 4) leaf_kernel<0, 4><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        else leaf_kernel<0, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
+    } else {
+        if (tt == 1) leaf_kernel<1, 1><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        else if (tt == 4) leaf_kernel<1, 4><<<(unsigned)nleaves, NT, 0, st>>>(P);
+        else leaf_kernel<1, 2><<<(unsigned)nleaves, NT, 0, st>>>(P);
+    }
     PK_CUDA(cudaGetLastError());
 }
 

