@@ -26,7 +26,7 @@ const Tuning &tuning() {
         }
         r.i8_min_boxes = env_int("PKGPU_M2L_I8_MIN", r.i8_min_boxes, 1);
         r.i8_small_boxes = env_int("PKGPU_I8_SMALL", r.i8_small_boxes, 0);
-        r.i8_window = env_int("PKGPU_I8_WINDOW", r.i8_window, 1);
+        r.i8_window = env_int("PKGPU_I8_WINDOW", r.i8_window, 0);
         if (const char *e = std::getenv("PKGPU_I8_KERNEL")) {
             if (!std::strcmp(e, "single")) r.i8_kernel = I8Kernel::single;
             else if (!std::strcmp(e, "dual")) r.i8_kernel = I8Kernel::dual;

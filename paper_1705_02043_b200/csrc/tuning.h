@@ -20,7 +20,7 @@ struct Tuning {
     int nmod = 16, beta_a = 52, beta_b = 52; // PKGPU_M2L_I8 = "nmod,beta_a,beta_b"
     int64_t i8_min_boxes = 1;          // PKGPU_M2L_I8_MIN: levels with fewer boxes use DMMA
     int64_t i8_small_boxes = 1024;     // PKGPU_I8_SMALL: levels up to this size share packed runs
-    int64_t i8_window = 65536;         // PKGPU_I8_WINDOW: columns per int8 M2L window (bounds R)
+    int64_t i8_window = 0;             // PKGPU_I8_WINDOW: columns per int8 M2L window (0: 65536, 8192 at p >= 10)
     I8Kernel i8_kernel = I8Kernel::automatic; // PKGPU_I8_KERNEL = single | dual | pairdual
     int i8_by_index = -1;              // PKGPU_I8_BYINDEX = 0 | 1: chunks as slot-index windows (-1: per kernel)
     int i8_tile_fast = -1;             // PKGPU_I8_TILEFAST = 0 | 1: unit order, column tile fastest
