@@ -125,12 +125,9 @@ __device__ __forceinline__ void accumulate_tt(const Stage<KERNEL> &S, const doub
         double ux[TT], uy[TT], uz[TT];
 #pragma unroll
         for (int k = 0; k < TT; k++) ux[k] = tx[k] - S.sx[s], uy[k] = ty[k] - S.sy[s], uz[k] = tz[k] - S.sz[s];
-        const int beg = S.begin[s], end = S.begin[s + 1];
-        // lane j takes the stage's sources q = j (mod G) across segment boundaries: every
-        // lane's share of the stage differs by at most one (per-segment round robin from
-        // each segment's start gave the low lanes one extra source in every short U leaf)
+        const int end = S.begin[s + 1];
 #pragma unroll 2
-        for (int q = beg + ((j - beg) % G + G) % G; q < end; q += G) {
+        for (int q = S.begin[s] + j; q < end; q += G) {
             const double sx = S.x[q], sy = S.y[q], sz = S.z[q];
 #pragma unroll
             for (int k = 0; k < TT; k++) {
