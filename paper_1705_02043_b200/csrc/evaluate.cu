@@ -1119,6 +1119,22 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
             if (l >= 1 && Lay.i8[l]) {
                 // M2L done above
+            } else if (l >= 1 && ctx.i8.fft) {
+                // M2L by FFT on the surface lattice (m2l_fft.h)
+                pm = prof.begin("m2l");
+                ctx.launches += m2l_fft_prepare(ops, ws, st);
+                FftLevelArgs fa;
+                fa.ncols = (int)(c1 - c0);
+                fa.out_box = Lay.out_box + c0;
+                fa.src = Lay.m2l_table + c0;
+                fa.ld = Lay.ncols;
+                fa.box0 = T.level_off[l];
+                fa.box1 = T.level_off[l + 1];
+                fa.X = Pup;
+                fa.Y = Q;
+                fa.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573)
+                ctx.launches += m2l_fft_level(ops, fa, ws, st);
+                prof.end(pm);
             } else if (l >= 1) {
                 GemmArgs a;
                 a.Kp = Kp;

@@ -1,0 +1,51 @@
+// FFT-accelerated M2L (the PVFMM scheme) for the V lists of
+// src/fmm.cpp:560-574: an alternative to the dense offset operators of src/fmm.cpp:135-175.
+//
+// The equivalent (source) and check (target) points of an M2L pair are the same surface
+// lattice (inner 1.05 surface, spacing 1.05 / (p - 1) at the root) around the two box
+// centres, so for a fixed cell offset d the operator is a convolution on the lattice:
+//   q_a(g_i) = sum_b sum_j k_{d,ab}(g_i - g_j) phi_b(g_j),  k_{d,ab}(dg) = K_ab(dg D - d)
+// (root scale; level l scales by 2^l, degree -1 kernels, as the dense path). On an N^3 grid,
+// N = 2p, the cyclic convolution equals the linear one at every surface point. Per level:
+//   phi_b of every source box scattered onto the grid, batched R2C FFTs (cuFFT);
+//   Q^_a(w) = sum over V entries sum_b K^_{d,ab}(w) Phi^_{src,b}(w)   (fft_hadamard_kernel);
+//   batched C2R FFTs, check potentials gathered at the surface points.
+// FP64 throughout (no fixed point); rounding differs from the dense product only at the
+// FFT's ~1e-15 relative level. K^ (316 offsets x kt x ks spectra) is built once per (kernel, p).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <vector>
+
+#include "common.h"
+
+namespace pkgpu {
+
+struct KifmmOps;
+
+struct FftOps {
+    int N = 0, nw = 0;               // grid edge 2p; half spectrum N * N * (N / 2 + 1)
+    double *khat = nullptr;          // [316][kt][ks][nw] complex (interleaved re, im)
+    int *gidx = nullptr;             // [n] grid index of surface point i
+    bool ready = false;
+    std::map<int, long long> plans_r2c, plans_c2r; // cufftHandle per batch size
+    ~FftOps();
+};
+
+struct FftLevelArgs {
+    int ncols = 0;               // multiple of 8
+    const int *out_box = nullptr; // [ncols] output box, -1 padding
+    const int *src = nullptr;     // [316 * ld] source box per (slot, column), -1 none
+    int64_t ld = 0;
+    int64_t box0 = 0, box1 = 0;   // the level's boxes (every source lies in [box0, box1))
+    const double *X = nullptr;    // phi_up [box][Kp]
+    double *Y = nullptr;          // q [box][Kp]: Y += alpha * M2L
+    double alpha = 1.0;
+};
+
+// builds K^ on first use; returns kernel launches
+int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st);
+int m2l_fft_level(KifmmOps &ops, const FftLevelArgs &a, Workspace &ws, cudaStream_t st);
+
+} // namespace pkgpu

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.h"
+#include "m2l_fft.h"
 #include "m2l_i8.h"
 
 namespace pkgpu {
@@ -38,6 +39,7 @@ struct KifmmOps {
     I8Operators i8;                         // M2L residues for the int8 tensor pipe (lazy)
     I8Operators i8_m2m, i8_l2l;             // M2M / L2L residues (lazy, i8_translate)
     I8Operators i8_ut_up, i8_v_up, i8_ut_dn, i8_v_dn; // pseudo-inverse factors (reset on upload)
+    FftOps fft;                             // M2L kernel spectra (lazy, the FFT M2L path)
     bool factors_ready = false, translations_ready = false;
 };
 

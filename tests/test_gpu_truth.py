@@ -41,7 +41,7 @@ def truth_error(pot, truth, kt, tp):
     return float(np.linalg.norm(d) / np.linalg.norm(truth))
 
 
-@pytest.mark.parametrize("path", ["int8", "dmma"])
+@pytest.mark.parametrize("path", ["int8", "dmma", "fft"])
 @pytest.mark.parametrize("case", CASES)
 def test_accuracy_vs_truth_no_worse_than_reference(case, path):
     g = load(f"eval_{case}.npz")
