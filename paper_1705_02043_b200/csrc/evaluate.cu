@@ -392,7 +392,8 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
             padded += (count[l * 8 + o] + BN - 1) / BN * BN;
             padded128 += (count[l * 8 + o] + 127) / 128 * 128;
         }
-        grouped[l] = padded * 189 <= (nl + BN - 1) / BN * BN * 316 ? 1 : 0;
+        // (the FFT M2L wants Morton order: 64-box tiles of compact blocks share their sources)
+        grouped[l] = !is.fft && padded * 189 <= (nl + BN - 1) / BN * BN * 316 ? 1 : 0;
         // 128-column DMMA M2L tiles (one 17-warp CTA per SM) measured slower than two
         // 64-column CTAs per SM on cfg2/3/4 (49.3 vs 46.3 ms M2L at cfg2): not used
         (void)padded128;

@@ -1,6 +1,7 @@
 // FFT-accelerated M2L (see m2l_fft.h).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <string>
 
 #include <cub/cub.cuh>
@@ -83,15 +84,18 @@ __global__ void fft_gather_kernel(const double *__restrict__ grid, const int *__
 
 // Q^[col][a][w] = sum_slots sum_b K^[slot][a][b][w] Phi^[map(src)][b][w]; a thread per
 // frequency, FFT_TC columns per CTA (one K^ read serves them all)
+// (only_tiles: the 64-column tiles with tile_nsrc < 0, whose sources overflowed the staging)
 template <int KS>
 __global__ void __launch_bounds__(FFT_THREADS) fft_hadamard_kernel(const double2 *__restrict__ khat,
                                                                    const double2 *__restrict__ phat,
                                                                    const int *__restrict__ smap,
                                                                    const int *__restrict__ table, int64_t ld,
-                                                                   int nw, double2 *__restrict__ qhat) {
+                                                                   int nw, double2 *__restrict__ qhat,
+                                                                   const int *__restrict__ only_tiles) {
     constexpr int KT = KS;
     const int w = blockIdx.x * FFT_THREADS + threadIdx.x;
     const int c0 = blockIdx.y * FFT_TC;
+    if (only_tiles && only_tiles[c0 / 64] >= 0) return;
     double2 acc[FFT_TC][KT];
 #pragma unroll
     for (int c = 0; c < FFT_TC; c++)
@@ -135,6 +139,185 @@ __global__ void __launch_bounds__(FFT_THREADS) fft_hadamard_kernel(const double2
         for (int a = 0; a < KT; a++) qhat[((int64_t)(c0 + c) * KT + a) * nw + w] = acc[c][a];
 }
 
+// ---------------------------------------------------------------------------
+// Source-staged accumulation (the main kernel). A tile is 64 consecutive target columns
+// (Morton order: a compact block of boxes whose V lists share most sources -- ~512 unique
+// sources for the 64 x 189 entries of a uniform level). fft_tile_sources_kernel dedups a
+// tile's sources (shared-memory hash) into tile_srcs and maps every (slot, target) entry to
+// its position there (srcmap, int16). fft_stage_kernel then runs one CTA per (tile, block of
+// 4 frequencies), two CTAs per SM: the tile's source spectra for those frequencies are
+// staged in shared memory once (chunks of 448 sources), the kernel spectra 32 slots at a
+// time, and every (target, slot) entry reads both from there -- the kernel spectrum of a
+// slot is the same address across a warp (32 targets, one frequency): a broadcast.
+constexpr int FT_TILE = 64;   // targets per tile
+constexpr int FT_WB = 4;      // frequencies per CTA (a warp of 32 targets per frequency)
+constexpr int FT_CH = 320;    // staged sources per chunk (Stokes: 320 x 13 x 16 B = 67 KB)
+constexpr int FT_SCH = 32;    // slots whose kernel spectra are staged at a time (18 KB)
+constexpr int FT_HS = 4096;   // dedup hash slots per tile
+constexpr int FT_MAXU = 3072; // unique sources per tile handled by staging (more: the direct kernel)
+constexpr int FT_THREADS = 256;
+
+__device__ __forceinline__ int ft_hash(int k) { return (int)(((unsigned)k * 2654435761u) >> 20) & (FT_HS - 1); }
+
+__global__ void __launch_bounds__(FT_THREADS) fft_tile_sources_kernel(const int *__restrict__ table, int64_t ld,
+                                                                       const int *__restrict__ smap, int *tile_nsrc,
+                                                                       int *tile_srcs, short *srcmap) {
+    __shared__ int keys[FT_HS], vals[FT_HS];
+    __shared__ int s_count, s_over;
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int c0 = tile * FT_TILE;
+    for (int h = tid; h < FT_HS; h += FT_THREADS) keys[h] = -1;
+    if (tid == 0) s_count = 0, s_over = 0;
+    __syncthreads();
+    constexpr int NE = kSlots * FT_TILE;
+    for (int e = tid; e < NE; e += FT_THREADS) {
+        const int b = table[(int64_t)(e / FT_TILE) * ld + c0 + e % FT_TILE];
+        if (b < 0) continue;
+        const int key = smap[b];
+        int h = ft_hash(key);
+        for (int probe = 0; probe < FT_HS; probe++) {
+            const int old = atomicCAS(&keys[h], -1, key);
+            if (old == -1 || old == key) break;
+            h = (h + 1) & (FT_HS - 1);
+        }
+    }
+    __syncthreads();
+    // positions in slot order of the hash table (deterministic for a given key set)
+    for (int h = tid; h < FT_HS; h += FT_THREADS)
+        if (keys[h] >= 0) {
+            const int idx = atomicAdd(&s_count, 1);
+            vals[h] = idx;
+        }
+    __syncthreads();
+    const int u = s_count;
+    if (u > FT_MAXU) {
+        if (tid == 0) tile_nsrc[tile] = -1; // too many: this tile takes the direct kernel
+        return;
+    }
+    for (int h = tid; h < FT_HS; h += FT_THREADS)
+        if (keys[h] >= 0) tile_srcs[(int64_t)tile * FT_MAXU + vals[h]] = keys[h];
+    for (int e = tid; e < NE; e += FT_THREADS) {
+        const int b = table[(int64_t)(e / FT_TILE) * ld + c0 + e % FT_TILE];
+        short v = -1;
+        if (b >= 0) {
+            const int key = smap[b];
+            int h = ft_hash(key);
+            while (keys[h] != key) h = (h + 1) & (FT_HS - 1);
+            v = (short)vals[h];
+        }
+        srcmap[(int64_t)tile * NE + e] = v;
+    }
+    if (tid == 0) tile_nsrc[tile] = u;
+}
+
+__device__ __forceinline__ void ft_cp16(void *smem, const void *gmem, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void ft_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void ft_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int KS>
+__global__ void __launch_bounds__(FT_THREADS, 2) fft_stage_kernel(const double2 *__restrict__ khat,
+                                                                   const double2 *__restrict__ phat,
+                                                                   const int *__restrict__ tile_nsrc,
+                                                                   const int *__restrict__ tile_srcs,
+                                                                   const short *__restrict__ srcmap, int nw,
+                                                                   double2 *__restrict__ qhat) {
+    constexpr int KT = KS;
+    constexpr int SST = KS * FT_WB + 1;            // source stride (double2): odd, so 32 random sources
+                                                   // spread over all eight 16-byte bank groups
+    constexpr int KCH = FT_SCH * KT * KS * FT_WB;  // double2 per kernel-spectrum chunk
+    constexpr int MCH = FT_SCH * FT_TILE / 8;      // srcmap chunk in 16-byte units (8 shorts)
+    extern __shared__ __align__(16) double2 ft_smem[];
+    double2 *stage = ft_smem;                      // [FT_CH][SST] source spectra
+    double2 *kst = stage + FT_CH * SST;            // 2 x [FT_SCH][KT][KS][FT_WB] kernel spectra
+    short *mst = reinterpret_cast<short *>(kst + 2 * KCH); // 2 x [FT_SCH][FT_TILE] source positions
+    const int tile = blockIdx.y, tid = threadIdx.x;
+    const int u = tile_nsrc[tile];
+    if (u < 0) return; // overflow tile: the direct kernel covers it
+    const int t = tid % FT_TILE, wl = tid / FT_TILE; // warp = 32 targets, one frequency
+    const int w0 = blockIdx.x * FT_WB, w = w0 + wl;
+    double2 acc[KT], acc2[KT];
+#pragma unroll
+    for (int a = 0; a < KT; a++) acc[a] = acc2[a] = make_double2(0.0, 0.0);
+    const short *smg = srcmap + (int64_t)tile * kSlots * FT_TILE;
+    constexpr int NSC = (kSlots + FT_SCH - 1) / FT_SCH;
+    auto load_chunk = [&](int c, int buf) { // kernel spectra + source positions of slot chunk c
+        const int s0 = c * FT_SCH, ns = min(FT_SCH, kSlots - s0);
+        double2 *kd = kst + buf * KCH;
+        for (int e = tid; e < ns * KT * KS * FT_WB; e += FT_THREADS) {
+            const int sab = e / FT_WB, ww = e % FT_WB;
+            const bool ok = w0 + ww < nw;
+            ft_cp16(kd + e, khat + ((int64_t)s0 * KT * KS + sab) * nw + (ok ? w0 + ww : 0), ok);
+        }
+        short *md = mst + buf * FT_SCH * FT_TILE;
+        for (int e = tid; e < ns * FT_TILE / 8; e += FT_THREADS) ft_cp16(md + 8 * e, smg + (int64_t)s0 * FT_TILE + 8 * e, true);
+    };
+    for (int k0 = 0; k0 < u; k0 += FT_CH) {
+        const int nk = min(FT_CH, u - k0);
+        __syncthreads(); // previous chunk's readers are done with the buffers
+        for (int e = tid; e < nk * KS * FT_WB; e += FT_THREADS) {
+            const int k = e / (KS * FT_WB), cw = e % (KS * FT_WB), c = cw / FT_WB, ww = cw % FT_WB;
+            const int src = tile_srcs[(int64_t)tile * FT_MAXU + k0 + k];
+            const bool ok = w0 + ww < nw;
+            ft_cp16(stage + k * SST + cw, phat + ((int64_t)src * KS + c) * nw + (ok ? w0 + ww : 0), ok);
+        }
+        load_chunk(0, 0);
+        ft_commit();
+        for (int c = 0; c < NSC; c++) {
+            if (c + 1 < NSC) load_chunk(c + 1, (c + 1) & 1);
+            ft_commit();
+            ft_wait<1>(); // chunk c (and the sources) landed
+            __syncthreads();
+            const int ns = min(FT_SCH, kSlots - c * FT_SCH);
+            const double2 *kb = kst + (c & 1) * KCH + wl;
+            const short *mb = mst + (c & 1) * FT_SCH * FT_TILE + t;
+            // two slots per step into two accumulator sets: twice the independent DFMA chains
+            // (the dependent chain per set is 2 KS DFMAs long; "wait" stalls dominated with one set)
+            for (int s = 0; s < ns; s += 2) {
+                const int li0 = (int)mb[s * FT_TILE] - k0;
+                const int li1 = s + 1 < ns ? (int)mb[(s + 1) * FT_TILE] - k0 : -1;
+                const bool on0 = li0 >= 0 && li0 < nk, on1 = li1 >= 0 && li1 < nk;
+                if (on0) {
+                    const double2 *st = stage + (int64_t)li0 * SST + wl;
+                    const double2 *kk = kb + (int64_t)s * KT * KS * FT_WB;
+#pragma unroll
+                    for (int b = 0; b < KS; b++) {
+                        const double2 p = st[b * FT_WB];
+#pragma unroll
+                        for (int a = 0; a < KT; a++) {
+                            const double2 k = kk[(a * KS + b) * FT_WB]; // same address across the warp
+                            acc[a].x = fma(k.x, p.x, fma(-k.y, p.y, acc[a].x));
+                            acc[a].y = fma(k.x, p.y, fma(k.y, p.x, acc[a].y));
+                        }
+                    }
+                }
+                if (on1) {
+                    const double2 *st = stage + (int64_t)li1 * SST + wl;
+                    const double2 *kk = kb + (int64_t)(s + 1) * KT * KS * FT_WB;
+#pragma unroll
+                    for (int b = 0; b < KS; b++) {
+                        const double2 p = st[b * FT_WB];
+#pragma unroll
+                        for (int a = 0; a < KT; a++) {
+                            const double2 k = kk[(a * KS + b) * FT_WB];
+                            acc2[a].x = fma(k.x, p.x, fma(-k.y, p.y, acc2[a].x));
+                            acc2[a].y = fma(k.x, p.y, fma(k.y, p.x, acc2[a].y));
+                        }
+                    }
+                }
+            }
+            __syncthreads(); // chunk c's buffers are refilled two chunks later
+        }
+    }
+    if (w >= nw) return;
+    const int col = tile * FT_TILE + t;
+#pragma unroll
+    for (int a = 0; a < KT; a++)
+        qhat[((int64_t)col * KT + a) * nw + w] = make_double2(acc[a].x + acc2[a].x, acc[a].y + acc2[a].y);
+}
+
 // unique source boxes of a window: flags over the level's boxes
 __global__ void fft_mark_kernel(const int *__restrict__ table, int64_t ld, int ncols, int64_t box0, int *flags) {
     const int64_t total = (int64_t)kSlots * ncols;
@@ -152,6 +335,18 @@ __global__ void fft_map_kernel(const int *__restrict__ list, int n, int64_t box0
 __global__ void offset_list_kernel(int *list, int n, int64_t box0) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) list[k] += (int)box0;
+}
+
+template <class F> void set_smem_once(F *kernel, size_t bytes) {
+    static std::mutex mtx;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    int dev = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mtx);
+    size_t &d = done[{reinterpret_cast<const void *>(kernel), dev}];
+    if (d >= bytes) return;
+    PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    d = bytes;
 }
 
 cufftHandle plan_for(std::map<int, long long> &cache, int N, int batch, bool r2c) {
@@ -210,14 +405,14 @@ int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st) {
 
 int m2l_fft_level(KifmmOps &ops, const FftLevelArgs &a, Workspace &ws, cudaStream_t st) {
     if (a.ncols == 0) return 0;
-    if (a.ncols % FFT_TC != 0) throw RuntimeError("m2l_fft: columns must be a multiple of 8");
+    if (a.ncols % FT_TILE != 0) throw RuntimeError("m2l_fft: columns must be a multiple of 64");
     FftOps &f = ops.fft;
     const int ks = ops.ks, kt = ops.kt, n = ops.n;
     const int64_t N3 = (int64_t)f.N * f.N * f.N, nlev = a.box1 - a.box0;
     int launches = 0;
     // columns per window: spectra of the window's targets and of their (unique) sources
     const int64_t per_col = (int64_t)(kt + 2 * ks) * (f.nw * 16 + N3 * 8);
-    const int W = (int)std::max<int64_t>(FFT_TC, std::min<int64_t>(a.ncols, (int64_t)12e9 / per_col) / FFT_TC * FFT_TC);
+    const int W = (int)std::max<int64_t>(FT_TILE, std::min<int64_t>(a.ncols, (int64_t)12e9 / per_col) / FT_TILE * FT_TILE);
     int *flags = ws.get<int>("fft_flags", nlev), *list = ws.get<int>("fft_list", nlev), *cnt = ws.get<int>("fft_cnt", 1);
     int *smap = ws.get<int>("fft_smap", nlev);
     PK_CUDA(cudaMemsetAsync(smap, 0xff, nlev * sizeof(int), st));
@@ -250,17 +445,36 @@ int m2l_fft_level(KifmmOps &ops, const FftLevelArgs &a, Workspace &ws, cudaStrea
             a.X, ops.Kp, list, nsrc, n, ks, f.gidx, N3, gin);
         double *phat = ws.get<double>("fft_phat", ngs * f.nw * 2);
         exec_batched(f, true, gin, phat, ngs, st);
-        // frequency-domain accumulation over the V lists
+        // frequency-domain accumulation over the V lists: source-staged tiles of 64 targets,
+        // the direct kernel for tiles whose sources overflow the staging
         double *qhat = ws.get<double>("fft_qhat", (int64_t)wc * kt * f.nw * 2);
+        const int ntiles = wc / FT_TILE;
+        int *tile_nsrc = ws.get<int>("fft_tile_nsrc", ntiles);
+        int *tile_srcs = ws.get<int>("fft_tile_srcs", (int64_t)ntiles * FT_MAXU);
+        short *srcmap = ws.get<short>("fft_srcmap", (int64_t)ntiles * kSlots * FT_TILE);
+        fft_tile_sources_kernel<<<ntiles, FT_THREADS, 0, st>>>(tab, a.ld, smap_abs, tile_nsrc, tile_srcs, srcmap);
+        const dim3 sgrid((f.nw + FT_WB - 1) / FT_WB, ntiles);
+        const size_t ssm = ((size_t)FT_CH * (ks * FT_WB + 1) + 2 * FT_SCH * kt * ks * FT_WB) * sizeof(double2) +
+                           2 * FT_SCH * FT_TILE * sizeof(short);
         const dim3 grid((f.nw + FFT_THREADS - 1) / FFT_THREADS, wc / FFT_TC);
-        if (ks == 1)
+        if (ks == 1) {
+            set_smem_once(fft_stage_kernel<1>, ssm);
+            fft_stage_kernel<1><<<sgrid, FT_THREADS, ssm, st>>>(reinterpret_cast<const double2 *>(f.khat),
+                                                                reinterpret_cast<const double2 *>(phat), tile_nsrc,
+                                                                tile_srcs, srcmap, f.nw, reinterpret_cast<double2 *>(qhat));
             fft_hadamard_kernel<1><<<grid, FFT_THREADS, 0, st>>>(reinterpret_cast<const double2 *>(f.khat),
                                                                  reinterpret_cast<const double2 *>(phat), smap_abs, tab,
-                                                                 a.ld, f.nw, reinterpret_cast<double2 *>(qhat));
-        else
+                                                                 a.ld, f.nw, reinterpret_cast<double2 *>(qhat), tile_nsrc);
+        } else {
+            set_smem_once(fft_stage_kernel<3>, ssm);
+            fft_stage_kernel<3><<<sgrid, FT_THREADS, ssm, st>>>(reinterpret_cast<const double2 *>(f.khat),
+                                                                reinterpret_cast<const double2 *>(phat), tile_nsrc,
+                                                                tile_srcs, srcmap, f.nw, reinterpret_cast<double2 *>(qhat));
             fft_hadamard_kernel<3><<<grid, FFT_THREADS, 0, st>>>(reinterpret_cast<const double2 *>(f.khat),
                                                                  reinterpret_cast<const double2 *>(phat), smap_abs, tab,
-                                                                 a.ld, f.nw, reinterpret_cast<double2 *>(qhat));
+                                                                 a.ld, f.nw, reinterpret_cast<double2 *>(qhat), tile_nsrc);
+        }
+        launches += 3;
         // inverse, then the check potentials at the surface points (1 / N^3: cuFFT is unnormalised)
         double *gout = ws.get<double>("fft_gout", (int64_t)wc * kt * N3);
         exec_batched(f, false, qhat, gout, (int64_t)wc * kt, st);

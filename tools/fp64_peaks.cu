@@ -36,6 +36,28 @@ __global__ void dfma_loop(double *out, int iters, double a, double b) {
     if (s == 12345.678) out[0] = s;
 }
 
+// the same with three per-thread (vector-register) operands, as a real kernel's DFMA has:
+// x_i = fma(x_i, y_i, z_i), y and z rotating through registers
+__global__ void dfma3_loop(double *out, int iters, double a, double b) {
+    double x[8], y[8], z[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        x[k] = threadIdx.x * 1e-9 + k;
+        y[k] = a + k * 1e-12 + threadIdx.x * 1e-15;
+        z[k] = b + k * 1e-13;
+    }
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+#pragma unroll
+            for (int k = 0; k < 8; k++) x[k] = fma(x[k], y[(k + j) & 7], z[(k + 3 * j) & 7]);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += x[k];
+    if (s == 12345.678) out[0] = s;
+}
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
@@ -86,6 +108,18 @@ int main() {
         CK(cudaEventSynchronize(e1));
         cudaEventElapsedTime(&ms, e0, e1);
         const double flops = 2.0 * 16 * 8 * (double)iters * threads * blocks;
+        {
+            dfma3_loop<<<blocks, threads>>>(dout, 10, 1.0000001, 1e-9);
+            CK(cudaEventRecord(e0));
+            dfma3_loop<<<blocks, threads>>>(dout, iters, 1.0000001, 1e-9);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms3 = 0;
+            CK(cudaEventElapsedTime(&ms3, e0, e1));
+            const double fl3 = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+            printf("{\"kind\": \"dfma_3vec\", \"blocks_per_sm\": %d, \"tflops\": %.3f, \"ms\": %.3f}\n", occ,
+                   fl3 / (ms3 * 1e-3) / 1e12, ms3);
+        }
         printf("{\"kind\": \"dfma\", \"blocks_per_sm\": %d, \"tflops\": %.3f, \"ms\": %.3f}\n", occ,
                flops / (ms * 1e-3) / 1e12, ms);
     }
