@@ -478,9 +478,12 @@ class Context:
         """M2L arithmetic: "int8" (exact residue GEMMs on the int8 tensor pipe for levels
         with >= min_boxes boxes, FP64 DMMA elsewhere; the default) or "dmma" (FP64 DMMA
         everywhere) or "int8_all" (as "int8", plus M2M / L2L / pseudo-inverses on the int8
-        pipe) or "fft" (FP64 FFT convolution on the surface lattice, the PVFMM scheme).
+        pipe) or "fft" (FP64 FFT convolution on the surface lattice, the PVFMM scheme) or
+        "int8_dense" (as "int8" without the lattice FFT M2L). Except with "dmma" and
+        "int8_dense", levels whose box lattice is filled run M2L as one convolution over the
+        lattice (surface FFT x lattice FFT, FP64; PKGPU_M2L_LATTICE=0 disables it).
         nmod / beta_a / beta_b override the residue parameters."""
-        code = {"int8": 0, "dmma": 1, "int8_all": 2, "fft": 3}[path]
+        code = {"int8": 0, "dmma": 1, "int8_all": 2, "fft": 3, "int8_dense": 4}[path]
         if lib().pkgpu_context_set_m2l(self._h, code, int(min_boxes), int(nmod), int(beta_a), int(beta_b)) != 0:
             raise ValueError(f"set_m2l: invalid settings {path, min_boxes, nmod, beta_a, beta_b}")
 

@@ -13,6 +13,7 @@
 #include "context.h"
 #include "gemm.h"
 #include "periodize.h"
+#include "tuning.h"
 
 using namespace pkgpu;
 
@@ -309,12 +310,13 @@ pkgpu_status pkgpu_context_set_profiling(pkgpu_context *ctx, int on) {
 
 pkgpu_status pkgpu_context_set_m2l(pkgpu_context *ctx, int path, int64_t min_boxes, int nmod, int beta_a,
                                    int beta_b) {
-    if (path < 0 || path > 3 || (nmod > 0 && (nmod < 14 || nmod > kI8MaxModuli))) return PKGPU_INVALID_ARGUMENT;
+    if (path < 0 || path > 4 || (nmod > 0 && (nmod < 14 || nmod > kI8MaxModuli))) return PKGPU_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lock(ctx->mtx);
     I8Settings &s = ctx->i8;
-    s.enabled = path == 0 || path == 2;
+    s.enabled = path == 0 || path == 2 || path == 4;
     s.trans = path == 2;
     s.fft = path == 3;
+    s.lattice = (path == 0 || path == 2 || path == 3) && tuning().m2l_lattice;
     if (min_boxes > 0) s.min_boxes = min_boxes;
     if (nmod > 0) s.nmod = nmod;
     if (beta_a > 0) s.beta_a = beta_a;

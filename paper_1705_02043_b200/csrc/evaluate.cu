@@ -10,6 +10,8 @@
 // All device work is on the context stream; timings are CUDA events.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 
@@ -321,6 +323,7 @@ struct Layout {
     int i8[kMaxLevels + 1] = {0};                  // M2L on the int8 tensor pipe (256-column tiles)
     int i8_last[kMaxLevels + 1] = {0};             // int8 run starting at this level ends at i8_last
     int i8_big[kMaxLevels + 1] = {0};              // ... and is one big level (dual-tile kernel)
+    int lat[kMaxLevels + 1] = {0};                 // M2L by the lattice FFT (m2l_lattice_level)
     int64_t ncols = 0, noct = 0, nm2m = 0;
     int *col_of_box = nullptr, *out_box = nullptr, *out_m2m = nullptr, *m2m_src = nullptr, *m2l_table = nullptr;
     int *out_oct = nullptr, *l2l_src = nullptr, *tile_oct = nullptr;
@@ -349,7 +352,7 @@ __global__ void l2l_src8_kernel(const int *__restrict__ l2l_src, const int *__re
 // pairs than Morton order with (nearly) all 316 offsets active. L2L always uses the
 // octant layout so each tile has a single L2L matrix. M2M gets its own compact layout
 // of internal boxes with sources.
-Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cudaStream_t st) {
+Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, const int *lat, cudaStream_t st) {
     Workspace &ws = ctx.ws;
     const int nb = (int)T.nboxes;
     const TreeView tv = T.view();
@@ -379,8 +382,10 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, cu
     const int64_t small_max = tuning().i8_small_boxes;
     const I8Settings &is = ctx.i8;
     auto i8_level = [&](int lv) {
-        return is.enabled && lv >= 1 && lv <= T.depth && T.level_off[lv + 1] - T.level_off[lv] >= is.min_boxes;
+        return is.enabled && lv >= 1 && lv <= T.depth && !lat[lv] &&
+               T.level_off[lv + 1] - T.level_off[lv] >= is.min_boxes;
     };
+    for (int l = 0; l <= T.depth; l++) L.lat[l] = lat[l];
     auto small_level = [&](int lv) { return T.level_off[lv + 1] - T.level_off[lv] <= small_max; };
     int run_first = -1; // first level of the int8 run being laid out
     for (int l = 0; l <= T.depth; l++) {
@@ -943,12 +948,57 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             small_or_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(T.view(), Part.in, small_max, lmask);
             ctx.launches++;
         }
-        Layout Lay = build_layout(ctx, T, lmask, st);
         ListSetup ls{};
         if (periodic && ell >= 1)
             for (int a = 0; a < 3; a++) ls.periodic[a] = axes[a];
+        // levels whose M2L runs as a lattice convolution (m2l_fft.h): filled lattices within
+        // the device budget, single-rank runs
+        int lat[kMaxLevels + 1] = {0};
+        if (ctx.i8.lattice && !partitioned) {
+            const Tuning &tu = tuning();
+            int64_t used = 0;
+            for (int l = 1; l <= T.depth; l++) {
+                const double cells = std::ldexp(1.0, 3 * l);
+                const int64_t nl = T.level_off[l + 1] - T.level_off[l];
+                const int64_t bytes = m2l_lattice_bytes(ops, l, ls.periodic);
+                if (nl >= tu.lattice_fill * cells && used + bytes <= tu.lattice_budget) {
+                    lat[l] = 1;
+                    used += bytes;
+                }
+            }
+        }
+        Layout Lay = build_layout(ctx, T, lmask, lat, st);
         build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
                          &ctx.launches, lmask);
+        // the lattice levels' V lists must be exactly the stencil (they are for filled levels;
+        // a level that is not falls back to the dense product)
+        if (std::any_of(Lay.lat, Lay.lat + T.depth + 1, [](int v) { return v != 0; })) {
+            ctx.launches += m2l_fft_prepare(ops, ws, st);
+            int *bad = ws.get<int>("lat_bad", kMaxLevels + 1);
+            PK_CUDA(cudaMemsetAsync(bad, 0, (kMaxLevels + 1) * sizeof(int), st));
+            for (int l = 1; l <= T.depth; l++) {
+                if (!Lay.lat[l]) continue;
+                LatticeLevelArgs la;
+                la.level = l;
+                for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
+                la.box0 = T.level_off[l];
+                la.box1 = T.level_off[l + 1];
+                la.cell = T.cell;
+                ctx.launches += m2l_lattice_check(ops, la, Lay.m2l_table + Lay.colbase[l], Lay.ncols,
+                                                  Lay.out_box + Lay.colbase[l],
+                                                  (int)(Lay.colbase[l + 1] - Lay.colbase[l]), bad + l, ws, st);
+            }
+            int hb[kMaxLevels + 1];
+            PK_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, st));
+            PK_CUDA(cudaStreamSynchronize(st));
+            static const bool dbg = std::getenv("PKGPU_LATTICE_DEBUG") != nullptr;
+            for (int l = 1; l <= T.depth; l++) {
+                if (dbg && Lay.lat[l])
+                    std::fprintf(stderr, "lattice level %d: %lld boxes, %d V-list mismatches\n", l,
+                                 (long long)(T.level_off[l + 1] - T.level_off[l]), hb[l]);
+                if (Lay.lat[l] && hb[l]) Lay.lat[l] = 0; // dense fallback (DMMA)
+            }
+        }
         prof.end(pm);
         // pseudo-inverse scratch: one level at a time (indexed by box id through a level offset)
         int64_t maxlev = 1;
@@ -1118,7 +1168,21 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         for (int l = 0; l <= T.depth; l++) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (l >= 1 && Lay.i8[l]) {
+            if (l >= 1 && Lay.lat[l]) {
+                // M2L as a convolution on the level's lattice (m2l_fft.h)
+                pm = prof.begin("m2l");
+                LatticeLevelArgs la;
+                la.level = l;
+                for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
+                la.box0 = lo;
+                la.box1 = hi;
+                la.cell = T.cell;
+                la.X = Pup;
+                la.Y = Q;
+                la.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573)
+                ctx.launches += m2l_lattice_level(ops, la, ws, st);
+                prof.end(pm);
+            } else if (l >= 1 && Lay.i8[l]) {
                 // M2L done above
             } else if (l >= 1 && ctx.i8.fft) {
                 // M2L by FFT on the surface lattice (m2l_fft.h)

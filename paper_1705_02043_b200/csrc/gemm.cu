@@ -57,7 +57,7 @@ struct KParams {
     const int *tile_nact;   // [coltiles] (null: every tile has the one slot of an identity gather)
     int rowtiles, coltiles; // unit = row + rowtiles * (col + coltiles * split)
     int total_units;
-    int *counter;           // persistent scheduler
+    int *counter;           // persistent scheduler (self-resetting: the CTA taking the last fetch zeroes it)
 };
 
 struct TmaParams {
@@ -96,14 +96,9 @@ __global__ void slot_scan_kernel(GemmArgs a, int bn, int *tile_slots, int *tile_
     }
 }
 
-// epilogue of one accumulator element (row r, column c)
-__device__ __forceinline__ void store_out(const KParams &kp, int split, int r, int c, double v) {
-    const GemmArgs &a = kp.a;
+// epilogue of one output element (row r, column c) from its full sum
+__device__ __forceinline__ void store_final(const GemmArgs &a, int r, int c, double v) {
     if (r >= a.Kp) return; // zero-filled operator rows of the last row tile
-    if (kp.nsplit > 1) {
-        kp.part[((int64_t)split * a.ncols + c) * a.Kp + r] = v;
-        return;
-    }
     const int ob = col_out(a, c);
     if (ob < 0) return;
     double *y = a.Y + (int64_t)ob * a.Kp + r;
@@ -113,6 +108,15 @@ __device__ __forceinline__ void store_out(const KParams &kp, int split, int r, i
     } else {
         *y = (a.beta != 0.0 ? a.beta * *y : 0.0) + a.alpha * v;
     }
+}
+
+// epilogue of one accumulator element: a split unit's partial, or the final value
+__device__ __forceinline__ void store_out(const KParams &kp, int split, int r, int c, double v) {
+    if (kp.nsplit > 1) {
+        if (r < kp.a.Kp) kp.part[((int64_t)split * kp.a.ncols + c) * kp.a.Kp + r] = v;
+        return;
+    }
+    store_final(kp.a, r, c, v);
 }
 
 __device__ __forceinline__ void unit_range(const KParams &kp, int nact, int split, int &it0, int &it1) {
@@ -174,7 +178,13 @@ __global__ void __maxnreg__(96)
 
     int g = 0; // pipeline iterations issued/consumed so far by this CTA (stage ring position)
     for (;;) {
-        if (tid == 0) s_unit = atomicAdd(kp.counter, 1);
+        if (tid == 0) {
+            const int u = atomicAdd(kp.counter, 1);
+            // every CTA ends on one failed fetch: total_units + gridDim.x fetches in all, so the
+            // last one leaves the counter at zero for the next launch on the stream
+            if (u == kp.total_units + (int)gridDim.x - 1) *kp.counter = 0;
+            s_unit = u;
+        }
         __syncthreads();
         const int unit = s_unit;
         __syncthreads();
@@ -348,6 +358,16 @@ CUtensorMap operator_map(const double *A, int nmat, int Kp, int BM) {
     return cache.emplace(key, m).first->second;
 }
 
+// int counters that every launch leaves at zero: zeroed here only when (re)allocated
+int *zeroed_counters(Workspace &ws, const char *name, size_t n, cudaStream_t st) {
+    auto &b = ws.bufs[name];
+    if (!b) b = std::make_unique<DevBuf>();
+    const size_t before = b->bytes;
+    int *p = b->as<int>(n);
+    if (b->bytes != before) PK_CUDA(cudaMemsetAsync(p, 0, b->bytes, st)); // new allocation
+    return p;
+}
+
 } // namespace
 
 int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) {
@@ -393,8 +413,7 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
         kp.tile_nact = tnact;
         launches = 1;
     }
-    kp.counter = ws.get<int>("gemm_counter", 1);
-    PK_CUDA(cudaMemsetAsync(kp.counter, 0, sizeof(int), st));
+    kp.counter = zeroed_counters(ws, "gemm_counter", 1, st);
     TmaParams tp;
     std::memset(&tp, 0, sizeof tp);
     tp.kp = kp;

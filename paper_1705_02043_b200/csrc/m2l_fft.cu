@@ -1,8 +1,11 @@
 // FFT-accelerated M2L (see m2l_fft.h).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 #include <cufft.h>
@@ -24,6 +27,8 @@ namespace pkgpu {
 FftOps::~FftOps() {
     for (auto &kv : plans_r2c) cufftDestroy((cufftHandle)kv.second);
     for (auto &kv : plans_c2r) cufftDestroy((cufftHandle)kv.second);
+    for (auto &kv : lattice)
+        if (kv.second.plan >= 0) cufftDestroy((cufftHandle)kv.second.plan);
 }
 
 namespace {
@@ -376,6 +381,567 @@ void exec_batched(FftOps &f, bool r2c, void *in, void *out, int64_t nbatch, cuda
 }
 
 } // namespace
+
+
+namespace {
+
+constexpr int LAT_E = 14; // stored offset classes e = c - o with code (ex+1) 9 + (ey+1) 3 + (ez+1) >= 13
+
+__host__ __device__ inline int sym_index(int a, int b, int ks) { // (a, b) -> packed upper triangle
+    if (a > b) {
+        const int t = a;
+        a = b;
+        b = t;
+    }
+    return ks == 1 ? 0 : (a == 0 ? b : (a == 1 ? 2 + b : 5));
+}
+
+// M[kappa][e'][comp][w] = sum_{D, |2D + e| >= 2} K^_{2D+e}[a][b][w] exp(+2 pi i kappa.D / m)
+__global__ void lat_build_kernel(const double2 *__restrict__ khat, const int *__restrict__ slot_of_code, int ks,
+                                 int nw, int mx, int my, int mz, double2 *__restrict__ M) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nc = ks * (ks + 1) / 2;
+    const int ec = blockIdx.y / nc, comp = blockIdx.y % nc;
+    const int64_t kap = blockIdx.z;
+    if (w >= nw) return;
+    int a = 0, b = 0;
+    if (ks == 3) {
+        const int A[6] = {0, 0, 0, 1, 1, 2}, B[6] = {0, 1, 2, 1, 2, 2};
+        a = A[comp];
+        b = B[comp];
+    }
+    const int code = 13 + ec;
+    const int ex = code / 9 - 1, ey = (code / 3) % 3 - 1, ez = code % 3 - 1;
+    const int kx = (int)(kap / ((int64_t)my * mz)), ky = (int)((kap / mz) % my), kz = (int)(kap % mz);
+    double re = 0.0, im = 0.0;
+    for (int Dx = -1; Dx <= 1; Dx++)
+        for (int Dy = -1; Dy <= 1; Dy++)
+            for (int Dz = -1; Dz <= 1; Dz++) {
+                const int dx = 2 * Dx + ex, dy = 2 * Dy + ey, dz = 2 * Dz + ez;
+                if (max(abs(dx), max(abs(dy), abs(dz))) < 2) continue; // adjacent: U / W / X lists
+                const int slot = slot_of_code[(dx + 3) * 49 + (dy + 3) * 7 + (dz + 3)];
+                const double2 k = khat[((int64_t)(slot * ks + a) * ks + b) * nw + w];
+                // exp(+2 pi i (kx Dx / mx + ky Dy / my + kz Dz / mz)), exact for the period
+                const double ph = (double)kx * Dx / mx + (double)ky * Dy / my + (double)kz * Dz / mz;
+                double s, c;
+                sincospi(2.0 * ph, &s, &c);
+                re += k.x * c - k.y * s;
+                im += k.x * s + k.y * c;
+            }
+    M[((kap * LAT_E + ec) * nc + comp) * nw + w] = make_double2(re, im);
+}
+
+// box of each (parent-lattice point u, octant c); -1 for absent boxes and padding
+__global__ void lat_boxmap_kernel(const int4 *__restrict__ cell, int64_t box0, int64_t nl, int my, int mz,
+                                  int *__restrict__ box_of) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nl) return;
+    const int4 c = cell[box0 + k];
+    const int64_t u = ((int64_t)(c.x >> 1) * my + (c.y >> 1)) * mz + (c.z >> 1);
+    box_of[u * 8 + ((c.x & 1) | (c.y & 1) << 1 | (c.z & 1) << 2)] = (int)(box0 + k);
+}
+
+// the dense layout's V-list entries against the lattice stencil: bad += mismatches, plus
+// level boxes that are not output columns
+__global__ void lat_check_kernel(const int *__restrict__ table, int64_t ld, const int *__restrict__ out_box, int ncols,
+                                 const int *__restrict__ code_of_slot, const int4 *__restrict__ cell,
+                                 const int *__restrict__ box_of, int n, int px, int py, int pz, int my, int mz,
+                                 int64_t box0, int64_t nl, int *__restrict__ seen, int *bad, int *dbg) {
+    const int64_t total = (int64_t)kNumM2L * ncols;
+    int nbad = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(t / ncols), col = (int)(t % ncols);
+        const int tb = out_box[col];
+        const int got = table[(int64_t)s * ld + col];
+        if (tb < 0) {
+            nbad += got >= 0;
+            continue;
+        }
+        if (tb < box0 || tb >= box0 + nl) { // not a box of this level
+            nbad++;
+            continue;
+        }
+        if (s == 0) seen[tb - box0] = 1;
+        const int code = code_of_slot[s];
+        const int4 c = cell[tb];
+        const int dx = code / 49 - 3, dy = (code / 7) % 7 - 3, dz = code % 7 - 3;
+        int x = c.x + dx, y = c.y + dy, z = c.z + dz;
+        int want = -1;
+        // the octant's stencil: the parents adjacent, d + o in [-2, 3] per axis
+        bool in = dx + (c.x & 1) >= -2 && dx + (c.x & 1) <= 3 && dy + (c.y & 1) >= -2 && dy + (c.y & 1) <= 3 &&
+                  dz + (c.z & 1) >= -2 && dz + (c.z & 1) <= 3;
+        if (px) x = ((x % n) + n) % n; else in &= x >= 0 && x < n;
+        if (py) y = ((y % n) + n) % n; else in &= y >= 0 && y < n;
+        if (pz) z = ((z % n) + n) % n; else in &= z >= 0 && z < n;
+        if (in) want = box_of[(((int64_t)(x >> 1) * my + (y >> 1)) * mz + (z >> 1)) * 8 + ((x & 1) | (y & 1) << 1 | (z & 1) << 2)];
+        if (want != got) {
+            nbad++;
+            if (dbg) {
+                const int k = atomicAdd(dbg, 1);
+                if (k < 8) {
+                    dbg[1 + 4 * k] = s;
+                    dbg[2 + 4 * k] = tb;
+                    dbg[3 + 4 * k] = want;
+                    dbg[4 + 4 * k] = got;
+                }
+            }
+        }
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+__global__ void lat_seen_kernel(const int *__restrict__ seen, int64_t nl, int *bad) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < nl && !seen[k]) atomicAdd(bad, 1);
+}
+
+// Q~[kappa][o][a][w] = sum_c sum_b M_{c-o}[a][b](kappa, w) Psi~[kappa][c][b][w]; a thread per
+// (kappa, w), the 8 octants' spectra in shared memory, the 8 outputs in registers; each
+// offset class e is loaded once and applied to every (o, c) pair with c - o = e
+template <int KS>
+__global__ void __launch_bounds__(128) lat_mul_kernel(const double2 *__restrict__ M, const double2 *__restrict__ Psi,
+                                                      double2 *__restrict__ Q, int nw) {
+    constexpr int NC = KS * (KS + 1) / 2;
+    __shared__ double2 ps[8 * KS][128];
+    const int w = blockIdx.x * 128 + threadIdx.x;
+    const int64_t kap = blockIdx.y;
+    const bool on = w < nw;
+    const int64_t base = kap * 8 * KS * nw;
+#pragma unroll
+    for (int j = 0; j < 8 * KS; j++) ps[j][threadIdx.x] = on ? Psi[base + (int64_t)j * nw + w] : make_double2(0.0, 0.0);
+    double2 acc[8][KS];
+#pragma unroll
+    for (int o = 0; o < 8; o++)
+#pragma unroll
+        for (int a = 0; a < KS; a++) acc[o][a] = make_double2(0.0, 0.0);
+    // one offset class e (code) with its spectra m (conjugated for -e)
+    auto apply = [&](int code, const double2 (&m)[NC], bool cj) {
+        const int ex = code / 9 - 1, ey = (code / 3) % 3 - 1, ez = code % 3 - 1;
+        const double sg = cj ? -1.0 : 1.0;
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int cx = (o & 1) + ex, cy = ((o >> 1) & 1) + ey, cz = ((o >> 2) & 1) + ez;
+            if (cx < 0 || cx > 1 || cy < 0 || cy > 1 || cz < 0 || cz > 1) continue;
+            const int c = cx | cy << 1 | cz << 2;
+#pragma unroll
+            for (int b = 0; b < KS; b++) {
+                const double2 p = ps[c * KS + b][threadIdx.x];
+#pragma unroll
+                for (int a = 0; a < KS; a++) {
+                    const double2 k = m[sym_index(a, b, KS)];
+                    const double ky = sg * k.y;
+                    acc[o][a].x = fma(k.x, p.x, fma(-ky, p.y, acc[o][a].x));
+                    acc[o][a].y = fma(k.x, p.y, fma(ky, p.x, acc[o][a].y));
+                }
+            }
+        }
+    };
+    if (on) {
+        // each stored class serves e and -e (M_{-e} = conj(M_e)): one load per class
+        for (int ec = 0; ec < LAT_E; ec++) {
+            double2 m[NC];
+#pragma unroll
+            for (int k = 0; k < NC; k++) m[k] = M[((kap * LAT_E + ec) * NC + k) * nw + w];
+            apply(13 + ec, m, false);
+            if (ec) apply(13 - ec, m, true);
+        }
+    }
+    if (!on) return;
+#pragma unroll
+    for (int o = 0; o < 8; o++)
+#pragma unroll
+        for (int a = 0; a < KS; a++) Q[base + (int64_t)(o * KS + a) * nw + w] = acc[o][a];
+}
+
+// In-register radix-2 FFT of M points (M a power of two <= 32), sign -1 forward / +1 inverse
+__host__ __device__ constexpr int bit_reverse(int i, int M) {
+    int r = 0;
+    for (int b = 1; b < M; b <<= 1) r = (r << 1) | ((i & b) ? 1 : 0);
+    return r;
+}
+template <int M> __device__ __forceinline__ void reg_fft(double2 (&v)[M], double sign) {
+#pragma unroll
+    for (int i = 0; i < M; i++) { // bit reversal (compile-time indices)
+        const int j = bit_reverse(i, M);
+        if (i < j) {
+            const double2 t = v[i];
+            v[i] = v[j];
+            v[j] = t;
+        }
+    }
+#pragma unroll
+    for (int len = 2; len <= M; len <<= 1) {
+#pragma unroll
+        for (int k = 0; k < len / 2; k++) {
+            double s, c;
+            sincospi(sign * 2.0 * k / len, &s, &c);
+#pragma unroll
+            for (int i = 0; i < M; i += len) {
+                const double2 a = v[i + k], b = v[i + k + len / 2];
+                const double2 t = make_double2(b.x * c - b.y * s, b.x * s + b.y * c);
+                v[i + k] = make_double2(a.x + t.x, a.y + t.y);
+                v[i + k + len / 2] = make_double2(a.x - t.x, a.y - t.y);
+            }
+        }
+    }
+}
+
+// One axis of the 3D lattice transform, in place: X[u][j] (j fastest, S columns); a thread
+// per (column j, line along the axis), M points per line at u stride `ustride`
+template <int M>
+__global__ void __launch_bounds__(128) lat_fft_axis_kernel(double2 *__restrict__ X, int64_t S, int64_t nlines,
+                                                           int64_t ustride, int64_t inner, double sign) {
+    const int64_t j = blockIdx.x * 128 + threadIdx.x;
+    const int64_t line = blockIdx.y;
+    if (j >= S) return;
+    // line -> base u: lines enumerate (outer, inner) around the axis
+    const int64_t u0 = (line / inner) * (inner * M) + (line % inner);
+    double2 v[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) v[i] = X[(u0 + i * ustride) * S + j];
+    reg_fft<M>(v, sign);
+#pragma unroll
+    for (int i = 0; i < M; i++) X[(u0 + i * ustride) * S + j] = v[i];
+    (void)nlines;
+}
+
+// the whole 3D transform of small lattices (M3 <= 512) in shared memory: a CTA per block of
+// JB consecutive columns, one read and one write of the data
+template <int MX, int MY, int MZ, int JB>
+__global__ void __launch_bounds__(256) lat_fft_smem_kernel(double2 *__restrict__ X, int64_t S, double sign) {
+    constexpr int M3 = MX * MY * MZ;
+    extern __shared__ double2 lat_sm[]; // [M3][JB]
+    const int64_t j0 = (int64_t)blockIdx.x * JB;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < M3 * JB; e += 256) {
+        const int u = e / JB, jj = e % JB;
+        lat_sm[e] = j0 + jj < S ? X[(int64_t)u * S + j0 + jj] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    auto pass = [&](auto mc, int stride, int inner) {
+        constexpr int M = decltype(mc)::value;
+        constexpr int L = M3 / M; // lines per column
+        for (int e = tid; e < L * JB; e += 256) {
+            const int line = e / JB, jj = e % JB;
+            const int u0 = (line / inner) * (inner * M) + (line % inner);
+            double2 v[M];
+#pragma unroll
+            for (int i = 0; i < M; i++) v[i] = lat_sm[(u0 + i * stride) * JB + jj];
+            reg_fft<M>(v, sign);
+#pragma unroll
+            for (int i = 0; i < M; i++) lat_sm[(u0 + i * stride) * JB + jj] = v[i];
+        }
+        __syncthreads();
+    };
+    if (MZ > 1) pass(std::integral_constant<int, MZ>{}, 1, 1);
+    if (MY > 1) pass(std::integral_constant<int, MY>{}, MZ, MZ);
+    if (MX > 1) pass(std::integral_constant<int, MX>{}, MY * MZ, MY * MZ);
+    for (int e = tid; e < M3 * JB; e += 256) {
+        const int u = e / JB, jj = e % JB;
+        if (j0 + jj < S) X[(int64_t)u * S + j0 + jj] = lat_sm[e];
+    }
+}
+
+template <int MX, int MY, int MZ> void lat_fft_smem(double2 *X, int64_t S, double sign, cudaStream_t st) {
+    constexpr int JB = 16;
+    constexpr size_t smem = (size_t)MX * MY * MZ * JB * sizeof(double2);
+    auto k = lat_fft_smem_kernel<MX, MY, MZ, JB>;
+    set_smem_once(k, smem);
+    k<<<(unsigned)((S + JB - 1) / JB), 256, smem, st>>>(X, S, sign);
+}
+
+template <int M> void lat_fft_axis(double2 *X, int64_t S, int64_t M3, int64_t ustride, double sign, cudaStream_t st) {
+    const int64_t nlines = M3 / M;
+    lat_fft_axis_kernel<M><<<dim3((unsigned)((S + 127) / 128), (unsigned)nlines), 128, 0, st>>>(X, S, nlines, ustride,
+                                                                                                  ustride, sign);
+}
+
+// 3D transform over the lattice (mx, my, mz) of every column: in place, unnormalised
+int lat_fft(double2 *X, int64_t S, const int m[3], double sign, cudaStream_t st) {
+    const int64_t M3 = (int64_t)m[0] * m[1] * m[2];
+    if (M3 == 1) return 0;
+#define LAT_SMEM(a, b, c)                                                                                              \
+    if (m[0] == a && m[1] == b && m[2] == c) {                                                                         \
+        lat_fft_smem<a, b, c>(X, S, sign, st);                                                                         \
+        return 1;                                                                                                      \
+    }
+    LAT_SMEM(2, 2, 2) LAT_SMEM(4, 4, 4) LAT_SMEM(8, 8, 8)
+    LAT_SMEM(2, 2, 1) LAT_SMEM(2, 1, 2) LAT_SMEM(1, 2, 2) LAT_SMEM(2, 1, 1) LAT_SMEM(1, 2, 1) LAT_SMEM(1, 1, 2)
+    LAT_SMEM(4, 4, 8) LAT_SMEM(4, 8, 4) LAT_SMEM(8, 4, 4) LAT_SMEM(2, 2, 4) LAT_SMEM(2, 4, 2) LAT_SMEM(4, 2, 2)
+#undef LAT_SMEM
+    int launches = 0;
+    const int64_t inner[3] = {(int64_t)m[1] * m[2], m[2], 1};
+    for (int ax = 2; ax >= 0; ax--) {
+        const int64_t stride = inner[ax];
+        switch (m[ax]) {
+        case 1: break;
+        case 2: lat_fft_axis<2>(X, S, M3, stride, sign, st), launches++; break;
+        case 4: lat_fft_axis<4>(X, S, M3, stride, sign, st), launches++; break;
+        case 8: lat_fft_axis<8>(X, S, M3, stride, sign, st), launches++; break;
+        case 16: lat_fft_axis<16>(X, S, M3, stride, sign, st), launches++; break;
+        case 32: lat_fft_axis<32>(X, S, M3, stride, sign, st), launches++; break;
+        default: throw RuntimeError("lattice M2L: lattice edge " + std::to_string(m[ax]) + " unsupported");
+        }
+    }
+    return launches;
+}
+
+// ---- pruned surface transforms (replace scatter + cuFFT D2Z and cuFFT Z2D + gather) ----
+// The density of a box lives on the p^3 corner of its N^3 grid (N = 2p), only at the
+// surface points; the check potentials are needed only there. Each transform runs as
+// three direct DFT stages over the nonzero / needed index ranges (sums of p terms), one
+// CTA per grid, with the half-spectrum layout and sign of cuFFT's D2Z ([kx][ky][kz],
+// kz <= N/2, exp(-2 pi i k.g / N), unnormalised).
+constexpr int LS_THREADS = 256;
+
+// Psi[grid][w] for grid = (u 8 + c) ks + b; box_of[u 8 + c] < 0: zero spectrum
+__global__ void __launch_bounds__(LS_THREADS) lat_surface_fwd_kernel(const double *__restrict__ X, int64_t Kp,
+                                                                     const int *__restrict__ box_of, int ks, int p,
+                                                                     int n, const int *__restrict__ gidx,
+                                                                     double2 *__restrict__ Psi) {
+    extern __shared__ double ls_sm[];
+    const int N = 2 * p, NH = p + 1, nw = N * N * NH;
+    double2 *tw = reinterpret_cast<double2 *>(ls_sm);         // [N] exp(-2 pi i k / N)
+    double *cube = reinterpret_cast<double *>(tw + N);        // [p][p][p]
+    double2 *f1 = reinterpret_cast<double2 *>(cube + ((p * p * p + 1) & ~1)); // [x][y][kz] (p p NH)
+    double2 *f2 = f1 + p * p * NH;                              // [x][ky][kz] (p N NH)
+    const int64_t grid = blockIdx.x;
+    const int uc = (int)(grid / ks), b = (int)(grid % ks);
+    const int box = box_of[uc];
+    double2 *out = Psi + grid * nw;
+    const int tid = threadIdx.x;
+    if (box < 0) {
+        for (int w = tid; w < nw; w += LS_THREADS) out[w] = make_double2(0.0, 0.0);
+        return;
+    }
+    for (int k = tid; k < N; k += LS_THREADS) {
+        double s, c;
+        sincospi(-2.0 * k / N, &s, &c);
+        tw[k] = make_double2(c, s);
+    }
+    for (int e = tid; e < p * p * p; e += LS_THREADS) cube[e] = 0.0;
+    __syncthreads();
+    const double *src = X + (int64_t)box * Kp + b;
+    for (int i = tid; i < n; i += LS_THREADS) {
+        const int g = gidx[i], x = g / (N * N), y = (g / N) % N, z = g % N;
+        cube[(x * p + y) * p + z] = src[(int64_t)ks * i];
+    }
+    __syncthreads();
+    // z: real -> half spectrum
+    for (int e = tid; e < p * p * NH; e += LS_THREADS) {
+        const int xy = e / NH, kz = e % NH;
+        const double *line = cube + xy * p;
+        double re = 0.0, im = 0.0;
+        for (int z = 0; z < p; z++) {
+            const double2 t = tw[(kz * z) % N];
+            re = fma(line[z], t.x, re);
+            im = fma(line[z], t.y, im);
+        }
+        f1[e] = make_double2(re, im);
+    }
+    __syncthreads();
+    // y: p -> N
+    for (int e = tid; e < p * N * NH; e += LS_THREADS) {
+        const int x = e / (N * NH), ky = (e / NH) % N, kz = e % NH;
+        double re = 0.0, im = 0.0;
+        for (int y = 0; y < p; y++) {
+            const double2 a = f1[(x * p + y) * NH + kz], t = tw[(ky * y) % N];
+            re = fma(a.x, t.x, fma(-a.y, t.y, re));
+            im = fma(a.x, t.y, fma(a.y, t.x, im));
+        }
+        f2[e] = make_double2(re, im);
+    }
+    __syncthreads();
+    // x: p -> N, straight to the spectrum
+    for (int w = tid; w < nw; w += LS_THREADS) {
+        const int kx = w / (N * NH), r = w % (N * NH);
+        double re = 0.0, im = 0.0;
+        for (int x = 0; x < p; x++) {
+            const double2 a = f2[x * N * NH + r], t = tw[(kx * x) % N];
+            re = fma(a.x, t.x, fma(-a.y, t.y, re));
+            im = fma(a.x, t.y, fma(a.y, t.x, im));
+        }
+        out[w] = make_double2(re, im);
+    }
+}
+
+// Y[box][kt i + a] += scale * (inverse transform of Q[grid], grid = (u 8 + o) kt + a) at the
+// surface points; C2R semantics (the kz = 0 and N/2 planes contribute their real parts)
+__global__ void __launch_bounds__(LS_THREADS) lat_surface_inv_kernel(const double2 *__restrict__ Q,
+                                                                     const int *__restrict__ box_of, int kt, int p,
+                                                                     int n, const int *__restrict__ gidx, double scale,
+                                                                     int64_t Kp, double *__restrict__ Y) {
+    extern __shared__ double ls_sm[];
+    const int N = 2 * p, NH = p + 1, nw = N * N * NH;
+    double2 *tw = reinterpret_cast<double2 *>(ls_sm);   // [N] exp(+2 pi i k / N)
+    double2 *b1 = tw + N;                                // [x][ky][kz] (p N NH)
+    double2 *b2 = b1 + p * N * NH;                       // [x][y][kz]  (p p NH)
+    const int64_t grid = blockIdx.x;
+    const int uo = (int)(grid / kt), a = (int)(grid % kt);
+    const int box = box_of[uo];
+    if (box < 0) return;
+    const double2 *in = Q + grid * nw;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < N; k += LS_THREADS) {
+        double s, c;
+        sincospi(2.0 * k / N, &s, &c);
+        tw[k] = make_double2(c, s);
+    }
+    __syncthreads();
+    // x: N -> p
+    for (int e = tid; e < p * N * NH; e += LS_THREADS) {
+        const int x = e / (N * NH), r = e % (N * NH);
+        double re = 0.0, im = 0.0;
+        for (int kx = 0; kx < N; kx++) {
+            const double2 q = in[kx * N * NH + r], t = tw[(kx * x) % N];
+            re = fma(q.x, t.x, fma(-q.y, t.y, re));
+            im = fma(q.x, t.y, fma(q.y, t.x, im));
+        }
+        b1[e] = make_double2(re, im);
+    }
+    __syncthreads();
+    // y: N -> p
+    for (int e = tid; e < p * p * NH; e += LS_THREADS) {
+        const int x = e / (p * NH), y = (e / NH) % p, kz = e % NH;
+        double re = 0.0, im = 0.0;
+        for (int ky = 0; ky < N; ky++) {
+            const double2 q = b1[(x * N + ky) * NH + kz], t = tw[(ky * y) % N];
+            re = fma(q.x, t.x, fma(-q.y, t.y, re));
+            im = fma(q.x, t.y, fma(q.y, t.x, im));
+        }
+        b2[e] = make_double2(re, im);
+    }
+    __syncthreads();
+    // z: Hermitian half spectrum -> real, at the surface points only
+    double *dst = Y + (int64_t)box * Kp + a;
+    for (int i = tid; i < n; i += LS_THREADS) {
+        const int g = gidx[i], x = g / (N * N), y = (g / N) % N, z = g % N;
+        const double2 *line = b2 + (x * p + y) * NH;
+        double v = line[0].x + ((z & 1) ? -line[p].x : line[p].x);
+        double s = 0.0;
+        for (int kz = 1; kz < p; kz++) {
+            const double2 q = line[kz], t = tw[(kz * z) % N];
+            s = fma(q.x, t.x, fma(-q.y, t.y, s));
+        }
+        v += 2.0 * s;
+        dst[(int64_t)kt * i] += scale * v;
+    }
+}
+
+std::array<int, 3> lattice_dims(int level, const int periodic[3]) {
+    const int m = 1 << (level - 1);
+    return {periodic[0] ? m : 2 * m, periodic[1] ? m : 2 * m, periodic[2] ? m : 2 * m};
+}
+
+LatticeShape &lattice_shape(KifmmOps &ops, const std::array<int, 3> &m, cudaStream_t st, int *launches) {
+    FftOps &f = ops.fft;
+    LatticeShape &S = f.lattice[m];
+    if (S.M) return S;
+    S.m[0] = m[0], S.m[1] = m[1], S.m[2] = m[2];
+    S.M3 = (int64_t)m[0] * m[1] * m[2];
+    const int nc = ops.ks * (ops.ks + 1) / 2;
+    S.M = ops.ws.get<double>("lat_M_" + std::to_string(m[0]) + "_" + std::to_string(m[1]) + "_" + std::to_string(m[2]),
+                             (size_t)S.M3 * LAT_E * nc * f.nw * 2);
+    const dim3 grid((f.nw + 127) / 128, LAT_E * nc, (unsigned)S.M3);
+    lat_build_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(f.khat), ops.slot_of_code, ops.ks, f.nw,
+                                           m[0], m[1], m[2], reinterpret_cast<double2 *>(S.M));
+    PK_CUDA(cudaGetLastError());
+    *launches += 1;
+    return S;
+}
+
+} // namespace
+
+int64_t m2l_lattice_bytes(const KifmmOps &ops, int level, const int periodic[3]) {
+    const int p = ops.p, N = 2 * p, nw = N * N * (N / 2 + 1);
+    const auto m = lattice_dims(level, periodic);
+    const int64_t M3 = (int64_t)m[0] * m[1] * m[2];
+    const int nc = ops.ks * (ops.ks + 1) / 2;
+    const int64_t spectra = M3 * LAT_E * nc * nw * 16;            // M
+    const int64_t lat = 2 * M3 * 8 * ops.ks * (int64_t)nw * 16;   // Psi~, Q~
+    return spectra + lat;
+}
+
+int m2l_lattice_check(KifmmOps &ops, const LatticeLevelArgs &a, const int *table, int64_t ld, const int *out_box,
+                      int ncols, int *bad, Workspace &ws, cudaStream_t st) {
+    const auto m = lattice_dims(a.level, a.periodic);
+    const int64_t M3 = (int64_t)m[0] * m[1] * m[2], nl = a.box1 - a.box0;
+    const int n = 1 << a.level;
+    int *box_of = ws.get<int>("lat_boxof_chk", M3 * 8);
+    int *seen = ws.get<int>("lat_seen", std::max<int64_t>(nl, 1));
+    int *d_code = ops.ws.get<int>("fft_code", kNumM2L); // uploaded by m2l_fft_prepare
+    static const bool debug = std::getenv("PKGPU_LATTICE_DEBUG") != nullptr;
+    int *dbg = nullptr;
+    if (debug) {
+        dbg = ws.get<int>("lat_dbg", 33);
+        PK_CUDA(cudaMemsetAsync(dbg, 0, 33 * sizeof(int), st));
+    }
+    PK_CUDA(cudaMemsetAsync(box_of, 0xff, M3 * 8 * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(seen, 0, nl * sizeof(int), st));
+    lat_boxmap_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(a.cell, a.box0, nl, m[1], m[2], box_of);
+    const int64_t total = (int64_t)kNumM2L * ncols;
+    lat_check_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+        table, ld, out_box, ncols, d_code, a.cell, box_of, n, a.periodic[0], a.periodic[1], a.periodic[2], m[1], m[2],
+        a.box0, nl, seen, bad, dbg);
+    lat_seen_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(seen, nl, bad);
+    PK_CUDA(cudaGetLastError());
+    if (debug) {
+        int h[33];
+        PK_CUDA(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        std::vector<int> cells(4 * 8 * 2);
+        for (int k = 0; k < std::min(h[0], 8); k++) {
+            int4 ct{}, cw{}, cg{};
+            PK_CUDA(cudaMemcpy(&ct, a.cell + h[2 + 4 * k], sizeof ct, cudaMemcpyDeviceToHost));
+            if (h[3 + 4 * k] >= 0) PK_CUDA(cudaMemcpy(&cw, a.cell + h[3 + 4 * k], sizeof cw, cudaMemcpyDeviceToHost));
+            if (h[4 + 4 * k] >= 0) PK_CUDA(cudaMemcpy(&cg, a.cell + h[4 + 4 * k], sizeof cg, cudaMemcpyDeviceToHost));
+            const int code = ops.h_code_of_slot[h[1 + 4 * k]];
+            std::fprintf(stderr, "  level %d slot %d d=(%d,%d,%d) target %d (%d,%d,%d) want %d (%d,%d,%d) got %d (%d,%d,%d)\n",
+                         a.level, h[1 + 4 * k], code / 49 - 3, (code / 7) % 7 - 3, code % 7 - 3, h[2 + 4 * k], ct.x, ct.y,
+                         ct.z, h[3 + 4 * k], cw.x, cw.y, cw.z, h[4 + 4 * k], cg.x, cg.y, cg.z);
+        }
+    }
+    return 3;
+}
+
+int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st) {
+    FftOps &f = ops.fft;
+    int launches = 0;
+    const auto m = lattice_dims(a.level, a.periodic);
+    LatticeShape &S = lattice_shape(ops, m, st, &launches);
+    const int ks = ops.ks, kt = ops.kt, n = ops.n;
+    const int64_t M3 = S.M3, N3 = (int64_t)f.N * f.N * f.N, nl = a.box1 - a.box0;
+    int *box_of = ws.get<int>("lat_boxof", M3 * 8);
+    PK_CUDA(cudaMemsetAsync(box_of, 0xff, M3 * 8 * sizeof(int), st));
+    lat_boxmap_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(a.cell, a.box0, nl, m[1], m[2], box_of);
+    // densities -> surface spectra Psi[u][c][b][w] (pruned DFT stages, no grids in memory)
+    const int64_t ng = M3 * 8 * ks;
+    double *psi = ws.get<double>("lat_psi", (size_t)ng * f.nw * 2);
+    const int p = ops.p, NH = p + 1;
+    const size_t fsm = (size_t)f.N * 16 + (size_t)((p * p * p + 1) & ~1) * 8 + (size_t)(p * p * NH + p * f.N * NH) * 16;
+    set_smem_once(lat_surface_fwd_kernel, fsm);
+    lat_surface_fwd_kernel<<<(unsigned)ng, LS_THREADS, fsm, st>>>(a.X, ops.Kp, box_of, ks, p, n, f.gidx,
+                                                                  reinterpret_cast<double2 *>(psi));
+    const int64_t Sd = ng / M3 * f.nw; // columns (c, b, w) per lattice point
+    launches += lat_fft(reinterpret_cast<double2 *>(psi), Sd, S.m, -1.0, st);
+    // pointwise products over (kappa, w)
+    double *q = ws.get<double>("lat_q", (size_t)M3 * 8 * kt * f.nw * 2);
+    const dim3 grid((f.nw + 127) / 128, (unsigned)M3);
+    if (ks == 1)
+        lat_mul_kernel<1><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
+                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
+    else
+        lat_mul_kernel<3><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
+                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
+    launches += lat_fft(reinterpret_cast<double2 *>(q), (int64_t)8 * kt * f.nw, S.m, 1.0, st);
+    // spectra -> check potentials at the surface points (unnormalised transforms: 1 / (N^3 M3))
+    const size_t ism = (size_t)f.N * 16 + (size_t)(p * f.N * NH + p * p * NH) * 16;
+    set_smem_once(lat_surface_inv_kernel, ism);
+    lat_surface_inv_kernel<<<(unsigned)(M3 * 8 * kt), LS_THREADS, ism, st>>>(
+        reinterpret_cast<const double2 *>(q), box_of, kt, p, n, f.gidx, a.alpha / ((double)N3 * (double)M3), ops.Kp,
+        a.Y);
+    PK_CUDA(cudaGetLastError());
+    return launches + 5;
+}
 
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st) {
     FftOps &f = ops.fft;

@@ -14,6 +14,7 @@
 // FFT's ~1e-15 relative level. K^ (316 offsets x kt x ks spectra) is built once per (kernel, p).
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <vector>
@@ -24,12 +25,24 @@ namespace pkgpu {
 
 struct KifmmOps;
 
+// Lattice M2L of one level shape (parent-lattice edges mx, my, mz; see m2l_lattice_level):
+// the stencil spectra M_e(kappa, w) for the 14 box-offset classes e >= 0 (the other 13 are
+// their conjugates), symmetric (a, b) components only.
+struct LatticeShape {
+    int m[3] = {0, 0, 0};
+    int64_t M3 = 0;
+    double *M = nullptr;            // [M3][14][ncomp][nw] complex, ncomp = ks (ks + 1) / 2
+    long long plan = -1;            // cufftHandle: batched 3D Z2Z over the parent lattice
+    int64_t plan_batch = 0;
+};
+
 struct FftOps {
     int N = 0, nw = 0;               // grid edge 2p; half spectrum N * N * (N / 2 + 1)
     double *khat = nullptr;          // [316][kt][ks][nw] complex (interleaved re, im)
     int *gidx = nullptr;             // [n] grid index of surface point i
     bool ready = false;
     std::map<int, long long> plans_r2c, plans_c2r; // cufftHandle per batch size
+    std::map<std::array<int, 3>, LatticeShape> lattice; // per parent-lattice shape
     ~FftOps();
 };
 
@@ -43,6 +56,31 @@ struct FftLevelArgs {
     double *Y = nullptr;          // q [box][Kp]: Y += alpha * M2L
     double alpha = 1.0;
 };
+
+// Lattice M2L of a filled level (SURVEY §8f rank 3 taken one step further): with the
+// level's boxes embedded in their lattice (absent boxes = zero densities), the V lists of
+// every target of octant o are the same box stencil, so the V-list sum is a convolution on
+// the PARENT lattice u (box 2u + c, c the octant):
+//   Q_o(u) = sum_c sum_{D in {-1,0,1}^3, |2D + c - o| >= 2} K_{2D+c-o} phi_c(u + D),
+// periodic axes wrapping (edge m = 2^(l-1)), free axes zero-padded to 2m. After the surface
+// FFT (Phi^) and a 3D FFT over u, it is a pointwise 24 x 24 (Stokes) product per
+// (kappa, w) with M_e(kappa, w) = sum_D K^_{2D+e}(w) exp(+2 pi i kappa.D / m), e = c - o.
+struct LatticeLevelArgs {
+    int level = 0;                 // l >= 1
+    int periodic[3] = {0, 0, 0};
+    int64_t box0 = 0, box1 = 0;    // the level's boxes (BFS ids)
+    const int4 *cell = nullptr;    // box cells (x, y, z, level)
+    const double *X = nullptr;     // phi_up [box][Kp]
+    double *Y = nullptr;           // q [box][Kp]: Y += alpha * M2L
+    double alpha = 1.0;
+};
+// device workspace bytes the level needs (kernel spectra, grids, lattice spectra)
+int64_t m2l_lattice_bytes(const KifmmOps &ops, int level, const int periodic[3]);
+// counts into bad[0] the (slot, column) V-list entries of the dense layout that differ from
+// the lattice stencil (0: the lattice sum equals the V-list sum exactly)
+int m2l_lattice_check(KifmmOps &ops, const LatticeLevelArgs &a, const int *table, int64_t ld, const int *out_box,
+                      int ncols, int *bad, Workspace &ws, cudaStream_t st);
+int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st);
 
 // builds K^ on first use; returns kernel launches
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st);

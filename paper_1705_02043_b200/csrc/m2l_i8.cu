@@ -1250,6 +1250,7 @@ const I8Settings &i8_settings() {
         r.beta_a = t.beta_a;
         r.beta_b = t.beta_b;
         r.min_boxes = t.i8_min_boxes;
+        r.lattice = t.m2l_int8 && t.m2l_lattice;
         return r;
     }();
     return s;

@@ -45,6 +45,7 @@ struct I8Settings {
     bool enabled = false;
     bool trans = false;       // M2M / L2L / pseudo-inverses on the int8 pipe too (i8_translate)
     bool fft = false;         // M2L by FFT on the surface lattice (m2l_fft.h) instead of dense products
+    bool lattice = false;     // filled levels by the lattice FFT M2L (m2l_lattice_level), any path but DMMA
     int nmod = 16, beta_a = 52, beta_b = 52; // accuracy study: profiles/r01_m2l_arith_study.md
     int64_t min_boxes = 1;    // levels with fewer boxes stay on the DMMA gather-GEMM
 };

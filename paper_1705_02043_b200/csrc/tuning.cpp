@@ -41,6 +41,9 @@ const Tuning &tuning() {
         r.gemm_min_iters_small = env_int("PKGPU_GEMM_MINIT_SMALL", r.gemm_min_iters_small, 1);
         r.list_warp_max = env_int("PKGPU_LIST_WARP_MAX", r.list_warp_max, 0);
         r.leaf_tt = (int)env_int("PKGPU_LEAF_TT", r.leaf_tt, 1);
+        r.m2l_lattice = env_int("PKGPU_M2L_LATTICE", 1, 0) != 0;
+        if (const char *e = std::getenv("PKGPU_LATTICE_FILL")) r.lattice_fill = std::atof(e);
+        r.lattice_budget = env_int("PKGPU_LATTICE_GB", r.lattice_budget >> 30, 0) << 30;
         return r;
     }();
     return t;

@@ -24,13 +24,16 @@ struct Tuning {
     I8Kernel i8_kernel = I8Kernel::automatic; // PKGPU_I8_KERNEL = single | dual | pairdual
     int i8_by_index = -1;              // PKGPU_I8_BYINDEX = 0 | 1: chunks as slot-index windows (-1: per kernel)
     int i8_tile_fast = -1;             // PKGPU_I8_TILEFAST = 0 | 1: unit order, column tile fastest
-    int i8_min_chunks = 0;
-    int i8_dynamic = 0;                // PKGPU_I8_DYNAMIC = 0 | 1: dynamic unit schedule (dual-tile kernels)             // PKGPU_I8_CHUNKS: at least this many slot chunks per tile
+    int i8_min_chunks = 0;             // PKGPU_I8_CHUNKS: at least this many slot chunks per tile
+    int i8_dynamic = 0;                // PKGPU_I8_DYNAMIC = 0 | 1: dynamic unit schedule (dual-tile kernels)
     int64_t gemm_units_per_cta = 32;   // PKGPU_GEMM_UNITS: DMMA gather-GEMM work units per CTA
     int64_t gemm_min_iters = 16;       // PKGPU_GEMM_MINIT: k-iterations per split-K unit
     int64_t gemm_min_iters_small = 4;  // PKGPU_GEMM_MINIT_SMALL: same, latency-bound one-slot GEMMs
-    int64_t list_warp_max = 50000;
-    int leaf_tt = 2;                   // PKGPU_LEAF_TT = 1 | 2 | 4: targets per thread in the leaf pass     // PKGPU_LIST_WARP_MAX: trees up to this size list a warp per box
+    int64_t list_warp_max = 50000;     // PKGPU_LIST_WARP_MAX: trees up to this size list a warp per box
+    int leaf_tt = 2;                   // PKGPU_LEAF_TT = 1 | 2 | 4: targets per thread in the leaf pass
+    bool m2l_lattice = true;           // PKGPU_M2L_LATTICE = 0 | 1: filled levels by the lattice FFT M2L
+    double lattice_fill = 0.5;         // PKGPU_LATTICE_FILL: least fraction of the level's lattice present
+    int64_t lattice_budget = 48LL << 30; // PKGPU_LATTICE_GB: device bytes the lattice levels may use
 };
 
 const Tuning &tuning();
