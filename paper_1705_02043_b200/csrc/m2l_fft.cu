@@ -27,8 +27,6 @@ namespace pkgpu {
 FftOps::~FftOps() {
     for (auto &kv : plans_r2c) cufftDestroy((cufftHandle)kv.second);
     for (auto &kv : plans_c2r) cufftDestroy((cufftHandle)kv.second);
-    for (auto &kv : lattice)
-        if (kv.second.plan >= 0) cufftDestroy((cufftHandle)kv.second.plan);
 }
 
 namespace {
@@ -685,56 +683,75 @@ int lat_fft(double2 *X, int64_t S, const int m[3], double sign, cudaStream_t st)
     return launches;
 }
 
-// ---- pruned surface transforms (replace scatter + cuFFT D2Z and cuFFT Z2D + gather) ----
-// The density of a box lives on the p^3 corner of its N^3 grid (N = 2p), only at the
-// surface points; the check potentials are needed only there. Each transform runs as
-// three direct DFT stages over the nonzero / needed index ranges (sums of p terms), one
-// CTA per grid, with the half-spectrum layout and sign of cuFFT's D2Z ([kx][ky][kz],
-// kz <= N/2, exp(-2 pi i k.g / N), unnormalised).
+// ---- surface transforms of the lattice path -------------------------------------------
+// The lattice and surface transforms commute, so the lattice FFT runs on the raw surface
+// values (n per box and component, 8x less data than spectra) and the surface transforms
+// run per lattice frequency kappa on complex data. A density lives on the p^3 corner of
+// its N^3 grid (N = 2p), only at the surface points, and the check potentials are needed
+// only there: each surface transform is three direct DFT stages over the nonzero / needed
+// index ranges (sums of p terms), one CTA per (kappa, octant, component), with cuFFT's D2Z
+// half-spectrum layout and sign ([kx][ky][kz], kz <= N/2, exp(-2 pi i k.g / N)).
 constexpr int LS_THREADS = 256;
 
-// Psi[grid][w] for grid = (u 8 + c) ks + b; box_of[u 8 + c] < 0: zero spectrum
-__global__ void __launch_bounds__(LS_THREADS) lat_surface_fwd_kernel(const double *__restrict__ X, int64_t Kp,
-                                                                     const int *__restrict__ box_of, int ks, int p,
-                                                                     int n, const int *__restrict__ gidx,
-                                                                     double2 *__restrict__ Psi) {
-    extern __shared__ double ls_sm[];
-    const int N = 2 * p, NH = p + 1, nw = N * N * NH;
-    double2 *tw = reinterpret_cast<double2 *>(ls_sm);         // [N] exp(-2 pi i k / N)
-    double *cube = reinterpret_cast<double *>(tw + N);        // [p][p][p]
-    double2 *f1 = reinterpret_cast<double2 *>(cube + ((p * p * p + 1) & ~1)); // [x][y][kz] (p p NH)
-    double2 *f2 = f1 + p * p * NH;                              // [x][ky][kz] (p N NH)
-    const int64_t grid = blockIdx.x;
-    const int uc = (int)(grid / ks), b = (int)(grid % ks);
-    const int box = box_of[uc];
-    double2 *out = Psi + grid * nw;
-    const int tid = threadIdx.x;
-    if (box < 0) {
-        for (int w = tid; w < nw; w += LS_THREADS) out[w] = make_double2(0.0, 0.0);
-        return;
+// A[u][(c ks + b) n + i] = phi of box (u, c), component b, surface point i (0: absent box)
+__global__ void lat_gather_surface_kernel(const double *__restrict__ X, int64_t Kp, const int *__restrict__ box_of,
+                                          int64_t M3, int ks, int n, double2 *__restrict__ A) {
+    const int64_t S = (int64_t)8 * ks * n, total = M3 * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = t / S;
+        const int j = (int)(t % S), c = j / (ks * n), r = j % (ks * n), b = r / n, i = r % n;
+        const int box = box_of[u * 8 + c];
+        A[t] = make_double2(box >= 0 ? X[(int64_t)box * Kp + ks * i + b] : 0.0, 0.0);
     }
+}
+
+// Y[box (u, o)][kt i + a] += scale * Re A[u][(o kt + a) n + i]
+__global__ void lat_scatter_surface_kernel(const double2 *__restrict__ A, const int *__restrict__ box_of, int64_t M3,
+                                           int kt, int n, double scale, int64_t Kp, double *__restrict__ Y) {
+    const int64_t S = (int64_t)8 * kt * n, total = M3 * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = t / S;
+        const int j = (int)(t % S), o = j / (kt * n), r = j % (kt * n), a = r / n, i = r % n;
+        const int box = box_of[u * 8 + o];
+        if (box >= 0) Y[(int64_t)box * Kp + kt * i + a] += scale * A[t].x;
+    }
+}
+
+// Psi[g][w] = surface DFT of the n complex values A[g][i], g = (kappa 8 + c) ks + b
+__global__ void __launch_bounds__(LS_THREADS) lat_surface_fwd_kernel(const double2 *__restrict__ A, int p, int n,
+                                                                     const int *__restrict__ gidx,
+                                                                     double2 *__restrict__ Psi) {
+    extern __shared__ double2 ls_sm[];
+    const int N = 2 * p, NH = p + 1, nw = N * N * NH;
+    double2 *tw = ls_sm;                 // [N] exp(-2 pi i k / N)
+    double2 *cube = tw + N;              // [x][y][z] (p^3)
+    double2 *f1 = cube + p * p * p;      // [x][y][kz]  (p p NH)
+    double2 *f2 = f1 + p * p * NH;       // [x][ky][kz] (p N NH)
+    const int64_t g = blockIdx.x;
+    const double2 *in = A + g * n;
+    double2 *out = Psi + g * nw;
+    const int tid = threadIdx.x;
     for (int k = tid; k < N; k += LS_THREADS) {
         double s, c;
         sincospi(-2.0 * k / N, &s, &c);
         tw[k] = make_double2(c, s);
     }
-    for (int e = tid; e < p * p * p; e += LS_THREADS) cube[e] = 0.0;
+    for (int e = tid; e < p * p * p; e += LS_THREADS) cube[e] = make_double2(0.0, 0.0);
     __syncthreads();
-    const double *src = X + (int64_t)box * Kp + b;
     for (int i = tid; i < n; i += LS_THREADS) {
-        const int g = gidx[i], x = g / (N * N), y = (g / N) % N, z = g % N;
-        cube[(x * p + y) * p + z] = src[(int64_t)ks * i];
+        const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
+        cube[(x * p + y) * p + z] = in[i];
     }
     __syncthreads();
-    // z: real -> half spectrum
+    // z: p -> kz <= N/2 (the half spectrum; the rest is the conjugate at -kappa)
     for (int e = tid; e < p * p * NH; e += LS_THREADS) {
         const int xy = e / NH, kz = e % NH;
-        const double *line = cube + xy * p;
+        const double2 *line = cube + xy * p;
         double re = 0.0, im = 0.0;
         for (int z = 0; z < p; z++) {
-            const double2 t = tw[(kz * z) % N];
-            re = fma(line[z], t.x, re);
-            im = fma(line[z], t.y, im);
+            const double2 a = line[z], t = tw[(kz * z) % N];
+            re = fma(a.x, t.x, fma(-a.y, t.y, re));
+            im = fma(a.x, t.y, fma(a.y, t.x, im));
         }
         f1[e] = make_double2(re, im);
     }
@@ -764,22 +781,21 @@ __global__ void __launch_bounds__(LS_THREADS) lat_surface_fwd_kernel(const doubl
     }
 }
 
-// Y[box][kt i + a] += scale * (inverse transform of Q[grid], grid = (u 8 + o) kt + a) at the
-// surface points; C2R semantics (the kz = 0 and N/2 planes contribute their real parts)
+// A[g][i] = inverse surface DFT at the surface points of the full spectrum of lattice
+// frequency kappa, g = (kappa 8 + o) kt + a. Only kz <= N/2 is stored: the other half is
+// conj(Q(-kappa, -w)), so a CTA takes the pair (kappa, -kappa) and writes both.
 __global__ void __launch_bounds__(LS_THREADS) lat_surface_inv_kernel(const double2 *__restrict__ Q,
-                                                                     const int *__restrict__ box_of, int kt, int p,
-                                                                     int n, const int *__restrict__ gidx, double scale,
-                                                                     int64_t Kp, double *__restrict__ Y) {
-    extern __shared__ double ls_sm[];
+                                                                     const int64_t *__restrict__ pairs, int kt, int p,
+                                                                     int n, const int *__restrict__ gidx,
+                                                                     double2 *__restrict__ A) {
+    extern __shared__ double2 ls_sm[];
     const int N = 2 * p, NH = p + 1, nw = N * N * NH;
-    double2 *tw = reinterpret_cast<double2 *>(ls_sm);   // [N] exp(+2 pi i k / N)
-    double2 *b1 = tw + N;                                // [x][ky][kz] (p N NH)
-    double2 *b2 = b1 + p * N * NH;                       // [x][y][kz]  (p p NH)
-    const int64_t grid = blockIdx.x;
-    const int uo = (int)(grid / kt), a = (int)(grid % kt);
-    const int box = box_of[uo];
-    if (box < 0) return;
-    const double2 *in = Q + grid * nw;
+    double2 *tw = ls_sm;                 // [N] exp(+2 pi i k / N)
+    double2 *b1 = tw + N;                // 2 x [x][ky][kz] (p N NH)
+    double2 *b2 = b1 + 2 * p * N * NH;   // 2 x [x][y][kz]  (p p NH)
+    const int64_t pr = pairs[blockIdx.x / (8 * kt)];
+    const int oa = blockIdx.x % (8 * kt);
+    const int64_t kap[2] = {pr & 0xffffffffLL, pr >> 32};
     const int tid = threadIdx.x;
     for (int k = tid; k < N; k += LS_THREADS) {
         double s, c;
@@ -787,9 +803,11 @@ __global__ void __launch_bounds__(LS_THREADS) lat_surface_inv_kernel(const doubl
         tw[k] = make_double2(c, s);
     }
     __syncthreads();
-    // x: N -> p
-    for (int e = tid; e < p * N * NH; e += LS_THREADS) {
-        const int x = e / (N * NH), r = e % (N * NH);
+    const int nh = kap[0] == kap[1] ? 1 : 2;
+    // x: N -> p, then y: N -> p, for kappa and -kappa
+    for (int e = tid; e < nh * p * N * NH; e += LS_THREADS) {
+        const int h = e / (p * N * NH), r0 = e % (p * N * NH), x = r0 / (N * NH), r = r0 % (N * NH);
+        const double2 *in = Q + (kap[h] * 8 * kt + oa) * nw;
         double re = 0.0, im = 0.0;
         for (int kx = 0; kx < N; kx++) {
             const double2 q = in[kx * N * NH + r], t = tw[(kx * x) % N];
@@ -799,32 +817,194 @@ __global__ void __launch_bounds__(LS_THREADS) lat_surface_inv_kernel(const doubl
         b1[e] = make_double2(re, im);
     }
     __syncthreads();
-    // y: N -> p
-    for (int e = tid; e < p * p * NH; e += LS_THREADS) {
-        const int x = e / (p * NH), y = (e / NH) % p, kz = e % NH;
+    for (int e = tid; e < nh * p * p * NH; e += LS_THREADS) {
+        const int h = e / (p * p * NH), r0 = e % (p * p * NH), x = r0 / (p * NH), y = (r0 / NH) % p, kz = r0 % NH;
+        const double2 *src = b1 + h * p * N * NH;
         double re = 0.0, im = 0.0;
         for (int ky = 0; ky < N; ky++) {
-            const double2 q = b1[(x * N + ky) * NH + kz], t = tw[(ky * y) % N];
+            const double2 q = src[(x * N + ky) * NH + kz], t = tw[(ky * y) % N];
             re = fma(q.x, t.x, fma(-q.y, t.y, re));
             im = fma(q.x, t.y, fma(q.y, t.x, im));
         }
         b2[e] = make_double2(re, im);
     }
     __syncthreads();
-    // z: Hermitian half spectrum -> real, at the surface points only
-    double *dst = Y + (int64_t)box * Kp + a;
-    for (int i = tid; i < n; i += LS_THREADS) {
-        const int g = gidx[i], x = g / (N * N), y = (g / N) % N, z = g % N;
-        const double2 *line = b2 + (x * p + y) * NH;
-        double v = line[0].x + ((z & 1) ? -line[p].x : line[p].x);
-        double s = 0.0;
-        for (int kz = 1; kz < p; kz++) {
-            const double2 q = line[kz], t = tw[(kz * z) % N];
-            s = fma(q.x, t.x, fma(-q.y, t.y, s));
+    // z: the full line of kappa is B(kappa, kz) for kz <= N/2 and conj(B(-kappa, N - kz)) above
+    for (int e = tid; e < nh * n; e += LS_THREADS) {
+        const int h = e / n, i = e % n;
+        const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
+        const double2 *own = b2 + h * p * p * NH + (x * p + y) * NH;
+        const double2 *oth = b2 + (nh == 2 ? 1 - h : 0) * p * p * NH + (x * p + y) * NH;
+        double re = 0.0, im = 0.0;
+        for (int kz = 0; kz <= p; kz++) {
+            const double2 q = own[kz], t = tw[(kz * z) % N];
+            re = fma(q.x, t.x, fma(-q.y, t.y, re));
+            im = fma(q.x, t.y, fma(q.y, t.x, im));
         }
-        v += 2.0 * s;
-        dst[(int64_t)kt * i] += scale * v;
+        for (int kz = p + 1; kz < N; kz++) {
+            const double2 q = oth[N - kz], t = tw[(kz * z) % N]; // conj(q) * t
+            re = fma(q.x, t.x, fma(q.y, t.y, re));
+            im = fma(q.x, t.y, fma(-q.y, t.x, im));
+        }
+        A[(kap[h] * 8 * kt + oa) * n + i] = make_double2(re, im);
     }
+}
+
+// The same two transforms with p a compile-time constant: every twiddle index is a
+// constant, each thread keeps one input column in registers and produces all its outputs
+// (no per-term index arithmetic, one shared-memory read per input).
+template <int P> struct Tw {
+    static constexpr int N = 2 * P;
+};
+template <int P> __device__ __forceinline__ double2 twid(const double2 *tw, int k) { return tw[k % (2 * P)]; }
+__device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 t) {
+    acc.x = fma(a.x, t.x, fma(-a.y, t.y, acc.x));
+    acc.y = fma(a.x, t.y, fma(a.y, t.x, acc.y));
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restrict__ A, int n,
+                                                         const int *__restrict__ gidx, double2 *__restrict__ Psi) {
+    constexpr int N = 2 * P, NH = P + 1, NW = N * N * NH;
+    extern __shared__ double2 lt_sm[];
+    double2 *tw = lt_sm;                 // [N]
+    double2 *cube = tw + N;              // [P^3]
+    double2 *f1 = cube + P * P * P;      // [x][y][kz]
+    double2 *f2 = f1 + P * P * NH;       // [x][ky][kz]
+    const int64_t g = blockIdx.x;
+    const double2 *in = A + g * n;
+    double2 *out = Psi + g * NW;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int k = tid; k < N; k += nt) {
+        double s, c;
+        sincospi(-2.0 * k / N, &s, &c);
+        tw[k] = make_double2(c, s);
+    }
+    for (int e = tid; e < P * P * P; e += nt) cube[e] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) {
+        const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
+        cube[(x * P + y) * P + z] = in[i];
+    }
+    __syncthreads();
+    for (int xy = tid; xy < P * P; xy += nt) { // z: P -> NH
+        double2 v[P];
+#pragma unroll
+        for (int z = 0; z < P; z++) v[z] = cube[xy * P + z];
+#pragma unroll
+        for (int kz = 0; kz < NH; kz++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int z = 0; z < P; z++) cmac(acc, v[z], tw[(kz * z) % N]);
+            f1[xy * NH + kz] = acc;
+        }
+    }
+    __syncthreads();
+    for (int col = tid; col < P * NH; col += nt) { // y: P -> N, column (x, kz)
+        const int x = col / NH, kz = col % NH;
+        double2 v[P];
+#pragma unroll
+        for (int y = 0; y < P; y++) v[y] = f1[(x * P + y) * NH + kz];
+#pragma unroll
+        for (int ky = 0; ky < N; ky++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int y = 0; y < P; y++) cmac(acc, v[y], tw[(ky * y) % N]);
+            f2[(x * N + ky) * NH + kz] = acc;
+        }
+    }
+    __syncthreads();
+    for (int r = tid; r < N * NH; r += nt) { // x: P -> N, column (ky, kz), straight out
+        double2 v[P];
+#pragma unroll
+        for (int x = 0; x < P; x++) v[x] = f2[x * N * NH + r];
+#pragma unroll
+        for (int kx = 0; kx < N; kx++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int x = 0; x < P; x++) cmac(acc, v[x], tw[(kx * x) % N]);
+            out[kx * N * NH + r] = acc;
+        }
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restrict__ Q, const int64_t *__restrict__ pairs,
+                                                         int kt, int n, const int *__restrict__ gidx,
+                                                         double2 *__restrict__ A) {
+    constexpr int N = 2 * P, NH = P + 1, NW = N * N * NH;
+    extern __shared__ double2 lt_sm[];
+    double2 *tw = lt_sm;                             // [N]
+    double2 *const b1 = tw + N;                  // 2 x [x][ky][kz] (per half)
+    double2 *const b2 = b1 + 2 * P * N * NH;     // 2 x [x][y][kz]
+    const int64_t pr = pairs[blockIdx.x / (8 * kt)];
+    const int oa = blockIdx.x % (8 * kt);
+    const int64_t kap[2] = {pr & 0xffffffffLL, pr >> 32};
+    const int nh = kap[0] == kap[1] ? 1 : 2;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int k = tid; k < N; k += nt) {
+        double s, c;
+        sincospi(2.0 * k / N, &s, &c);
+        tw[k] = make_double2(c, s);
+    }
+    __syncthreads();
+    for (int e = tid; e < nh * N * NH; e += nt) { // x: N -> P, column (h, ky, kz)
+        const int h = e / (N * NH), r = e % (N * NH);
+        const double2 *in = Q + (kap[h] * 8 * kt + oa) * NW + r;
+        double2 v[N];
+#pragma unroll
+        for (int kx = 0; kx < N; kx++) v[kx] = in[kx * N * NH];
+#pragma unroll
+        for (int x = 0; x < P; x++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int kx = 0; kx < N; kx++) cmac(acc, v[kx], tw[(kx * x) % N]);
+            b1[h * P * N * NH + x * N * NH + r] = acc;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < nh * P * NH; e += nt) { // y: N -> P, column (h, x, kz)
+        const int h = e / (P * NH), x = (e / NH) % P, kz = e % NH;
+        double2 v[N];
+#pragma unroll
+        for (int ky = 0; ky < N; ky++) v[ky] = b1[h * P * N * NH + (x * N + ky) * NH + kz];
+#pragma unroll
+        for (int y = 0; y < P; y++) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int ky = 0; ky < N; ky++) cmac(acc, v[ky], tw[(ky * y) % N]);
+            b2[h * P * P * NH + (x * P + y) * NH + kz] = acc;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < nh * n; e += nt) { // z at the surface points
+        const int h = e / n, i = e % n;
+        const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
+        const double2 *own = b2 + h * P * P * NH + (x * P + y) * NH;
+        const double2 *oth = b2 + (nh == 2 ? 1 - h : 0) * P * P * NH + (x * P + y) * NH;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int kz = 0; kz <= P; kz++) cmac(acc, own[kz], tw[(kz * z) % N]);
+#pragma unroll
+        for (int kz = P + 1; kz < N; kz++) {
+            const double2 q = oth[N - kz];
+            cmac(acc, make_double2(q.x, -q.y), tw[(kz * z) % N]);
+        }
+        A[(kap[h] * 8 * kt + oa) * n + i] = acc;
+    }
+}
+
+// the lattice frequencies as (kappa, -kappa) pairs, each pair once (self-conjugate: kappa twice)
+std::vector<int64_t> conjugate_pairs(const int m[3]) {
+    std::vector<int64_t> out;
+    const int64_t M3 = (int64_t)m[0] * m[1] * m[2];
+    for (int64_t k = 0; k < M3; k++) {
+        const int kx = (int)(k / ((int64_t)m[1] * m[2])), ky = (int)((k / m[2]) % m[1]), kz = (int)(k % m[2]);
+        const int64_t c = ((int64_t)((m[0] - kx) % m[0]) * m[1] + (m[1] - ky) % m[1]) * m[2] + (m[2] - kz) % m[2];
+        if (c < k) continue;
+        out.push_back(k | (c << 32));
+    }
+    return out;
 }
 
 std::array<int, 3> lattice_dims(int level, const int periodic[3]) {
@@ -846,6 +1026,13 @@ LatticeShape &lattice_shape(KifmmOps &ops, const std::array<int, 3> &m, cudaStre
                                            m[0], m[1], m[2], reinterpret_cast<double2 *>(S.M));
     PK_CUDA(cudaGetLastError());
     *launches += 1;
+    const std::vector<int64_t> pr = conjugate_pairs(S.m);
+    S.npairs = (int64_t)pr.size();
+    S.pairs = ops.ws.get<int64_t>("lat_pairs_" + std::to_string(m[0]) + "_" + std::to_string(m[1]) + "_" +
+                                      std::to_string(m[2]),
+                                  pr.size());
+    PK_CUDA(cudaMemcpyAsync(S.pairs, pr.data(), pr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PK_CUDA(cudaStreamSynchronize(st)); // pr is a host temporary
     return S;
 }
 
@@ -913,16 +1100,32 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     int *box_of = ws.get<int>("lat_boxof", M3 * 8);
     PK_CUDA(cudaMemsetAsync(box_of, 0xff, M3 * 8 * sizeof(int), st));
     lat_boxmap_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(a.cell, a.box0, nl, m[1], m[2], box_of);
-    // densities -> surface spectra Psi[u][c][b][w] (pruned DFT stages, no grids in memory)
+    // surface values -> lattice spectra (in place) -> surface spectra Psi~[kappa][c][b][w]
+    const int p = ops.p, NH = p + 1;
+    const int64_t Ss = (int64_t)8 * ks * n, St = (int64_t)8 * kt * n;
+    double2 *A = reinterpret_cast<double2 *>(ws.get<double>("lat_surf", (size_t)M3 * std::max(Ss, St) * 2));
+    lat_gather_surface_kernel<<<(unsigned)std::min<int64_t>((M3 * Ss + 255) / 256, 148 * 32), 256, 0, st>>>(
+        a.X, ops.Kp, box_of, M3, ks, n, A);
+    launches += lat_fft(A, Ss, S.m, -1.0, st);
     const int64_t ng = M3 * 8 * ks;
     double *psi = ws.get<double>("lat_psi", (size_t)ng * f.nw * 2);
-    const int p = ops.p, NH = p + 1;
-    const size_t fsm = (size_t)f.N * 16 + (size_t)((p * p * p + 1) & ~1) * 8 + (size_t)(p * p * NH + p * f.N * NH) * 16;
-    set_smem_once(lat_surface_fwd_kernel, fsm);
-    lat_surface_fwd_kernel<<<(unsigned)ng, LS_THREADS, fsm, st>>>(a.X, ops.Kp, box_of, ks, p, n, f.gidx,
-                                                                  reinterpret_cast<double2 *>(psi));
-    const int64_t Sd = ng / M3 * f.nw; // columns (c, b, w) per lattice point
-    launches += lat_fft(reinterpret_cast<double2 *>(psi), Sd, S.m, -1.0, st);
+    const int tpb = std::min(256, (f.N * NH + 31) / 32 * 32);
+    switch (p) {
+#define LAT_FWD(PP)                                                                                                    \
+    case PP: {                                                                                                         \
+        const size_t sm = (size_t)(2 * PP + PP * PP * PP + PP * PP * (PP + 1) + PP * 2 * PP * (PP + 1)) * 16;          \
+        set_smem_once(lat_surface_fwd_t<PP>, sm);                                                                      \
+        lat_surface_fwd_t<PP><<<(unsigned)ng, tpb, sm, st>>>(A, n, f.gidx, reinterpret_cast<double2 *>(psi));          \
+        break;                                                                                                         \
+    }
+        LAT_FWD(4) LAT_FWD(5) LAT_FWD(6) LAT_FWD(7) LAT_FWD(8) LAT_FWD(9) LAT_FWD(10)
+#undef LAT_FWD
+    default: {
+        const size_t fsm = (size_t)(f.N + p * p * p + p * p * NH + p * f.N * NH) * 16;
+        set_smem_once(lat_surface_fwd_kernel, fsm);
+        lat_surface_fwd_kernel<<<(unsigned)ng, LS_THREADS, fsm, st>>>(A, p, n, f.gidx, reinterpret_cast<double2 *>(psi));
+    }
+    }
     // pointwise products over (kappa, w)
     double *q = ws.get<double>("lat_q", (size_t)M3 * 8 * kt * f.nw * 2);
     const dim3 grid((f.nw + 127) / 128, (unsigned)M3);
@@ -932,15 +1135,31 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     else
         lat_mul_kernel<3><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
                                                 reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
-    launches += lat_fft(reinterpret_cast<double2 *>(q), (int64_t)8 * kt * f.nw, S.m, 1.0, st);
-    // spectra -> check potentials at the surface points (unnormalised transforms: 1 / (N^3 M3))
-    const size_t ism = (size_t)f.N * 16 + (size_t)(p * f.N * NH + p * p * NH) * 16;
-    set_smem_once(lat_surface_inv_kernel, ism);
-    lat_surface_inv_kernel<<<(unsigned)(M3 * 8 * kt), LS_THREADS, ism, st>>>(
-        reinterpret_cast<const double2 *>(q), box_of, kt, p, n, f.gidx, a.alpha / ((double)N3 * (double)M3), ops.Kp,
-        a.Y);
+    // surface values per lattice frequency -> inverse lattice transform -> check potentials
+    // (unnormalised transforms: 1 / (N^3 M3))
+    switch (p) {
+#define LAT_INV(PP)                                                                                                    \
+    case PP: {                                                                                                         \
+        const size_t sm = (size_t)(2 * PP + 2 * PP * 2 * PP * (PP + 1) + 2 * PP * PP * (PP + 1)) * 16;                 \
+        set_smem_once(lat_surface_inv_t<PP>, sm);                                                                      \
+        lat_surface_inv_t<PP><<<(unsigned)(S.npairs * 8 * kt), tpb, sm, st>>>(reinterpret_cast<const double2 *>(q),   \
+                                                                               S.pairs, kt, n, f.gidx, A);             \
+        break;                                                                                                         \
+    }
+        LAT_INV(4) LAT_INV(5) LAT_INV(6) LAT_INV(7) LAT_INV(8) LAT_INV(9) LAT_INV(10)
+#undef LAT_INV
+    default: {
+        const size_t ism = (size_t)(f.N + 2 * p * f.N * NH + 2 * p * p * NH) * 16;
+        set_smem_once(lat_surface_inv_kernel, ism);
+        lat_surface_inv_kernel<<<(unsigned)(S.npairs * 8 * kt), LS_THREADS, ism, st>>>(
+            reinterpret_cast<const double2 *>(q), S.pairs, kt, p, n, f.gidx, A);
+    }
+    }
+    launches += lat_fft(A, St, S.m, 1.0, st);
+    lat_scatter_surface_kernel<<<(unsigned)std::min<int64_t>((M3 * St + 255) / 256, 148 * 32), 256, 0, st>>>(
+        A, box_of, M3, kt, n, a.alpha / ((double)N3 * (double)M3), ops.Kp, a.Y);
     PK_CUDA(cudaGetLastError());
-    return launches + 5;
+    return launches + 6;
 }
 
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st) {

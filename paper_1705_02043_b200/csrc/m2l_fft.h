@@ -32,8 +32,8 @@ struct LatticeShape {
     int m[3] = {0, 0, 0};
     int64_t M3 = 0;
     double *M = nullptr;            // [M3][14][ncomp][nw] complex, ncomp = ks (ks + 1) / 2
-    long long plan = -1;            // cufftHandle: batched 3D Z2Z over the parent lattice
-    int64_t plan_batch = 0;
+    int64_t *pairs = nullptr;       // [npairs] (kappa, -kappa) packed low | high << 32
+    int64_t npairs = 0;
 };
 
 struct FftOps {
