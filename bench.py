@@ -48,6 +48,10 @@ REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
 REFDUMP_NATIVE = os.path.join(REPO, "oracle", "_ref", "refdump_native")
 FP64_VEC_PEAK_TFLOPS = 34.23  # measured DFMA loop on this pool (profiles/r01_fp64_peaks.jsonl)
 FP64_VEC_PEAK_SOURCE = "measured: DFMA loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl)"
+GEMM_NCU_TRAFFIC = None  # filled from the ncu --set full capture of the level-4 pinv launch (profiles/)
+GEMM_NCU_NOTE = None
+LATMUL_NCU_TRAFFIC = None
+LATMUL_NCU_NOTE = None
 LEAF_NCU_TRAFFIC = 40.5e6  # dram read + write bytes per leaf_kernel launch (profiles/r02_leaf_ncu.txt)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
@@ -220,15 +224,70 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def roofline_entry(stats, steps):
-    """Roofline of the dominant kernel from the per-stage CUDA events of the profiled pass.
+def translations_roofline(stats, steps):
+    """The FP64 tensor-pipe translations (M2M, L2L, both pseudo-inverse factors): every
+    launch of gather_gemm_tma_kernel (DMMA.8x8x4) with its split-K reduction, against the
+    measured DMMA peak. Algorithmic FLOP: 2 K^2 per M2M / L2L translation, 4 K^2 + K per
+    pseudo-inverse, K = 888, padding not counted."""
+    st = [stats.get(k, {}) for k in ("m2m", "pinv_up", "l2l", "pinv_dn")]
+    sec = sum(x.get("seconds", 0.0) for x in st)
+    fl = sum(x.get("flops", 0.0) for x in st)
+    n = max(1.0, stats.get("dmma_gemm", {}).get("units", 0.0))
+    if sec <= 0:
+        return None
+    achieved = fl / sec / 1e12
+    return {"kernel": "gather_gemm_tma_kernel<128,4,64,8> (M2M, L2L, pinv U^T and V factors: DMMA.8x8x4, TMA operator "
+                      "tiles, cp.async gathered rows) + split_reduce_kernel", "bound": "tensor",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+            "traffic": GEMM_NCU_TRAFFIC, "traffic_note": GEMM_NCU_NOTE,
+            "flops_per_launch": fl / n, "ms_per_launch": 1e3 * sec / n, "launches_per_step": n / steps,
+            "ms_per_step": 1e3 * sec / steps, "peak_source": FP64_PEAK_SOURCE,
+            "flop_convention": "2 K^2 per M2M / L2L translation, 4 K^2 + K per pseudo-inverse, K = 888 (SURVEY §8d)"}
 
-    int8 M2L (default): achieved = algorithmic int8 ops (2 nmod K^2 per V application,
-    K = 888, no padding) / the kernels' device time, against the measured kind::i8 peak;
-    the FP64-equivalent rate (2 K^2 per application / the same time) is reported beside
-    it. DMMA M2L (PKGPU_M2L=dmma): the FP64 gather-GEMM against the DMMA peak."""
+
+def lattice_roofline(stats, steps):
+    """The lattice M2L's dominant kernel, lat_mul_kernel: one pass over the stencil spectra
+    M (14 offset classes x symmetric components), Psi~ in and Q~ out, 16 B per complex
+    value -- HBM-bound, against MEASURED_PEAKS.json's copy bandwidth. The dense-equivalent
+    FP64 rate of the whole M2L stage (2 K^2 per V application) is reported beside it."""
+    mul = stats.get("lat_mul", {})
+    if not mul.get("seconds"):
+        return None
+    n = max(1, mul.get("launches", 1))
+    gbs = mul["flops"] / mul["seconds"] / 1e9  # "flops" of lat_mul are its algorithmic bytes
+    peak, src = hbm_peak()
+    m2l, lat = stats.get("m2l", {}), stats.get("m2l_lattice", {})
+    return {"kernel": "lat_mul_kernel<3> (pointwise 24 x 24 stencil products per lattice frequency and surface "
+                      "frequency)", "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "traffic": LATMUL_NCU_TRAFFIC, "traffic_note": LATMUL_NCU_NOTE,
+            "bytes_per_launch": mul["flops"] / n, "ms_per_launch": 1e3 * mul["seconds"] / n,
+            "launches_per_step": n / steps, "peak_source": src,
+            "m2l_stage_ms_per_step": 1e3 * m2l.get("seconds", 0.0) / steps,
+            "m2l_dense_equivalent_tflops": (lat.get("flops", 0.0) / m2l["seconds"] / 1e12) if m2l.get("seconds") else None,
+            "byte_convention": "per (lattice frequency, surface frequency): (14 x 6 + 8 x 3 + 8 x 3) complex "
+                               "doubles; level l has (2^(l-1))^3 lattice frequencies, 16 x 16 x 9 surface frequencies"}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth)"
+    except Exception:
+        return 6560.0, "fallback: 6.56 TB/s measured copy bandwidth (B200_PROFILING.md)"
+
+
+def roofline_entry(stats, steps):
+    """Roofline of the step's dominant kernel from the per-stage CUDA events of the profiled
+    pass. With the lattice M2L (default; cfg2's levels are filled) the dominant kernel is
+    the FP64 DMMA gather-GEMM of the translations; the lattice M2L's HBM-bound product
+    kernel and the leaf pass are reported beside it (`m2l`, `p2p`). With the dense int8 M2L
+    (set_m2l("int8_dense")) the dominant kernels are the tcgen05 kind::i8 GEMMs."""
     i8 = stats.get("m2l_i8", {})
     m2l = stats.get("m2l", {})
+    if stats.get("lat_mul", {}).get("seconds", 0) > 0:
+        r = translations_roofline(stats, steps)
+        r["m2l"] = lattice_roofline(stats, steps)
+        return r
     if i8.get("seconds", 0) > 0:
         n = max(1, i8.get("launches", 1))
         s, fl = i8["seconds"] / n, i8["flops"] / n

@@ -469,7 +469,8 @@ class Context:
         return lib().pkgpu_context_launch_count(self._h)
 
     STAGES = ("tree", "lists", "s2m", "m2m", "pinv_up", "x", "m2l", "l2l", "pinv_dn", "periodic", "leaf",
-              "m2l_prep", "m2l_i8", "m2l_crt")  # the last three: sub-stages of m2l on the int8 pipe
+              "m2l_prep", "m2l_i8", "m2l_crt",  # sub-stages of m2l on the int8 pipe
+              "lat_fwd", "lat_mul", "lat_inv")  # sub-stages of m2l on the lattice path (lat_mul "flops" = bytes)
 
     def set_profiling(self, on: bool):
         lib().pkgpu_context_set_profiling(self._h, 1 if on else 0)
@@ -493,7 +494,7 @@ class Context:
     def stage_stats(self):
         """{stage: dict(seconds, units, flops, launches)} accumulated while profiling."""
         out = {}
-        for st in self.STAGES + ("u_pairs", "m2l_mma_rows"):
+        for st in self.STAGES + ("u_pairs", "m2l_mma_rows", "m2l_lattice", "dmma_gemm"):
             sec, un, fl, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
             if lib().pkgpu_context_stage_stats(self._h, st.encode(), ctypes.byref(sec), ctypes.byref(un),
                                                ctypes.byref(fl), ctypes.byref(ln)) == 0:

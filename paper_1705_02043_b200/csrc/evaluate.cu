@@ -762,6 +762,7 @@ void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t 
     a.rdiv = up ? ops.s_up : ops.s_dn;
     a.rdiv_eps = up ? ops.up.eps : ops.dn.eps;
     ctx.launches += gather_gemm(a, ctx.ws, st, ctx.num_sms);
+    if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
     GemmArgs b = a;
     b.A = up ? ops.V_up : ops.V_dn;
     b.X = Tmp;
@@ -770,6 +771,7 @@ void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t 
     b.alpha = std::ldexp(1.0, -level); // phi /= 2^l (src/fmm.cpp:550-551, 595-596)
     b.beta = 0.0;
     ctx.launches += gather_gemm(b, ctx.ws, st, ctx.num_sms);
+    if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
 }
 
 // single-vector pinv: x = V (S+ (U^T b)) (src/linalg.cpp:78-87)
@@ -1055,6 +1057,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.beta = 0.0;
                 pm = prof.begin("m2m");
                 ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
+                if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
                 prof.end(pm);
             }
             pm = prof.begin("pinv_up");
@@ -1084,6 +1087,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         ctx.launches += ctx.lists.x.count ? 1 : 0;
         prof.end(pm);
         int i8_apps[kMaxLevels + 1] = {0}; // levels whose M2L ran on the int8 pipe
+        int lat_apps[kMaxLevels + 1] = {0}; // levels whose M2L ran as a lattice convolution
         bool mma_rows_zeroed = false;
         // ---- M2L on the int8 pipe: every int8 level in ONE launch (M2L reads only phi_up,
         // so it can precede the L2L chain; one pass streams each operator tile once for all
@@ -1180,8 +1184,27 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 la.X = Pup;
                 la.Y = Q;
                 la.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573)
+                struct Hook {
+                    Prof *prof;
+                    int open;
+                } hook{&prof, -1};
+                la.user = &hook;
+                la.mark = [](void *u, const char *stage, int begin) {
+                    Hook *h = static_cast<Hook *>(u);
+                    if (begin) {
+                        h->open = h->prof->begin(stage);
+                    } else {
+                        h->prof->end(h->open);
+                        // lat_mul is one kernel launch (the level's launches are added afterwards)
+                        if (h->open >= 0 && !std::strcmp(stage, "lat_mul")) h->prof->ctx.stats[stage].launches += 1;
+                    }
+                };
+                la.work = [](void *u, const char *stage, double units, double per_unit) {
+                    static_cast<Hook *>(u)->prof->work(stage, units, per_unit);
+                };
                 ctx.launches += m2l_lattice_level(ops, la, ws, st);
                 prof.end(pm);
+                lat_apps[l] = 1;
             } else if (l >= 1 && Lay.i8[l]) {
                 // M2L done above
             } else if (l >= 1 && ctx.i8.fft) {
@@ -1217,6 +1240,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.beta = 1.0;
                 pm = prof.begin("m2l");
                 ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
+                if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
                 prof.end(pm);
             }
             if (l >= 1 && ctx.i8.trans) {
@@ -1256,6 +1280,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 b.beta = 1.0;
                 pm = prof.begin("l2l");
                 ctx.launches += gather_gemm(b, ws, st, ctx.num_sms);
+                if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
                 prof.end(pm);
             }
             pm = prof.begin("pinv_dn");
@@ -1324,8 +1349,15 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             prof.work("m2l", (double)ctx.lists.v_total, dense);
             // int8 levels: V applications there (CSR offsets at the level bounds); the
             // algorithmic int8 work is nmod K^2 MACs per application (2 ops per MAC)
-            double v_i8 = 0;
+            double v_i8 = 0, v_lat = 0;
             for (int l = 1; l <= T.depth; l++) {
+                if (lat_apps[l]) {
+                    int64_t o2[2];
+                    PK_CUDA(cudaMemcpy(&o2[0], ctx.lists.v.off + T.level_off[l], sizeof(int64_t), cudaMemcpyDeviceToHost));
+                    PK_CUDA(cudaMemcpy(&o2[1], ctx.lists.v.off + T.level_off[l + 1], sizeof(int64_t),
+                                       cudaMemcpyDeviceToHost));
+                    v_lat += (double)(o2[1] - o2[0]);
+                }
                 if (!i8_apps[l]) continue;
                 int64_t o2[2];
                 PK_CUDA(cudaMemcpy(&o2[0], ctx.lists.v.off + T.level_off[l], sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -1333,6 +1365,8 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                                    cudaMemcpyDeviceToHost));
                 v_i8 += (double)(o2[1] - o2[0]);
             }
+            // lattice levels: V applications served by the convolution (dense-equivalent FLOP)
+            if (v_lat > 0) prof.work("m2l_lattice", v_lat, dense);
             if (v_i8 > 0) {
                 prof.work("m2l_i8", v_i8, 2.0 * ctx.i8.nmod * K * K);
                 if (mma_rows_zeroed) { // MMA rows issued vs V applications (tile padding / union waste)

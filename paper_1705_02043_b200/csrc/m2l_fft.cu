@@ -1098,6 +1098,10 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     const int ks = ops.ks, kt = ops.kt, n = ops.n;
     const int64_t M3 = S.M3, N3 = (int64_t)f.N * f.N * f.N, nl = a.box1 - a.box0;
     int *box_of = ws.get<int>("lat_boxof", M3 * 8);
+    auto mark = [&](const char *stage, int begin) {
+        if (a.mark) a.mark(a.user, stage, begin);
+    };
+    mark("lat_fwd", 1);
     PK_CUDA(cudaMemsetAsync(box_of, 0xff, M3 * 8 * sizeof(int), st));
     lat_boxmap_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(a.cell, a.box0, nl, m[1], m[2], box_of);
     // surface values -> lattice spectra (in place) -> surface spectra Psi~[kappa][c][b][w]
@@ -1126,8 +1130,10 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
         lat_surface_fwd_kernel<<<(unsigned)ng, LS_THREADS, fsm, st>>>(A, p, n, f.gidx, reinterpret_cast<double2 *>(psi));
     }
     }
-    // pointwise products over (kappa, w)
+    mark("lat_fwd", 0);
+    // pointwise products over (kappa, w): one pass over the stencil spectra, Psi~ and Q~
     double *q = ws.get<double>("lat_q", (size_t)M3 * 8 * kt * f.nw * 2);
+    mark("lat_mul", 1);
     const dim3 grid((f.nw + 127) / 128, (unsigned)M3);
     if (ks == 1)
         lat_mul_kernel<1><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
@@ -1135,6 +1141,10 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     else
         lat_mul_kernel<3><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
                                                 reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
+    mark("lat_mul", 0);
+    if (a.work) // algorithmic bytes: M (14 classes x symmetric components) + Psi~ in, Q~ out, 16 B each
+        a.work(a.user, "lat_mul", (double)M3 * f.nw, 16.0 * (LAT_E * (ks * (ks + 1) / 2) + 8 * ks + 8 * kt));
+    mark("lat_inv", 1);
     // surface values per lattice frequency -> inverse lattice transform -> check potentials
     // (unnormalised transforms: 1 / (N^3 M3))
     switch (p) {
@@ -1159,6 +1169,7 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     lat_scatter_surface_kernel<<<(unsigned)std::min<int64_t>((M3 * St + 255) / 256, 148 * 32), 256, 0, st>>>(
         A, box_of, M3, kt, n, a.alpha / ((double)N3 * (double)M3), ops.Kp, a.Y);
     PK_CUDA(cudaGetLastError());
+    mark("lat_inv", 0);
     return launches + 6;
 }
 

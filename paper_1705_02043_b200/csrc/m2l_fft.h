@@ -73,6 +73,13 @@ struct LatticeLevelArgs {
     const double *X = nullptr;     // phi_up [box][Kp]
     double *Y = nullptr;           // q [box][Kp]: Y += alpha * M2L
     double alpha = 1.0;
+    // stage profiler hook (optional): mark(user, stage, 1) before / (.., 0) after the phases
+    // "lat_fwd" (gather, lattice FFT, surface DFT), "lat_mul" (pointwise products) and
+    // "lat_inv" (surface DFT, lattice FFT, scatter); work(user, stage, units, per_unit)
+    // reports lat_mul's algorithmic bytes
+    void (*mark)(void *user, const char *stage, int begin) = nullptr;
+    void (*work)(void *user, const char *stage, double units, double per_unit) = nullptr;
+    void *user = nullptr;
 };
 // device workspace bytes the level needs (kernel spectra, grids, lattice spectra)
 int64_t m2l_lattice_bytes(const KifmmOps &ops, int level, const int periodic[3]);
