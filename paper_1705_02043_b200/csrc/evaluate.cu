@@ -754,6 +754,7 @@ void pinv_level(pkgpu_context &ctx, KifmmOps &ops, bool up, int64_t lo, int64_t 
         a.nvalid = (int)(hi - lo);
         a.box0 = (int)lo;
         a.ncols = round_up(a.nvalid, BN);
+        a.napps = a.nvalid;
     }
     if (a.ncols <= 0) return;
     a.A = up ? ops.Ut_up : ops.Ut_dn;
@@ -1055,6 +1056,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 a.Y = Q;
                 a.alpha = std::ldexp(1.0, l); // q += 2^l M2M_o phi_child (src/fmm.cpp:547)
                 a.beta = 0.0;
+                a.napps = (int)std::min<int64_t>(8 * (hi - lo), 1 << 30); // the level's parents x 8 children
                 pm = prof.begin("m2m");
                 ctx.launches += gather_gemm(a, ws, st, ctx.num_sms);
                 if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches
@@ -1278,6 +1280,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 b.Y = Q;
                 b.alpha = std::ldexp(1.0, l) * 0.5; // q += (2^l / 2) L2L_o phi_parent (src/fmm.cpp:590-591)
                 b.beta = 1.0;
+                b.napps = (int)std::min<int64_t>(hi - lo, 1 << 30); // one parent per box of the level
                 pm = prof.begin("l2l");
                 ctx.launches += gather_gemm(b, ws, st, ctx.num_sms);
                 if (ctx.profiling) ctx.stats["dmma_gemm"].units += 1; // gather_gemm_tma_kernel launches

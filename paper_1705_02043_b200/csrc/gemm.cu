@@ -291,6 +291,121 @@ __global__ void split_reduce_kernel(KParams kp) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Skinny launches (the top levels of the tree: at most SK_MAXAPP (column, slot) pairs, e.g.
+// the 8 + 64 M2M translations into levels 0 and 1 or the pseudo-inverse of 1-64 boxes) are
+// bound by streaming the operator matrices once, not by the FLOPs: on the tile kernel they
+// cost 40-75 us each at cfg2 (a 128 x 64 tile per unit whatever the column count, split-K
+// partials, three launches). Here a warp owns one output row for every column: it streams
+// that row of each matrix the pairs use (all rows prefetched into L2 up front, then held in
+// registers), takes the dot product with each pair's source vector (L1 / L2 hits) and sums a
+// column's slots in slot order -- one launch, no partials, bitwise deterministic.
+constexpr int SK_MAXAPP = 64;  // (column, slot) pairs
+constexpr int SK_MAXC = 1024;  // columns of the (padded) layout
+constexpr int SK_MAXJ = 24;    // Kp / 64
+constexpr int SK_WARPS = 4;
+
+__global__ void __launch_bounds__(SK_WARPS * 32) skinny_gemm_kernel(GemmArgs a) {
+    __shared__ int s_ci[SK_MAXAPP], s_src[SK_MAXAPP], s_mat[SK_MAXAPP]; // pair: column index, source box, matrix
+    __shared__ int s_col[SK_MAXAPP];                                    // valid columns
+    __shared__ short s_cmap[SK_MAXC];                                   // column -> index in s_col
+    __shared__ int s_wcnt[SK_WARPS], s_napp, s_ncol;
+    __shared__ double s_acc[SK_WARPS][SK_MAXAPP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NT = SK_WARPS * 32;
+    if (tid == 0) s_napp = s_ncol = 0;
+    for (int i = tid; i < SK_WARPS * SK_MAXAPP; i += NT) (&s_acc[0][0])[i] = 0.0;
+    __syncthreads();
+    // ordered compaction of the valid columns, then of the pairs (slot-major, column order)
+    for (int c0 = 0; c0 < a.ncols; c0 += NT) {
+        const int c = c0 + tid;
+        const bool v = c < a.ncols && col_out(a, c) >= 0;
+        const unsigned b = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) s_wcnt[warp] = __popc(b);
+        __syncthreads();
+        int base = s_ncol;
+        for (int w = 0; w < warp; w++) base += s_wcnt[w];
+        const int pos = base + __popc(b & ((1u << lane) - 1));
+        if (c < a.ncols) s_cmap[c] = v ? (short)min(pos, SK_MAXAPP - 1) : (short)-1;
+        if (v && pos < SK_MAXAPP) s_col[pos] = c;
+        __syncthreads();
+        if (tid == 0) {
+            int n = s_ncol;
+            for (int w = 0; w < SK_WARPS; w++) n += s_wcnt[w];
+            s_ncol = min(n, SK_MAXAPP);
+        }
+        __syncthreads();
+    }
+    const int total = a.nslots * a.ncols;
+    for (int e0 = 0; e0 < total; e0 += NT) {
+        const int e = e0 + tid;
+        int slot = 0, c = 0, sb = -1;
+        if (e < total) {
+            slot = e / a.ncols, c = e % a.ncols;
+            if (col_out(a, c) >= 0) sb = col_src(a, slot, c);
+        }
+        const bool v = sb >= 0;
+        const unsigned b = __ballot_sync(0xffffffffu, v);
+        if (lane == 0) s_wcnt[warp] = __popc(b);
+        __syncthreads();
+        int base = s_napp;
+        for (int w = 0; w < warp; w++) base += s_wcnt[w];
+        const int pos = base + __popc(b & ((1u << lane) - 1));
+        if (v && pos < SK_MAXAPP) {
+            s_ci[pos] = s_cmap[c];
+            s_src[pos] = sb;
+            s_mat[pos] = slot_matrix(a, slot, c / BN);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int n = s_napp;
+            for (int w = 0; w < SK_WARPS; w++) n += s_wcnt[w];
+            s_napp = min(n, SK_MAXAPP);
+        }
+        __syncthreads();
+    }
+    const int napp = s_napp, ncolv = s_ncol;
+    const int r = blockIdx.x * SK_WARPS + warp;
+    if (r >= a.Kp) return;
+    const int nj = a.Kp / 64;
+    // every matrix row this warp will read, requested from DRAM at once
+    for (int p = 0, prev = -1; p < napp; p++) {
+        const int m = s_mat[p];
+        if (m == prev) continue;
+        prev = m;
+        const char *row = reinterpret_cast<const char *>(a.A + ((int64_t)m * a.Kp + r) * a.Kp);
+        for (int off = lane * 128; off < a.Kp * 8; off += 32 * 128)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(row + off));
+    }
+    double2 ar[SK_MAXJ];
+    int cur = -1;
+    for (int p = 0; p < napp; p++) {
+        const int m = s_mat[p];
+        if (m != cur) {
+            cur = m;
+            const double2 *row = reinterpret_cast<const double2 *>(a.A + ((int64_t)m * a.Kp + r) * a.Kp) + lane;
+#pragma unroll
+            for (int j = 0; j < SK_MAXJ; j++)
+                if (j < nj) ar[j] = __ldg(row + 32 * j);
+        }
+        const double2 *x = reinterpret_cast<const double2 *>(a.X + (int64_t)s_src[p] * a.Kp) + lane;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < SK_MAXJ; j++)
+            if (j < nj) {
+                const double2 xv = __ldg(x + 32 * j);
+                d0 = fma(ar[j].x, xv.x, d0);
+                d1 = fma(ar[j].y, xv.y, d1);
+            }
+        double d = d0 + d1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0) s_acc[warp][s_ci[p]] += d; // a column's slots in slot order
+    }
+    __syncwarp();
+    for (int ci = lane; ci < ncolv; ci += 32) store_final(a, r, s_col[ci], s_acc[warp][ci]);
+}
+
 // one warp per row
 __global__ void gemv_kernel(const double *__restrict__ A, int rows, int cols, int lda, const double *__restrict__ x,
                             double *__restrict__ y, double alpha, double beta, const double *rdiv, double eps) {
@@ -374,6 +489,12 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     if (a.ncols == 0 || a.nslots == 0) return 0;
     if (a.Kp % 64 != 0 || a.ncols % BN != 0 || a.nslots > MAX_SLOTS)
         throw RuntimeError("gather_gemm: bad shape");
+    if (a.napps > 0 && a.napps <= std::min<int64_t>(tuning().gemm_skinny_apps, SK_MAXAPP) && a.ncols <= SK_MAXC &&
+        a.Kp / 64 <= SK_MAXJ) {
+        skinny_gemm_kernel<<<(a.Kp + SK_WARPS - 1) / SK_WARPS, SK_WARPS * 32, 0, st>>>(a);
+        PK_CUDA(cudaGetLastError());
+        return 1;
+    }
     // 128-row tiles for every K: the TMA zero-fills operator rows past Kp (3D tensor map,
     // out-of-bounds) and the epilogue drops them
     constexpr int BMsel = 128;

@@ -35,6 +35,8 @@ struct GemmArgs {
     double alpha = 1.0, beta = 0.0;  // y = beta*y + alpha*acc
     const double *rdiv = nullptr;    // pinv stage 1: y = (rdiv[r] > rdiv_eps) ? acc / rdiv[r] : 0
     double rdiv_eps = 0.0;
+    int napps = 0;                   // upper bound on the (valid column, sourced slot) pairs when the caller
+                                     // knows it (the top levels: 1-64): such launches take the skinny kernel
 };
 
 constexpr int kGemmBN = 64;

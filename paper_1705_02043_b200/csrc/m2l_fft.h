@@ -6,7 +6,8 @@
 // centres, so for a fixed cell offset d the operator is a convolution on the lattice:
 //   q_a(g_i) = sum_b sum_j k_{d,ab}(g_i - g_j) phi_b(g_j),  k_{d,ab}(dg) = K_ab(dg D - d)
 // (root scale; level l scales by 2^l, degree -1 kernels, as the dense path). On an N^3 grid,
-// N = 2p, the cyclic convolution equals the linear one at every surface point. Per level:
+// N = 2p - 1 (every surface difference once), the cyclic convolution equals the linear one at
+// every surface point. Per level:
 //   phi_b of every source box scattered onto the grid, batched R2C FFTs (cuFFT);
 //   Q^_a(w) = sum over V entries sum_b K^_{d,ab}(w) Phi^_{src,b}(w)   (fft_hadamard_kernel);
 //   batched C2R FFTs, check potentials gathered at the surface points.
@@ -37,7 +38,7 @@ struct LatticeShape {
 };
 
 struct FftOps {
-    int N = 0, nw = 0;               // grid edge 2p; half spectrum N * N * (N / 2 + 1)
+    int N = 0, nw = 0;               // grid edge 2p - 1; half spectrum N * N * (N / 2 + 1)
     double *khat = nullptr;          // [316][kt][ks][nw] complex (interleaved re, im)
     int *gidx = nullptr;             // [n] grid index of surface point i
     bool ready = false;
