@@ -278,6 +278,9 @@ pkgpu_status pkgpu_context_create(int device, pkgpu_context **ctx, char *err, si
         PK_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
         for (auto &e : c->ev) PK_CUDA(cudaEventCreate(&e));
+        PK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        PK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        PK_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         *ctx = c.release();
     });
 }
@@ -288,6 +291,9 @@ void pkgpu_context_destroy(pkgpu_context *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto &e : ctx->ev) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->own_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     delete ctx;
 }

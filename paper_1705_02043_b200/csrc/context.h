@@ -35,6 +35,8 @@ struct pkgpu_context {
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux_stream = nullptr;          // list building beside the upward pass (evaluate.cu)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t launches = 0;
     std::mutex mtx; // calls on one context are serialised (the reference evaluate is reentrant per call)
     pkgpu::OperatorCache ops;

@@ -971,37 +971,48 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             }
         }
         Layout Lay = build_layout(ctx, T, lmask, lat, st);
-        build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, st,
-                         &ctx.launches, lmask);
-        // the lattice levels' V lists must be exactly the stencil (they are for filled levels;
-        // a level that is not falls back to the dense product)
-        if (std::any_of(Lay.lat, Lay.lat + T.depth + 1, [](int v) { return v != 0; })) {
-            ctx.launches += m2l_fft_prepare(ops, ws, st);
-            int *bad = ws.get<int>("lat_bad", kMaxLevels + 1);
-            PK_CUDA(cudaMemsetAsync(bad, 0, (kMaxLevels + 1) * sizeof(int), st));
-            for (int l = 1; l <= T.depth; l++) {
-                if (!Lay.lat[l]) continue;
-                LatticeLevelArgs la;
-                la.level = l;
-                for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
-                la.box0 = T.level_off[l];
-                la.box1 = T.level_off[l + 1];
-                la.cell = T.cell;
-                ctx.launches += m2l_lattice_check(ops, la, Lay.m2l_table + Lay.colbase[l], Lay.ncols,
-                                                  Lay.out_box + Lay.colbase[l],
-                                                  (int)(Lay.colbase[l + 1] - Lay.colbase[l]), bad + l, ws, st);
+        // U / W / X lists, the M2L gather table and the lattice check feed the downward pass only:
+        // on a single rank they run on the context's auxiliary stream while the upward pass
+        // (S2M, M2M, pinv: layout only) runs on the work stream -- forked here, joined before
+        // the X pass. Profiling keeps everything on the work stream (stage times add up).
+        const bool overlap_lists = !partitioned && !ctx.profiling && tuning().overlap_lists && ctx.aux_stream;
+        auto lists_stage = [&](cudaStream_t ls_st) {
+            build_lists_eval(T, ls, ctx.lists, Lay.m2l_table, Lay.ncols, Lay.col_of_box, ops.slot_of_code, ls_st,
+                             &ctx.launches, lmask);
+            // the lattice levels' V lists must be exactly the stencil (they are for filled levels;
+            // a level that is not falls back to the dense product)
+            if (std::any_of(Lay.lat, Lay.lat + T.depth + 1, [](int v) { return v != 0; })) {
+                ctx.launches += m2l_fft_prepare(ops, ws, ls_st);
+                int *bad = ws.get<int>("lat_bad", kMaxLevels + 1);
+                PK_CUDA(cudaMemsetAsync(bad, 0, (kMaxLevels + 1) * sizeof(int), ls_st));
+                for (int l = 1; l <= T.depth; l++) {
+                    if (!Lay.lat[l]) continue;
+                    LatticeLevelArgs la;
+                    la.level = l;
+                    for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
+                    la.box0 = T.level_off[l];
+                    la.box1 = T.level_off[l + 1];
+                    la.cell = T.cell;
+                    ctx.launches += m2l_lattice_check(ops, la, Lay.m2l_table + Lay.colbase[l], Lay.ncols,
+                                                      Lay.out_box + Lay.colbase[l],
+                                                      (int)(Lay.colbase[l + 1] - Lay.colbase[l]), bad + l, ws, ls_st);
+                }
+                int hb[kMaxLevels + 1];
+                PK_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, ls_st));
+                PK_CUDA(cudaStreamSynchronize(ls_st));
+                static const bool dbg = std::getenv("PKGPU_LATTICE_DEBUG") != nullptr;
+                for (int l = 1; l <= T.depth; l++) {
+                    if (dbg && Lay.lat[l])
+                        std::fprintf(stderr, "lattice level %d: %lld boxes, %d V-list mismatches\n", l,
+                                     (long long)(T.level_off[l + 1] - T.level_off[l]), hb[l]);
+                    if (Lay.lat[l] && hb[l]) Lay.lat[l] = 0; // dense fallback (DMMA)
+                }
             }
-            int hb[kMaxLevels + 1];
-            PK_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, st));
-            PK_CUDA(cudaStreamSynchronize(st));
-            static const bool dbg = std::getenv("PKGPU_LATTICE_DEBUG") != nullptr;
-            for (int l = 1; l <= T.depth; l++) {
-                if (dbg && Lay.lat[l])
-                    std::fprintf(stderr, "lattice level %d: %lld boxes, %d V-list mismatches\n", l,
-                                 (long long)(T.level_off[l + 1] - T.level_off[l]), hb[l]);
-                if (Lay.lat[l] && hb[l]) Lay.lat[l] = 0; // dense fallback (DMMA)
-            }
-        }
+        };
+        if (overlap_lists)
+            PK_CUDA(cudaEventRecord(ctx.ev_fork, st)); // tree + layout complete
+        else
+            lists_stage(st);
         prof.end(pm);
         // pseudo-inverse scratch: one level at a time (indexed by box id through a level offset)
         int64_t maxlev = 1;
@@ -1065,6 +1076,13 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             pm = prof.begin("pinv_up");
             pinv_level(ctx, ops, true, lo, hi, l, Q, Tm - lo * Kp, Pup, st, PP, Lay);
             prof.end(pm);
+        }
+        if (overlap_lists) {
+            // the upward pass is queued; build the lists beside it and join
+            PK_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.ev_fork, 0));
+            lists_stage(ctx.aux_stream);
+            PK_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux_stream));
+            PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join, 0));
         }
         if (halo) {
             // straddlers summed, then the halo of V / W sources from their owners

@@ -503,12 +503,14 @@ __global__ void lat_seen_kernel(const int *__restrict__ seen, int64_t nl, int *b
 // offset class e is loaded once and applied to every (o, c) pair with c - o = e
 template <int KS>
 __global__ void __launch_bounds__(128) lat_mul_kernel(const double2 *__restrict__ M, const double2 *__restrict__ Psi,
-                                                      double2 *__restrict__ Q, int nw) {
+                                                      double2 *__restrict__ Q, int nw, int64_t total) {
     constexpr int NC = KS * (KS + 1) / 2;
     __shared__ double2 ps[8 * KS][128];
-    const int w = blockIdx.x * 128 + threadIdx.x;
-    const int64_t kap = blockIdx.y;
-    const bool on = w < nw;
+    // flat (kappa, w) index: nw = N N (N / 2 + 1) is odd-sized, so a block may span two kappa
+    const int64_t t = blockIdx.x * (int64_t)128 + threadIdx.x;
+    const bool on = t < total;
+    const int64_t kap = on ? t / nw : 0;
+    const int w = on ? (int)(t % nw) : 0;
     const int64_t base = kap * 8 * KS * nw;
 #pragma unroll
     for (int j = 0; j < 8 * KS; j++) ps[j][threadIdx.x] = on ? Psi[base + (int64_t)j * nw + w] : make_double2(0.0, 0.0);
@@ -541,12 +543,21 @@ __global__ void __launch_bounds__(128) lat_mul_kernel(const double2 *__restrict_
     };
     if (on) {
         // each stored class serves e and -e (M_{-e} = conj(M_e)): one load per class
-        for (int ec = 0; ec < LAT_E; ec++) {
-            double2 m[NC];
+        // (fully unrolled: the octant pairs of each class resolve at compile time, and the
+        // next class's spectra are in flight while this one is applied)
+        double2 m[NC], mn[NC];
 #pragma unroll
-            for (int k = 0; k < NC; k++) m[k] = M[((kap * LAT_E + ec) * NC + k) * nw + w];
+        for (int k = 0; k < NC; k++) m[k] = M[(kap * LAT_E * NC + k) * nw + w];
+#pragma unroll
+        for (int ec = 0; ec < LAT_E; ec++) {
+            if (ec + 1 < LAT_E) {
+#pragma unroll
+                for (int k = 0; k < NC; k++) mn[k] = M[((kap * LAT_E + ec + 1) * NC + k) * nw + w];
+            }
             apply(13 + ec, m, false);
             if (ec) apply(13 - ec, m, true);
+#pragma unroll
+            for (int k = 0; k < NC; k++) m[k] = mn[k];
         }
     }
     if (!on) return;
@@ -1141,13 +1152,16 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     // pointwise products over (kappa, w): one pass over the stencil spectra, Psi~ and Q~
     double *q = ws.get<double>("lat_q", (size_t)M3 * 8 * kt * f.nw * 2);
     mark("lat_mul", 1);
-    const dim3 grid((f.nw + 127) / 128, (unsigned)M3);
+    const int64_t total = M3 * f.nw;
+    const unsigned grid = (unsigned)((total + 127) / 128);
     if (ks == 1)
         lat_mul_kernel<1><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
-                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
+                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q),
+                                                f.nw, total);
     else
         lat_mul_kernel<3><<<grid, 128, 0, st>>>(reinterpret_cast<const double2 *>(S.M),
-                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q), f.nw);
+                                                reinterpret_cast<const double2 *>(psi), reinterpret_cast<double2 *>(q),
+                                                f.nw, total);
     mark("lat_mul", 0);
     if (a.work) // algorithmic bytes: M (14 classes x symmetric components) + Psi~ in, Q~ out, 16 B each
         a.work(a.user, "lat_mul", (double)M3 * f.nw, 16.0 * (LAT_E * (ks * (ks + 1) / 2) + 8 * ks + 8 * kt));

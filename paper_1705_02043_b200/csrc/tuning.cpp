@@ -40,6 +40,7 @@ const Tuning &tuning() {
         r.gemm_min_iters = env_int("PKGPU_GEMM_MINIT", r.gemm_min_iters, 1);
         r.gemm_min_iters_small = env_int("PKGPU_GEMM_MINIT_SMALL", r.gemm_min_iters_small, 1);
         r.gemm_skinny_apps = env_int("PKGPU_GEMM_SKINNY", r.gemm_skinny_apps, 0);
+        r.overlap_lists = env_int("PKGPU_OVERLAP_LISTS", 1, 0) != 0;
         r.list_warp_max = env_int("PKGPU_LIST_WARP_MAX", r.list_warp_max, 0);
         r.leaf_tt = (int)env_int("PKGPU_LEAF_TT", r.leaf_tt, 1);
         r.m2l_lattice = env_int("PKGPU_M2L_LATTICE", 1, 0) != 0;
