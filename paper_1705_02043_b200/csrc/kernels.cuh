@@ -59,10 +59,13 @@ __device__ __forceinline__ double surf_coord(double half, double t, double c) { 
 __device__ __forceinline__ double rinv_fast(double r2) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+    // r2 == 0 (ftz: anything below the smallest normal) -> 0: an integer select on the seed's high
+    // word (MUFU.RSQ64H defines only that word; the low word of the approximation is zero), off the
+    // FP64 pipe; the correction maps a zero seed to zero
+    y = __hiloint2double(__double2hiint(r2) < 0x00100000 ? 0 : __double2hiint(y), 0);
     const double e = __fma_rn(-r2 * y, y, 1.0);  // 1 - r2 y^2
     const double c = __fma_rn(0.375, e, 0.5);    // 1/2 + 3/8 e
-    y = __fma_rn(y * e, c, y);
-    return r2 > 0.0 ? y : 0.0;
+    return __fma_rn(y * e, c, y);
 }
 
 // Laplace pair: acc += rho / r

@@ -20,8 +20,15 @@ constexpr int MAXU = 128;
 
 template <int KERNEL> struct Stage {
     static constexpr int KS = KERNEL == 0 ? 1 : 3;
-    double x[SB], y[SB], z[SB];
-    double d[SB * KS];
+    // a staged source is two (Laplace) or three (Stokes) 16-byte words: (x, y), (z, d0), (d1, d2) --
+    // one LDS.128 each in the pair loops instead of 4 / 6 LDS.64 with separate index arithmetic
+    double2 xy[SB], zd[SB];
+    double2 dd[KERNEL == 0 ? 1 : SB];
+    __device__ __forceinline__ void put(int q, double x, double y, double z, const double (&d)[KS]) {
+        xy[q] = make_double2(x, y);
+        zd[q] = make_double2(z, d[0]);
+        if (KERNEL != 0) dd[q] = make_double2(d[1], d[2]);
+    }
     double sx[MAXSEG], sy[MAXSEG], sz[MAXSEG];
     int begin[MAXSEG + 1];
     int cnt[MAXSEG]; // count coincidences in this segment
@@ -36,14 +43,15 @@ __device__ __forceinline__ void accumulate(const Stage<KERNEL> &S, double tx, do
         const int end = S.begin[s + 1];
         int ncoin = 0;
         for (int q = S.begin[s] + j; q < end; q += G) {
+            const double2 a = S.xy[q], b = S.zd[q];
             if (KERNEL == 0) {
-                pair_laplace(ux, uy, uz, S.x[q], S.y[q], S.z[q], S.d[q], acc[0]);
+                pair_laplace(ux, uy, uz, a.x, a.y, b.x, b.y, acc[0]);
             } else {
-                pair_stokes(ux, uy, uz, S.x[q], S.y[q], S.z[q], S.d[3 * q], S.d[3 * q + 1], S.d[3 * q + 2], acc[0],
-                            acc[1], acc[2]);
+                const double2 c = S.dd[q];
+                pair_stokes(ux, uy, uz, a.x, a.y, b.x, b.y, c.x, c.y, acc[0], acc[1], acc[2]);
             }
             if (S.cnt[s]) {
-                const double rx = ux - S.x[q], ry = uy - S.y[q], rz = uz - S.z[q];
+                const double rx = ux - a.x, ry = uy - a.y, rz = uz - b.x;
                 ncoin += (rx * rx + ry * ry + rz * rz) == 0.0;
             }
         }
@@ -59,11 +67,11 @@ __device__ void stage_surface(Stage<KERNEL> &S, const double *__restrict__ tmpl,
     constexpr int KS = Stage<KERNEL>::KS;
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         const int i = i0 + q;
-        S.x[q] = surf_coord(half, tmpl[3 * i], cx);
-        S.y[q] = surf_coord(half, tmpl[3 * i + 1], cy);
-        S.z[q] = surf_coord(half, tmpl[3 * i + 2], cz);
+        double d[KS];
 #pragma unroll
-        for (int a = 0; a < KS; a++) S.d[KS * q + a] = phi[KS * i + a];
+        for (int a = 0; a < KS; a++) d[a] = phi[KS * i + a];
+        S.put(q, surf_coord(half, tmpl[3 * i], cx), surf_coord(half, tmpl[3 * i + 1], cy),
+              surf_coord(half, tmpl[3 * i + 2], cz), d);
     }
     if (threadIdx.x == 0) {
         S.nseg = 1;
@@ -78,12 +86,13 @@ template <int KERNEL>
 __device__ __forceinline__ void stage_point(Stage<KERNEL> &S, int q, const double4 *__restrict__ pos,
                                             const double4 *__restrict__ f, int64_t k) {
     const double4 p = pos[k];
-    S.x[q] = p.x, S.y[q] = p.y, S.z[q] = p.z;
+    S.xy[q] = make_double2(p.x, p.y);
     if (KERNEL == 0) {
-        S.d[q] = p.w;
+        S.zd[q] = make_double2(p.z, p.w);
     } else {
         const double4 v = f[k];
-        S.d[3 * q] = v.x, S.d[3 * q + 1] = v.y, S.d[3 * q + 2] = v.z;
+        S.zd[q] = make_double2(p.z, v.x);
+        S.dd[q] = make_double2(v.y, v.z);
     }
 }
 
@@ -128,14 +137,15 @@ __device__ __forceinline__ void accumulate_tt(const Stage<KERNEL> &S, const doub
         const int end = S.begin[s + 1];
 #pragma unroll 2
         for (int q = S.begin[s] + j; q < end; q += G) {
-            const double sx = S.x[q], sy = S.y[q], sz = S.z[q];
+            const double2 a = S.xy[q], b = S.zd[q];
+            double2 c = make_double2(0.0, 0.0);
+            if (KERNEL != 0) c = S.dd[q];
 #pragma unroll
             for (int k = 0; k < TT; k++) {
                 if (KERNEL == 0)
-                    pair_laplace(ux[k], uy[k], uz[k], sx, sy, sz, S.d[q], acc[k][0]);
+                    pair_laplace(ux[k], uy[k], uz[k], a.x, a.y, b.x, b.y, acc[k][0]);
                 else
-                    pair_stokes(ux[k], uy[k], uz[k], sx, sy, sz, S.d[3 * q], S.d[3 * q + 1], S.d[3 * q + 2], acc[k][0],
-                                acc[k][1], acc[k][2]);
+                    pair_stokes(ux[k], uy[k], uz[k], a.x, a.y, b.x, b.y, c.x, c.y, acc[k][0], acc[k][1], acc[k][2]);
             }
         }
     }
@@ -395,9 +405,10 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) direct_kernel(Direct
             __syncthreads();
             for (int q = tid; q < cnt; q += NT) {
                 const int64_t k = s0 + q;
-                S.x[q] = P.src[3 * k], S.y[q] = P.src[3 * k + 1], S.z[q] = P.src[3 * k + 2];
+                double d[KS];
 #pragma unroll
-                for (int a = 0; a < KS; a++) S.d[KS * q + a] = P.den[KS * k + a];
+                for (int a = 0; a < KS; a++) d[a] = P.den[KS * k + a];
+                S.put(q, P.src[3 * k], P.src[3 * k + 1], P.src[3 * k + 2], d);
             }
             if (tid == 0) {
                 S.nseg = 1, S.begin[0] = 0, S.begin[1] = cnt;
@@ -457,9 +468,10 @@ template <int KERNEL> __global__ void __launch_bounds__(NT) root_check_kernel(Ro
         __syncthreads();
         for (int q = tid; q < cnt; q += NT) {
             const int64_t k = s0 + q;
-            S.x[q] = P.src[3 * k], S.y[q] = P.src[3 * k + 1], S.z[q] = P.src[3 * k + 2];
+            double d[KS];
 #pragma unroll
-            for (int a = 0; a < KS; a++) S.d[KS * q + a] = P.den[KS * k + a];
+            for (int a = 0; a < KS; a++) d[a] = P.den[KS * k + a];
+            S.put(q, P.src[3 * k], P.src[3 * k + 1], P.src[3 * k + 2], d);
         }
         if (tid == 0) {
             S.nseg = 1, S.begin[0] = 0, S.begin[1] = cnt, S.cnt[0] = 0;
