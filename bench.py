@@ -48,10 +48,15 @@ REFDUMP = os.path.join(REPO, "oracle", "_ref", "refdump")
 REFDUMP_NATIVE = os.path.join(REPO, "oracle", "_ref", "refdump_native")
 FP64_VEC_PEAK_TFLOPS = 34.23  # measured DFMA loop on this pool (profiles/r01_fp64_peaks.jsonl)
 FP64_VEC_PEAK_SOURCE = "measured: DFMA loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl)"
-GEMM_NCU_TRAFFIC = None  # filled from the ncu --set full capture of the level-4 pinv launch (profiles/)
-GEMM_NCU_NOTE = None
-LATMUL_NCU_TRAFFIC = None
-LATMUL_NCU_NOTE = None
+GEMM_NCU_TRAFFIC = 73.1e6  # dram read + write bytes of a level-4 gather_gemm_tma_kernel launch
+GEMM_NCU_NOTE = "ncu --set full capture of the step's first gather_gemm_tma_kernel launch (pinv_up U^T factor, level 4, " \
+                "4096 columns): 35.9 MB read + 37.3 MB written (split-K partials); DMMA pipe 81.5% active " \
+                "(profiles/r02_lattice_step_ncu.txt). Algorithmic bytes of that launch: operator 6.3 MB + vectors in / out " \
+                "58.7 MB. The per-launch mean above covers all 28 launches per step (levels 0-4)"
+LATMUL_NCU_TRAFFIC = 1.93e9  # dram read + write bytes of the level-4 lat_mul_kernel launch
+LATMUL_NCU_NOTE = "ncu --set full capture of the level-4 launch (512 lattice x 1800 surface frequencies, algorithmic " \
+                  "1.946 GB): 1.593 GB read + 0.337 GB written in 336 us = 5.75 TB/s, 0.88 of the copy bandwidth " \
+                  "(profiles/r02_lattice_step_ncu.txt); the per-launch mean above averages levels 1-4"
 LEAF_NCU_TRAFFIC = 40.5e6  # dram read + write bytes per leaf_kernel launch (profiles/r02_leaf_ncu.txt)
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
