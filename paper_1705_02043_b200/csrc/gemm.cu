@@ -20,6 +20,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
+#include <vector>
 #include <tuple>
 
 #include <cudaTypedefs.h>
@@ -58,6 +60,14 @@ struct KParams {
     int rowtiles, coltiles; // unit = row + rowtiles * (col + coltiles * split)
     int total_units;
     int *counter;           // persistent scheduler (self-resetting: the CTA taking the last fetch zeroes it)
+    // hybrid schedule (plan_hybrid below): whole tiles for the full waves, then the rest of the
+    // iteration space cut into one equal chunk per resident CTA; a chunk is 1-3 pieces, each
+    // inside one tile. Null: the uniform split above.
+    const int4 *pieces;     // (tile = row + rowtiles * col, it0, it1 of nit_nom, partial index or -1: whole tile)
+    const int2 *chunks;     // [total_units] piece range [x, y)
+    const int *tile_parts;  // [rowtiles * coltiles] partials per tile (0: written directly)
+    int nit_nom;            // nominal iterations per tile the plan was cut in (nslots * Kp / 16)
+    int reduce_col0;        // first column holding a split tile
 };
 
 struct TmaParams {
@@ -112,7 +122,7 @@ __device__ __forceinline__ void store_final(const GemmArgs &a, int r, int c, dou
 
 // epilogue of one accumulator element: a split unit's partial, or the final value
 __device__ __forceinline__ void store_out(const KParams &kp, int split, int r, int c, double v) {
-    if (kp.nsplit > 1) {
+    if (split >= 0) {
         if (r < kp.a.Kp) kp.part[((int64_t)split * kp.a.ncols + c) * kp.a.Kp + r] = v;
         return;
     }
@@ -189,13 +199,30 @@ __global__ void __maxnreg__(96)
         const int unit = s_unit;
         __syncthreads();
         if (unit >= kp.total_units) break;
-        const int rt = unit % kp.rowtiles;
-        const int rest = unit / kp.rowtiles;
-        const int ct = rest % kp.coltiles, split = rest / kp.coltiles;
+        int pc0 = unit, pc1 = unit + 1;
+        if (kp.chunks) {
+            const int2 ch = kp.chunks[unit];
+            pc0 = ch.x, pc1 = ch.y;
+        }
+      for (int pc = pc0; pc < pc1; pc++) {
+        int rt, ct, split, it0, it1;
+        if (kp.pieces) {
+            const int4 pd = kp.pieces[pc];
+            rt = pd.x % kp.rowtiles, ct = pd.x / kp.rowtiles;
+            const int64_t niter = (int64_t)(kp.tile_nact ? kp.tile_nact[ct] : 1) * (a.Kp / BK);
+            it0 = (int)(niter * pd.y / kp.nit_nom);
+            it1 = (int)(niter * pd.z / kp.nit_nom);
+            split = pd.w;
+        } else {
+            rt = unit % kp.rowtiles;
+            const int rest = unit / kp.rowtiles;
+            ct = rest % kp.coltiles;
+            split = rest / kp.coltiles;
+            unit_range(kp, kp.tile_nact ? kp.tile_nact[ct] : 1, split, it0, it1);
+            if (kp.nsplit <= 1) split = -1; // the whole tile: final values
+        }
         const int row0 = rt * BM, col0 = ct * BNT;
         const int *slots = kp.tile_slots ? kp.tile_slots + ct * MAX_SLOTS : nullptr;
-        int it0, it1;
-        unit_range(kp, kp.tile_nact ? kp.tile_nact[ct] : 1, split, it0, it1);
         const int n = it1 - it0;
         if (warp == NCW) {
             // ---------------- producer ----------------
@@ -269,18 +296,24 @@ __global__ void __maxnreg__(96)
             }
         }
         g += n;
+      }
     }
 }
 
-__global__ void split_reduce_kernel(KParams kp) {
+__global__ void split_reduce_kernel(KParams kp, int bm, int bnt) {
     const GemmArgs &a = kp.a;
-    const int64_t total = (int64_t)a.ncols * a.Kp;
+    const int64_t total = (int64_t)(a.ncols - kp.reduce_col0) * a.Kp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i / a.Kp), r = (int)(i % a.Kp);
+        const int c = kp.reduce_col0 + (int)(i / a.Kp), r = (int)(i % a.Kp);
         const int ob = col_out(a, c);
         if (ob < 0) continue;
+        int np = kp.nsplit;
+        if (kp.tile_parts) {
+            np = kp.tile_parts[r / bm + kp.rowtiles * (c / bnt)];
+            if (np == 0) continue; // a whole tile, written by the GEMM
+        }
         double v = 0.0;
-        for (int s = 0; s < kp.nsplit; s++) v += kp.part[((int64_t)s * a.ncols + c) * a.Kp + r];
+        for (int s = 0; s < np; s++) v += kp.part[((int64_t)s * a.ncols + c) * a.Kp + r];
         double *y = a.Y + (int64_t)ob * a.Kp + r;
         if (a.rdiv) {
             const double d = a.rdiv[r];
@@ -483,6 +516,65 @@ int *zeroed_counters(Workspace &ws, const char *name, size_t n, cudaStream_t st)
     return p;
 }
 
+// Hybrid schedule for launches of one to a few waves of tiles (cfg2's level-4 pseudo-inverse:
+// 448 tiles on 296 resident CTAs). A uniform split-K (three units per tile there) pays
+// partials for every tile and still ends on a ragged wave. Here the full waves run whole
+// tiles, written directly, and the remaining tiles' iteration space is cut into one equal
+// chunk per resident CTA (a chunk crosses at most two tile boundaries; each piece writes a
+// partial, summed per tile in piece order by split_reduce_kernel: deterministic).
+struct HybridPlan {
+    const int4 *pieces = nullptr;
+    const int2 *chunks = nullptr;
+    const int *tile_parts = nullptr;
+    int nchunks = 0, maxparts = 0, reduce_col0 = 0;
+};
+
+HybridPlan plan_hybrid(Workspace &ws, int rowtiles, int coltiles, int bnt, int resident, int nit, cudaStream_t st) {
+    const std::string key = "gemm_plan_" + std::to_string(rowtiles) + "_" + std::to_string(coltiles) + "_" +
+                            std::to_string(resident) + "_" + std::to_string(nit);
+    const int base = rowtiles * coltiles;
+    const int full = base / resident * resident, rest = base - full;
+    std::vector<int4> pieces;
+    std::vector<int2> chunks;
+    std::vector<int> parts(base, 0);
+    for (int t = 0; t < full; t++) {
+        chunks.push_back(make_int2((int)pieces.size(), (int)pieces.size() + 1));
+        pieces.push_back(make_int4(t, 0, nit, -1));
+    }
+    const int64_t total = (int64_t)rest * nit;
+    for (int k = 0; k < resident; k++) {
+        int64_t pos = total * k / resident;
+        const int64_t hi = total * (k + 1) / resident;
+        if (hi <= pos) continue;
+        const int first = (int)pieces.size();
+        while (pos < hi) {
+            const int tl = (int)(pos / nit);
+            const int64_t tend = std::min<int64_t>(hi, (int64_t)(tl + 1) * nit);
+            const int a0 = (int)(pos - (int64_t)tl * nit), a1 = (int)(tend - (int64_t)tl * nit);
+            const bool whole = a0 == 0 && a1 == nit;
+            pieces.push_back(make_int4(full + tl, a0, a1, whole ? -1 : parts[full + tl]++));
+            pos = tend;
+        }
+        chunks.push_back(make_int2(first, (int)pieces.size()));
+    }
+    HybridPlan P;
+    P.nchunks = (int)chunks.size();
+    for (int v : parts) P.maxparts = std::max(P.maxparts, v);
+    P.reduce_col0 = full / rowtiles * bnt; // tiles are numbered row-fastest: the first column with a split tile
+    const bool fresh = ws.bufs.find(key + "_p") == ws.bufs.end();
+    int4 *dp = ws.get<int4>(key + "_p", pieces.size());
+    int2 *dc = ws.get<int2>(key + "_c", chunks.size());
+    int *dt = ws.get<int>(key + "_t", parts.size());
+    if (fresh) {
+        PK_CUDA(cudaMemcpyAsync(dp, pieces.data(), pieces.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaMemcpyAsync(dc, chunks.data(), chunks.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaMemcpyAsync(dt, parts.data(), parts.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        PK_CUDA(cudaStreamSynchronize(st)); // host temporaries
+    }
+    P.pieces = dp, P.chunks = dc, P.tile_parts = dt;
+    return P;
+}
+
 } // namespace
 
 int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) {
@@ -524,7 +616,20 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     kp.rowtiles = rowtiles;
     kp.coltiles = coltiles;
     kp.total_units = (int)(base * nsplit);
-    if (nsplit > 1) kp.part = ws.get<double>("gemm_part", (size_t)nsplit * a.ncols * a.Kp);
+    // one to a few waves of tiles that the uniform split would cut: the hybrid schedule, when
+    // its tail chunks are still at least gemm_min_iters long
+    bool hybrid = false;
+    if (tu.gemm_hybrid && nsplit > 1 && base >= resident && base < 8 * (int64_t)resident && base % resident != 0 &&
+        (base % resident) * iters / resident >= tu.gemm_min_iters) {
+        const HybridPlan P = plan_hybrid(ws, rowtiles, coltiles, bnt, resident, (int)iters, st);
+        kp.pieces = P.pieces, kp.chunks = P.chunks, kp.tile_parts = P.tile_parts;
+        kp.nit_nom = (int)iters;
+        kp.reduce_col0 = P.reduce_col0;
+        kp.total_units = P.nchunks;
+        kp.nsplit = nsplit = std::max(P.maxparts, 1);
+        hybrid = P.maxparts > 0;
+    }
+    if (nsplit > 1 || hybrid) kp.part = ws.get<double>("gemm_part", (size_t)nsplit * a.ncols * a.Kp);
     int launches = 0;
     if (a.src || a.nslots != 1) { // an identity gather's one slot is active in every tile
         int *tslots = ws.get<int>("gemm_tile_slots", (size_t)coltiles * MAX_SLOTS);
@@ -551,9 +656,10 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     }
     PK_CUDA(cudaGetLastError());
     launches++;
-    if (nsplit > 1) {
-        const int64_t total = (int64_t)a.ncols * a.Kp;
-        split_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, num_sms * 16), 256, 0, st>>>(kp);
+    if (nsplit > 1 || hybrid) {
+        const int64_t total = (int64_t)(a.ncols - kp.reduce_col0) * a.Kp;
+        split_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, num_sms * 16), 256, 0, st>>>(kp, BMsel,
+                                                                                                            bnt);
         PK_CUDA(cudaGetLastError());
         launches++;
     }

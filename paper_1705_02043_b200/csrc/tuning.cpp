@@ -39,6 +39,7 @@ const Tuning &tuning() {
         r.gemm_units_per_cta = env_int("PKGPU_GEMM_UNITS", r.gemm_units_per_cta, 1);
         r.gemm_min_iters = env_int("PKGPU_GEMM_MINIT", r.gemm_min_iters, 1);
         r.gemm_min_iters_small = env_int("PKGPU_GEMM_MINIT_SMALL", r.gemm_min_iters_small, 1);
+        r.gemm_hybrid = env_int("PKGPU_GEMM_HYBRID", 1, 0) != 0;
         r.gemm_skinny_apps = env_int("PKGPU_GEMM_SKINNY", r.gemm_skinny_apps, 0);
         r.overlap_lists = env_int("PKGPU_OVERLAP_LISTS", 1, 0) != 0;
         r.list_warp_max = env_int("PKGPU_LIST_WARP_MAX", r.list_warp_max, 0);

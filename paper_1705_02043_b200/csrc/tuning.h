@@ -29,6 +29,7 @@ struct Tuning {
     int64_t gemm_units_per_cta = 32;   // PKGPU_GEMM_UNITS: DMMA gather-GEMM work units per CTA
     int64_t gemm_min_iters = 16;       // PKGPU_GEMM_MINIT: k-iterations per split-K unit
     int64_t gemm_min_iters_small = 4;  // PKGPU_GEMM_MINIT_SMALL: same, latency-bound one-slot GEMMs
+    bool gemm_hybrid = true;           // PKGPU_GEMM_HYBRID = 0 | 1: whole tiles for the full waves + an equal tail chunk per CTA
     int64_t gemm_skinny_apps = 8;      // PKGPU_GEMM_SKINNY: launches of at most this many (column, slot) pairs
                                        // take the skinny row-per-warp kernel (0: never)
     bool overlap_lists = true;         // PKGPU_OVERLAP_LISTS = 0 | 1: lists on the auxiliary stream beside the upward pass
