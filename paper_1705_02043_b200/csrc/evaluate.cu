@@ -993,6 +993,8 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                     la.box0 = T.level_off[l];
                     la.box1 = T.level_off[l + 1];
                     la.cell = T.cell;
+                    la.srng = T.srng;
+                    la.trng = T.trng;
                     ctx.launches += m2l_lattice_check(ops, la, Lay.m2l_table + Lay.colbase[l], Lay.ncols,
                                                       Lay.out_box + Lay.colbase[l],
                                                       (int)(Lay.colbase[l + 1] - Lay.colbase[l]), bad + l, ws, ls_st);

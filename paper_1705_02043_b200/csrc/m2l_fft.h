@@ -71,6 +71,8 @@ struct LatticeLevelArgs {
     int periodic[3] = {0, 0, 0};
     int64_t box0 = 0, box1 = 0;    // the level's boxes (BFS ids)
     const int4 *cell = nullptr;    // box cells (x, y, z, level)
+    const int2 *srng = nullptr, *trng = nullptr; // boxes' source / target ranges (the check: the evaluate
+                                                 // lists leave out source-less sources and target-less targets)
     const double *X = nullptr;     // phi_up [box][Kp]
     double *Y = nullptr;           // q [box][Kp]: Y += alpha * M2L
     double alpha = 1.0;

@@ -131,3 +131,22 @@ def test_lattice_axis_fft_path(lat_ctx, dmma_ctx):
     print(f"2M uniform p=4: {v_lat:.0f} of {v_all:.0f} V applications on the lattice; vs dense {d:.3e}")
     assert v_lat == v_all > 0  # levels 1-6 all filled at 7.6 points per level-6 box
     assert d <= 1e-12
+
+
+def test_lattice_separate_targets(lat_ctx, dmma_ctx):
+    """Targets that are not the sources (src/fmm.cpp:301-389 builds one tree over both): target
+    boxes without sources carry zero densities on the lattice, source boxes without targets
+    get results nobody reads; the evaluate lists leave both out and the check accepts that."""
+    rng = np.random.default_rng(3)
+    src, f = pk.generate("uniform", 50000, 3, seed=9)
+    trg = np.ascontiguousarray(np.vstack([0.5 * rng.random((8000, 3)), rng.random((2000, 3))]))
+    setup = pk.PeriodicSetup.make(pk.Periodicity.tp, 2)
+    k = pk.KernelSpec.stokeslet()
+    req = pk.EvalRequest(kernel=k, sources=src, strengths=f, targets=trg, setup=setup, p=6,
+                         op=standin_operator(k, setup, 6), leaf_capacity=40)
+    res, v_lat, v_all = lattice_applications(lat_ctx, req)
+    dm = pk.evaluate(req, context=dmma_ctx).potentials
+    d = rel_l2(res, dm)
+    print(f"separate targets: {v_lat:.0f} of {v_all:.0f} V applications on the lattice; vs dense {d:.3e}")
+    assert v_lat > 0.9 * v_all
+    assert d <= 1e-9
