@@ -50,7 +50,7 @@ FP64_VEC_PEAK_TFLOPS = 34.23  # measured DFMA loop on this pool (profiles/r01_fp
 FP64_VEC_PEAK_SOURCE = "measured: DFMA loop, 148 SMs @1965 MHz (profiles/r01_fp64_peaks.jsonl)"
 GEMM_NCU_TRAFFIC = 73.1e6  # dram read + write bytes of a level-4 gather_gemm_tma_kernel launch
 GEMM_NCU_NOTE = "ncu --set full capture of the step's first gather_gemm_tma_kernel launch (pinv_up U^T factor, level 4, " \
-                "4096 columns): 35.9 MB read + 37.3 MB written (split-K partials); DMMA pipe 81.5% active " \
+                "4096 columns, uniform split-K): 35.9 MB read + 37.3 MB written (partials); DMMA pipe 81.5% active " \
                 "(profiles/r02_lattice_step_ncu.txt). Algorithmic bytes of that launch: operator 6.3 MB + vectors in / out " \
                 "58.7 MB. The per-launch mean above covers all 28 launches per step (levels 0-4)"
 LATMUL_NCU_TRAFFIC = 1.93e9  # dram read + write bytes of the level-4 lat_mul_kernel launch
@@ -242,7 +242,8 @@ def translations_roofline(stats, steps):
         return None
     achieved = fl / sec / 1e12
     return {"kernel": "gather_gemm_tma_kernel<128,4,64,8> (M2M, L2L, pinv U^T and V factors: DMMA.8x8x4, TMA operator "
-                      "tiles, cp.async gathered rows) + split_reduce_kernel", "bound": "tensor",
+                      "tiles, cp.async gathered rows) + split_reduce_kernel; the 10 launches of tree levels 0-1 run "
+                      "skinny_gemm_kernel (FP64 FMA, a row per warp)", "bound": "tensor",
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
             "traffic": GEMM_NCU_TRAFFIC, "traffic_note": GEMM_NCU_NOTE,
             "flops_per_launch": fl / n, "ms_per_launch": 1e3 * sec / n, "launches_per_step": n / steps,
