@@ -220,6 +220,15 @@ __global__ void m2m_fill_kernel(TreeView T, const int *__restrict__ list, int n,
     }
 }
 
+// buf[(b - lo) Kp + k] = phi_up[b][k] on the rank of the box's first leaf, 0 elsewhere
+__global__ void level_contrib_kernel(const double *__restrict__ X, const int *__restrict__ rlo, int me, int64_t lo,
+                                     int64_t hi, int Kp, double *__restrict__ buf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (hi - lo) * Kp) return;
+    const int64_t b = lo + i / Kp;
+    buf[i] = rlo[b] == me ? X[b * Kp + i % Kp] : 0.0;
+}
+
 __global__ void add_kernel(double *y, const double *x, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] += x[i];
@@ -622,7 +631,7 @@ Partition build_partition(pkgpu_context &ctx, const DeviceTree &T, int rank, int
 // owners the densities of the V / W sources of its own target boxes (alltoallv). Returns
 // the doubles this rank received (the bytes-moved statistic of the stage profiler).
 int64_t exchange_up(pkgpu_context &ctx, const DeviceTree &T, const Partition &P, const ListSetup &ls, double *Pup,
-                    int Kp, const pkgpu_partition *part, int64_t small_all, cudaStream_t st) {
+                    int Kp, const pkgpu_partition *part, int64_t small_all, cudaStream_t st, unsigned lat_levels = 0) {
     Workspace &ws = ctx.ws;
     const int nb = (int)T.nboxes, R = part->nranks, me = part->rank;
     if (R > 64) throw InvalidArgument("evaluate_partitioned: at most 64 ranks");
@@ -634,7 +643,7 @@ int64_t exchange_up(pkgpu_context &ctx, const DeviceTree &T, const Partition &P,
     compact(ctx, flags, nb, slist, cnt + 2 * R, "exs", st);
     // 2. who needs what, from the replicated tree
     unsigned long long *need = ws.get<unsigned long long>("ex_need", nb);
-    need_masks(T, ls, P.rlo, P.rhi, need, st);
+    need_masks(T, ls, P.rlo, P.rhi, need, st, lat_levels); // lattice levels' V sources come with the level gather
     if (small_all > 0) // modulus-split small-level run: every rank computes every small-level column
         need_small_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(T.view(), small_all,
                                                                 R == 64 ? ~0ull : (1ull << R) - 1ull, need);
@@ -955,9 +964,13 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         if (periodic && ell >= 1)
             for (int a = 0; a < 3; a++) ls.periodic[a] = axes[a];
         // levels whose M2L runs as a lattice convolution (m2l_fft.h): filled lattices within
-        // the device budget, single-rank runs
+        // the device budget. A partitioned evaluate runs them too, replicated on every rank
+        // (a level is one convolution): the level's equivalent densities are gathered after
+        // the upward exchange (below)
+        // -- up to lattice_max_ranks ranks: beyond, a rank's share of the dense products costs
+        // less than the whole level's convolution plus the gather
         int lat[kMaxLevels + 1] = {0};
-        if (ctx.i8.lattice && !partitioned) {
+        if (ctx.i8.lattice && (!partitioned || part->nranks <= tuning().lattice_max_ranks)) {
             const Tuning &tu = tuning();
             int64_t used = 0;
             for (int l = 1; l <= T.depth; l++) {
@@ -995,6 +1008,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                     la.cell = T.cell;
                     la.srng = T.srng;
                     la.trng = T.trng;
+                    la.mask = lmask;
                     ctx.launches += m2l_lattice_check(ops, la, Lay.m2l_table + Lay.colbase[l], Lay.ncols,
                                                       Lay.out_box + Lay.colbase[l],
                                                       (int)(Lay.colbase[l + 1] - Lay.colbase[l]), bad + l, ws, ls_st);
@@ -1089,7 +1103,10 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         if (halo) {
             // straddlers summed, then the halo of V / W sources from their owners
             pm = prof.begin("comm");
-            const int64_t moved = exchange_up(ctx, T, Part, ls, Pup, Kp, part, msplit ? small_max : 0, st);
+            unsigned lat_levels = 0;
+            for (int l = 1; l <= T.depth; l++)
+                if (Lay.lat[l]) lat_levels |= 1u << l;
+            const int64_t moved = exchange_up(ctx, T, Part, ls, Pup, Kp, part, msplit ? small_max : 0, st, lat_levels);
             prof.end(pm);
             prof.work("comm", 8.0 * moved, 0.0);
         } else if (partitioned) {
@@ -1101,6 +1118,26 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                 throw RuntimeError("evaluate_partitioned: allreduce of equivalent densities failed");
             prof.end(pm);
             prof.work("comm", 8.0 * nb * Kp, 0.0);
+        }
+        if (halo) {
+            // lattice levels need every box's density on every rank: each row is contributed by
+            // the rank of its first leaf (complete there: an owner's box, or a straddler after
+            // the straddler allreduce) and summed -- an allgather through the allreduce callback
+            for (int l = 1; l <= T.depth; l++) {
+                if (!Lay.lat[l]) continue;
+                const int64_t lo = T.level_off[l], hi = T.level_off[l + 1], cnt = (hi - lo) * Kp;
+                pm = prof.begin("comm");
+                double *buf = static_cast<double *>(part->alloc(part->user, cnt * sizeof(double)));
+                if (!buf) throw RuntimeError("evaluate_partitioned: allocation callback failed");
+                level_contrib_kernel<<<blocks_for(cnt, 256), 256, 0, st>>>(Pup, Part.rlo, part->rank, lo, hi, Kp, buf);
+                PK_CUDA(cudaStreamSynchronize(st));
+                if (part->allreduce(part->user, buf, cnt, st) != 0)
+                    throw RuntimeError("evaluate_partitioned: allreduce of a lattice level's densities failed");
+                PK_CUDA(cudaMemcpyAsync(Pup + lo * Kp, buf, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                ctx.launches += 1;
+                prof.end(pm);
+                prof.work("comm", 8.0 * cnt, 0.0);
+            }
         }
         // ---- downward pass (src/fmm.cpp:557-601) ----
         PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));

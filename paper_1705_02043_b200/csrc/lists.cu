@@ -419,18 +419,22 @@ struct EvalFillSink {
 struct NeedSink {
     unsigned long long *need;
     unsigned long long m;
+    bool skip_v;
     __device__ void u(int, int) {}
-    __device__ void v(int c, int) { atomicOr(need + c, m); }
+    __device__ void v(int c, int) {
+        if (!skip_v) atomicOr(need + c, m);
+    }
     __device__ void w(int c, int) { atomicOr(need + c, m); }
     __device__ void x(int, int) {}
 };
 
 __global__ void need_kernel(TreeView T, Params P, const int *__restrict__ rlo, const int *__restrict__ rhi,
-                            unsigned long long *need) {
+                            unsigned long long *need, unsigned skip_v_levels) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= T.nboxes) return;
     const int lo = rlo[b], hi = rhi[b];
-    NeedSink s{need, ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1ull)) >> lo) << lo};
+    NeedSink s{need, ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1ull)) >> lo) << lo,
+               ((skip_v_levels >> T.cell[b].w) & 1u) != 0};
     enumerate_box(T, P, b, s);
 }
 
@@ -509,10 +513,10 @@ void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cu
 }
 
 void need_masks(const DeviceTree &T, const ListSetup &S, const int *rlo, const int *rhi, unsigned long long *need,
-                cudaStream_t st) {
+                cudaStream_t st, unsigned skip_v_levels) {
     const int nb = (int)T.nboxes;
     PK_CUDA(cudaMemsetAsync(need, 0, nb * sizeof(unsigned long long), st));
-    need_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(T.view(), make_params(S, 1), rlo, rhi, need);
+    need_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(T.view(), make_params(S, 1), rlo, rhi, need, skip_v_levels);
     PK_CUDA(cudaGetLastError());
 }
 

@@ -451,7 +451,8 @@ __global__ void lat_check_kernel(const int *__restrict__ table, int64_t ld, cons
                                  const int *__restrict__ code_of_slot, const int4 *__restrict__ cell,
                                  const int *__restrict__ box_of, int n, int px, int py, int pz, int my, int mz,
                                  int64_t box0, int64_t nl, const int2 *__restrict__ srng,
-                                 const int2 *__restrict__ trng, int *__restrict__ seen, int *bad, int *dbg) {
+                                 const int2 *__restrict__ trng, const int *__restrict__ mask,
+                                 int *__restrict__ seen, int *bad, int *dbg) {
     const int64_t total = (int64_t)kNumM2L * ncols;
     int nbad = 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -482,7 +483,7 @@ __global__ void lat_check_kernel(const int *__restrict__ table, int64_t ld, cons
         // the evaluate lists omit sources without source points (zero densities on the lattice)
         // and give boxes without target points no list at all (their results are never read)
         const bool omitted = got < 0 && ((want >= 0 && srng && srng[want].y <= srng[want].x) ||
-                                         (trng && trng[tb].y <= trng[tb].x));
+                                         (trng && trng[tb].y <= trng[tb].x) || (mask && !mask[tb]));
         if (want != got && !omitted) {
             nbad++;
             if (dbg) {
@@ -1090,8 +1091,8 @@ int m2l_lattice_check(KifmmOps &ops, const LatticeLevelArgs &a, const int *table
     const int64_t total = (int64_t)kNumM2L * ncols;
     lat_check_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
         table, ld, out_box, ncols, d_code, a.cell, box_of, n, a.periodic[0], a.periodic[1], a.periodic[2], m[1], m[2],
-        a.box0, nl, a.srng, a.trng, seen, bad, dbg);
-    lat_seen_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(seen, nl, bad);
+        a.box0, nl, a.srng, a.trng, a.mask, seen, bad, dbg);
+    if (!a.mask) lat_seen_kernel<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(seen, nl, bad);
     PK_CUDA(cudaGetLastError());
     if (debug) {
         int h[33];

@@ -73,6 +73,7 @@ struct LatticeLevelArgs {
     const int4 *cell = nullptr;    // box cells (x, y, z, level)
     const int2 *srng = nullptr, *trng = nullptr; // boxes' source / target ranges (the check: the evaluate
                                                  // lists leave out source-less sources and target-less targets)
+    const int *mask = nullptr;     // the check, partitioned evaluates: boxes with mask[b] == 0 have empty lists
     const double *X = nullptr;     // phi_up [box][Kp]
     double *Y = nullptr;           // q [box][Kp]: Y += alpha * M2L
     double alpha = 1.0;
@@ -88,6 +89,8 @@ struct LatticeLevelArgs {
 int64_t m2l_lattice_bytes(const KifmmOps &ops, int level, const int periodic[3]);
 // counts into bad[0] the (slot, column) V-list entries of the dense layout that differ from
 // the lattice stencil (0: the lattice sum equals the V-list sum exactly)
+// (with a mask the level's boxes need not all be output columns: a rank's columns are the
+// boxes meeting its leaves)
 int m2l_lattice_check(KifmmOps &ops, const LatticeLevelArgs &a, const int *table, int64_t ld, const int *out_box,
                       int ncols, int *bad, Workspace &ws, cudaStream_t st);
 int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st);

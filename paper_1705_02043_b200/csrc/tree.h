@@ -87,8 +87,10 @@ struct DeviceLists {
 // Partitioned runs: need[b] = bit mask of the ranks that read box b's equivalent density
 // (V / W sources of target boxes meeting rank r's leaf range [rlo[c], rhi[c]]); all boxes
 // enumerated, nothing stored but the masks (ranks < 64).
+// (skip_v_levels: bit l set = level l's V sources are not needed -- its M2L runs on the lattice,
+// from the gathered level)
 void need_masks(const DeviceTree &T, const ListSetup &S, const int *rlo, const int *rhi, unsigned long long *need,
-                cudaStream_t st);
+                cudaStream_t st, unsigned skip_v_levels = 0);
 
 // Full CSR lists for all four types (export / tests).
 void build_lists_csr(const DeviceTree &T, const ListSetup &S, DeviceLists &L, cudaStream_t stream,

@@ -46,6 +46,7 @@ const Tuning &tuning() {
         r.leaf_tt = (int)env_int("PKGPU_LEAF_TT", r.leaf_tt, 1);
         r.m2l_lattice = env_int("PKGPU_M2L_LATTICE", 1, 0) != 0;
         if (const char *e = std::getenv("PKGPU_LATTICE_FILL")) r.lattice_fill = std::atof(e);
+        r.lattice_max_ranks = (int)env_int("PKGPU_LATTICE_RANKS", r.lattice_max_ranks, 0);
         r.lattice_budget = env_int("PKGPU_LATTICE_GB", r.lattice_budget >> 30, 0) << 30;
         return r;
     }();

@@ -38,6 +38,7 @@ struct Tuning {
     bool m2l_lattice = true;           // PKGPU_M2L_LATTICE = 0 | 1: filled levels by the lattice FFT M2L
     double lattice_fill = 0.5;         // PKGPU_LATTICE_FILL: least fraction of the level's lattice present
     int64_t lattice_budget = 48LL << 30; // PKGPU_LATTICE_GB: device bytes the lattice levels may use
+    int lattice_max_ranks = 4;         // PKGPU_LATTICE_RANKS: partitioned evaluates of more ranks keep the dense M2L
 };
 
 const Tuning &tuning();

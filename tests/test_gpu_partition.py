@@ -101,3 +101,25 @@ def test_partitioned_adaptive_separate_targets():
     single = pk.evaluate(req).potentials
     outs = run_ranks(req, 3)
     assert rel(outs[0], single) <= 1e-8
+
+
+@pytest.mark.parametrize("kernel,nranks", [("laplace", 2), ("stokeslet", 4)])
+def test_partitioned_lattice_levels(kernel, nranks):
+    """Uniform cloud to level 4: every level runs the lattice M2L, replicated on each rank from
+    the gathered level densities (up to 4 ranks; evaluate.cu), and the halo carries the W
+    sources only. Same potentials as the single-rank evaluate."""
+    k = pk.KernelSpec.laplace() if kernel == "laplace" else pk.KernelSpec.stokeslet()
+    pts, f = pk.generate("uniform", 30000, k.ks, seed=21)
+    per, opf = (pk.Periodicity.dp, "laplace_dp_ell2_p6_gated.pkm2l") if kernel == "laplace" else \
+        (pk.Periodicity.tp, "stokeslet_tp_ell2_p6_gated.pkm2l")
+    setup = pk.PeriodicSetup.make(per, 2)
+    op = pk.load_operator(os.path.join(GOLDEN, "ops", opf))
+    req = pk.EvalRequest(kernel=k, sources=pts, strengths=f, targets=pts, setup=setup, p=6, op=op, leaf_capacity=40)
+    single = pk.evaluate(req).potentials
+    moved = [0] * nranks
+    outs = run_ranks(req, nranks, moved=moved)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    err = rel(outs[0], single)
+    print(f"{kernel} uniform 30k R={nranks}: rel-L2 vs single rank {err:.3e}; doubles received per rank {moved}")
+    assert err <= (1e-12 if kernel == "laplace" else 1e-9)
