@@ -68,6 +68,75 @@ __device__ __forceinline__ double rinv_fast(double r2) {
     return __fma_rn(y * e, c, y);
 }
 
+// The same pair arithmetic for a tile of M = TT targets x NS sources, written step by step
+// across the M pairs: each pair is one dependent chain of ~20 FP64 operations, and issued one
+// pair after the other (as pair_laplace / pair_stokes in a loop compile under the register
+// cap) every operation waits out its predecessor's latency -- 34% of the leaf pass's warp
+// stalls were that wait (ncu source view, profiles/r02_lattice_step_ncu.txt). Interleaved,
+// the M chains fill each other's latency. Results are bit-identical to the pair functions
+// (same operations, same order of accumulation per target).
+template <int KERNEL, int TT, int NS>
+__device__ __forceinline__ void pair_tile(const double (&ux)[TT], const double (&uy)[TT], const double (&uz)[TT],
+                                          const double2 (&sxy)[NS], const double2 (&szd)[NS], const double2 (&sdd)[NS],
+                                          double (&acc)[TT][3]) {
+    constexpr int M = TT * NS;
+    double rx[M], ry[M], rz[M], r2[M], y[M], t[M], e[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+        rx[i] = ux[i % TT] - sxy[i / TT].x;
+        ry[i] = uy[i % TT] - sxy[i / TT].y;
+        rz[i] = uz[i % TT] - szd[i / TT].x;
+    }
+#pragma unroll
+    for (int i = 0; i < M; i++) r2[i] = ry[i] * ry[i];
+#pragma unroll
+    for (int i = 0; i < M; i++) r2[i] = __fma_rn(rx[i], rx[i], r2[i]);
+#pragma unroll
+    for (int i = 0; i < M; i++) r2[i] = __fma_rn(rz[i], rz[i], r2[i]);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[i]) : "d"(r2[i]));
+        y[i] = __hiloint2double(__double2hiint(r2[i]) < 0x00100000 ? 0 : __double2hiint(y[i]), 0);
+    }
+#pragma unroll
+    for (int i = 0; i < M; i++) t[i] = -r2[i] * y[i];
+#pragma unroll
+    for (int i = 0; i < M; i++) e[i] = __fma_rn(t[i], y[i], 1.0);
+#pragma unroll
+    for (int i = 0; i < M; i++) t[i] = y[i] * e[i];
+#pragma unroll
+    for (int i = 0; i < M; i++) e[i] = __fma_rn(0.375, e[i], 0.5);
+#pragma unroll
+    for (int i = 0; i < M; i++) y[i] = __fma_rn(t[i], e[i], y[i]);
+    if (KERNEL == 0) {
+#pragma unroll
+        for (int i = 0; i < M; i++) acc[i % TT][0] = __fma_rn(szd[i / TT].y, y[i], acc[i % TT][0]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; i++) t[i] = ry[i] * sdd[i / TT].x;
+#pragma unroll
+        for (int i = 0; i < M; i++) t[i] = __fma_rn(rx[i], szd[i / TT].y, t[i]);
+#pragma unroll
+        for (int i = 0; i < M; i++) t[i] = __fma_rn(rz[i], sdd[i / TT].y, t[i]);
+#pragma unroll
+        for (int i = 0; i < M; i++) t[i] = t[i] * y[i];
+#pragma unroll
+        for (int i = 0; i < M; i++) t[i] = t[i] * y[i];
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+            rx[i] = __fma_rn(rx[i], t[i], szd[i / TT].y);
+            ry[i] = __fma_rn(ry[i], t[i], sdd[i / TT].x);
+            rz[i] = __fma_rn(rz[i], t[i], sdd[i / TT].y);
+        }
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+            acc[i % TT][0] = __fma_rn(rx[i], y[i], acc[i % TT][0]);
+            acc[i % TT][1] = __fma_rn(ry[i], y[i], acc[i % TT][1]);
+            acc[i % TT][2] = __fma_rn(rz[i], y[i], acc[i % TT][2]);
+        }
+    }
+}
+
 // Laplace pair: acc += rho / r
 __device__ __forceinline__ void pair_laplace(double tx, double ty, double tz, double sx, double sy, double sz,
                                              double rho, double &acc) {

@@ -14,6 +14,12 @@ namespace pkgpu {
 namespace {
 
 constexpr int NT = 128;
+#ifndef LEAF_NS
+#define LEAF_NS 2
+#endif
+#ifndef LEAF_MINB
+#define LEAF_MINB 5
+#endif
 constexpr int SB = 512;
 constexpr int MAXSEG = 64;
 constexpr int MAXU = 128;
@@ -38,25 +44,36 @@ template <int KERNEL> struct Stage {
 template <int KERNEL>
 __device__ __forceinline__ void accumulate(const Stage<KERNEL> &S, double tx, double ty, double tz, int j, int G,
                                            double (&acc)[3], int *coincident) {
+    constexpr int NS = 4; // sources per step: four interleaved pair chains (kernels.cuh, pair_tile)
+    double a1[1][3] = {{acc[0], acc[1], acc[2]}};
     for (int s = 0; s < S.nseg; s++) {
-        const double ux = tx - S.sx[s], uy = ty - S.sy[s], uz = tz - S.sz[s];
+        const double ux[1] = {tx - S.sx[s]}, uy[1] = {ty - S.sy[s]}, uz[1] = {tz - S.sz[s]};
         const int end = S.begin[s + 1];
-        int ncoin = 0;
-        for (int q = S.begin[s] + j; q < end; q += G) {
-            const double2 a = S.xy[q], b = S.zd[q];
-            if (KERNEL == 0) {
-                pair_laplace(ux, uy, uz, a.x, a.y, b.x, b.y, acc[0]);
-            } else {
-                const double2 c = S.dd[q];
-                pair_stokes(ux, uy, uz, a.x, a.y, b.x, b.y, c.x, c.y, acc[0], acc[1], acc[2]);
+        int q = S.begin[s] + j;
+        for (; q + (NS - 1) * G < end; q += NS * G) {
+            double2 a[NS], b[NS], c[NS];
+#pragma unroll
+            for (int u = 0; u < NS; u++) {
+                a[u] = S.xy[q + u * G], b[u] = S.zd[q + u * G];
+                c[u] = KERNEL != 0 ? S.dd[q + u * G] : make_double2(0.0, 0.0);
             }
-            if (S.cnt[s]) {
-                const double rx = ux - a.x, ry = uy - a.y, rz = uz - b.x;
+            pair_tile<KERNEL, 1, NS>(ux, uy, uz, a, b, c, a1);
+        }
+        for (; q < end; q += G) {
+            const double2 a[1] = {S.xy[q]}, b[1] = {S.zd[q]};
+            const double2 c[1] = {KERNEL != 0 ? S.dd[q] : make_double2(0.0, 0.0)};
+            pair_tile<KERNEL, 1, 1>(ux, uy, uz, a, b, c, a1);
+        }
+        if (S.cnt[s]) { // count coincidences in this segment (direct mode; src/kernel.cpp:97-98)
+            int ncoin = 0;
+            for (int p = S.begin[s] + j; p < end; p += G) {
+                const double rx = ux[0] - S.xy[p].x, ry = uy[0] - S.xy[p].y, rz = uz[0] - S.zd[p].x;
                 ncoin += (rx * rx + ry * ry + rz * rz) == 0.0;
             }
+            if (ncoin) atomicAdd(coincident, ncoin);
         }
-        if (ncoin) atomicAdd(coincident, ncoin);
     }
+    acc[0] = a1[0][0], acc[1] = a1[0][1], acc[2] = a1[0][2];
 }
 
 // one-segment surface stage: points fma(half, t_i, c), density phi[i*ks + a]
@@ -135,18 +152,22 @@ __device__ __forceinline__ void accumulate_tt(const Stage<KERNEL> &S, const doub
 #pragma unroll
         for (int k = 0; k < TT; k++) ux[k] = tx[k] - S.sx[s], uy[k] = ty[k] - S.sy[s], uz[k] = tz[k] - S.sz[s];
         const int end = S.begin[s + 1];
-#pragma unroll 2
-        for (int q = S.begin[s] + j; q < end; q += G) {
-            const double2 a = S.xy[q], b = S.zd[q];
-            double2 c = make_double2(0.0, 0.0);
-            if (KERNEL != 0) c = S.dd[q];
+        int q = S.begin[s] + j;
+        // LEAF_NS sources per step: LEAF_NS x TT interleaved pair chains (kernels.cuh, pair_tile)
+        for (; q + (LEAF_NS - 1) * G < end; q += LEAF_NS * G) {
+            double2 a[LEAF_NS], b[LEAF_NS], c[LEAF_NS];
 #pragma unroll
-            for (int k = 0; k < TT; k++) {
-                if (KERNEL == 0)
-                    pair_laplace(ux[k], uy[k], uz[k], a.x, a.y, b.x, b.y, acc[k][0]);
-                else
-                    pair_stokes(ux[k], uy[k], uz[k], a.x, a.y, b.x, b.y, c.x, c.y, acc[k][0], acc[k][1], acc[k][2]);
+            for (int u = 0; u < LEAF_NS; u++) {
+                a[u] = S.xy[q + u * G], b[u] = S.zd[q + u * G];
+                c[u] = KERNEL != 0 ? S.dd[q + u * G] : make_double2(0.0, 0.0);
             }
+            pair_tile<KERNEL, TT, LEAF_NS>(ux, uy, uz, a, b, c, acc);
+        }
+        for (; q < end; q += G) {
+            const double2 a[1] = {S.xy[q]}, b[1] = {S.zd[q]};
+            double2 c[1] = {make_double2(0.0, 0.0)};
+            if (KERNEL != 0) c[0] = S.dd[q];
+            pair_tile<KERNEL, TT, 1>(ux, uy, uz, a, b, c, acc);
         }
     }
 }
@@ -155,7 +176,7 @@ __device__ __forceinline__ void accumulate_tt(const Stage<KERNEL> &S, const doub
 // group (any G, so no lane idles for want of a power of two); sources staged in shared
 // memory per batch of segments; the G partial sums of a group are reduced in a fixed order
 // through shared memory (deterministic, each target written once).
-template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, 5) leaf_kernel(LeafParams P) {
+template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) leaf_kernel(LeafParams P) {
     constexpr int KS = Stage<KERNEL>::KS;
     __shared__ union {
         Stage<KERNEL> S;
