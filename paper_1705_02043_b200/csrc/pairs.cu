@@ -21,8 +21,8 @@ constexpr int NT = 128;
 #define LEAF_MINB 5
 #endif
 constexpr int SB = 512;
-constexpr int MAXSEG = 64;
-constexpr int MAXU = 128;
+constexpr int MAXU = 128;     // U entries per batch: one per thread of the leaf pass (NT)
+constexpr int MAXSEG = MAXU;  // segments per stage: every entry of a batch may fall in one stage
 
 template <int KERNEL> struct Stage {
     static constexpr int KS = KERNEL == 0 ? 1 : 3;
@@ -183,9 +183,9 @@ template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) l
         double red[NT][TT][KS];
     } sm;
     Stage<KERNEL> &S = sm.S;
-    __shared__ int s_uc[MAXU], s_ucode[MAXU], s_ub[MAXU], s_ue[MAXU];
-    __shared__ int s_segsrc[MAXSEG];
-    __shared__ int s_pos, s_off;
+    __shared__ int s_ucode[MAXU], s_ub[MAXU];
+    __shared__ int s_pre[MAXU + 1]; // exclusive prefix of the batch's entry sizes (flat source index)
+    __shared__ int s_wtot[NT / 32];
     const int b = P.leaves[blockIdx.x];
     const int2 tr = P.T.trng[b];
     const int ntg = tr.y - tr.x;
@@ -236,54 +236,67 @@ template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) l
                 if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
             }
         }
-        // U: adjacent source leaves, packed into batches of segments
+        // U: adjacent source leaves. A batch of up to MAXU entries is one flat run of sources
+        // (prefix sums of the entry sizes, a block scan); stages are SB-source windows of that
+        // run. Every thread finds its sources' entries by binary search in the prefix, so the
+        // segment table and all loads of a stage are issued in parallel (no serial
+        // segmentation, no load chained per segment).
         const int64_t ub = P.u_off[b], ue = P.u_off[b + 1];
         for (int64_t e0 = ub; e0 < ue; e0 += MAXU) {
             const int ne = (int)(int64_t)::min((int64_t)MAXU, ue - e0);
-            __syncthreads();
-            for (int k = tid; k < ne; k += NT) {
-                const int2 en = P.u_ent[e0 + k];
+            __syncthreads(); // the previous stage's sums are done with S and the tables
+            int len = 0;
+            if (tid < ne) {
+                const int2 en = P.u_ent[e0 + tid];
                 const int2 r = P.T.srng[en.x];
-                s_uc[k] = en.x, s_ucode[k] = en.y, s_ub[k] = r.x, s_ue[k] = r.y;
+                s_ucode[tid] = en.y, s_ub[tid] = r.x;
+                len = r.y - r.x;
             }
-            __syncthreads();
-            if (tid == 0) {
-                s_pos = 0;
-                s_off = ne > 0 ? s_ub[0] : 0;
+            int inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((tid & 31) >= o) inc += v;
             }
+            if ((tid & 31) == 31) s_wtot[tid >> 5] = inc;
             __syncthreads();
-            while (s_pos < ne) {
-                if (tid == 0) {
-                    int pos = s_pos, off = s_off, fill = 0, nseg = 0;
-                    while (pos < ne && nseg < MAXSEG && fill < SB) {
-                        const int take = min(SB - fill, s_ue[pos] - off);
-                        S.begin[nseg] = fill;
-                        double a, bb, c;
-                        shift_of(s_ucode[pos], a, bb, c);
-                        S.sx[nseg] = a, S.sy[nseg] = bb, S.sz[nseg] = c;
-                        S.cnt[nseg] = 0;
-                        s_segsrc[nseg] = off;
-                        fill += take;
-                        off += take;
-                        nseg++;
-                        if (off >= s_ue[pos]) {
-                            pos++;
-                            if (pos < ne) off = s_ub[pos];
-                        }
-                    }
-                    S.begin[nseg] = fill;
-                    S.nseg = nseg;
-                    s_pos = pos;
-                    s_off = off;
+            int woff = 0;
+            for (int w = 0; w < (tid >> 5); w++) woff += s_wtot[w];
+            s_pre[tid] = woff + inc - len;
+            if (tid == NT - 1) s_pre[NT] = woff + inc;
+            __syncthreads();
+            const int total = s_pre[ne == NT ? NT : ne]; // entries past ne have length 0: s_pre[ne] is the total
+            // largest k in [lo, hi] with s_pre[k] <= p
+            auto entry_of = [&](int p, int lo, int hi) {
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pre[mid] <= p) lo = mid;
+                    else hi = mid - 1;
                 }
-                __syncthreads();
-                for (int sg = 0; sg < S.nseg; sg++) {
-                    const int beg = S.begin[sg], len = S.begin[sg + 1] - beg, src0 = s_segsrc[sg];
-                    for (int q = tid; q < len; q += NT) stage_point<KERNEL>(S, beg + q, P.src_pos, P.src_f, src0 + q);
+                return lo;
+            };
+            for (int t0 = 0; t0 < total; t0 += SB) {
+                const int t1 = min(total, t0 + SB);
+                const int k0 = entry_of(t0, 0, ne - 1), k1 = entry_of(t1 - 1, k0, ne - 1);
+                const int nseg = k1 - k0 + 1;
+                if (t0 > 0) __syncthreads(); // the previous stage's sums are done with S
+                for (int i = tid; i <= nseg; i += NT) {
+                    S.begin[i] = i < nseg ? max(s_pre[k0 + i], t0) - t0 : t1 - t0;
+                    if (i < nseg) {
+                        double a, bb, c;
+                        shift_of(s_ucode[k0 + i], a, bb, c);
+                        S.sx[i] = a, S.sy[i] = bb, S.sz[i] = c;
+                        S.cnt[i] = 0;
+                    }
+                }
+                if (tid == 0) S.nseg = nseg;
+#pragma unroll 4
+                for (int p = t0 + tid; p < t1; p += NT) {
+                    const int k = entry_of(p, k0, k1);
+                    stage_point<KERNEL>(S, p - t0, P.src_pos, P.src_f, s_ub[k] + (p - s_pre[k]));
                 }
                 __syncthreads();
                 if (active) accumulate_tt<KERNEL, TT>(S, tx, ty, tz, j, G, acc);
-                __syncthreads();
             }
         }
         // far field: root outer surface with the periodizing density (image layers
