@@ -185,7 +185,10 @@ template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) l
     Stage<KERNEL> &S = sm.S;
     __shared__ int s_ucode[MAXU], s_ub[MAXU];
     __shared__ int s_pre[MAXU + 1]; // exclusive prefix of the batch's entry sizes (flat source index)
-    __shared__ int s_wtot[NT / 32];
+    __shared__ int s_wtot[NT / 32], s_whead[NT / 32];
+    // runs of consecutive entries with the same image shift are one segment of the pair loops
+    // (an interior leaf's 27 neighbours: one run, no per-leaf tail of idle lanes)
+    __shared__ int s_run[MAXU], s_runstart[MAXU], s_runcode[MAXU];
     const int b = P.leaves[blockIdx.x];
     const int2 tr = P.T.trng[b];
     const int ntg = tr.y - tr.x;
@@ -264,6 +267,16 @@ template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) l
             for (int w = 0; w < (tid >> 5); w++) woff += s_wtot[w];
             s_pre[tid] = woff + inc - len;
             if (tid == NT - 1) s_pre[NT] = woff + inc;
+            const bool head = tid < ne && (tid == 0 || s_ucode[tid] != s_ucode[tid - 1]);
+            const unsigned hb = __ballot_sync(0xffffffffu, head);
+            if ((tid & 31) == 0) s_whead[tid >> 5] = __popc(hb);
+            __syncthreads();
+            if (tid < ne) {
+                int rid = __popc(hb & (0xffffffffu >> (31 - (tid & 31)))) - 1;
+                for (int w = 0; w < (tid >> 5); w++) rid += s_whead[w];
+                s_run[tid] = rid;
+                if (head) s_runstart[rid] = s_pre[tid], s_runcode[rid] = s_ucode[tid];
+            }
             __syncthreads();
             const int total = s_pre[ne == NT ? NT : ne]; // entries past ne have length 0: s_pre[ne] is the total
             // largest k in [lo, hi] with s_pre[k] <= p
@@ -278,13 +291,13 @@ template <int KERNEL, int TT> __global__ void __launch_bounds__(NT, LEAF_MINB) l
             for (int t0 = 0; t0 < total; t0 += SB) {
                 const int t1 = min(total, t0 + SB);
                 const int k0 = entry_of(t0, 0, ne - 1), k1 = entry_of(t1 - 1, k0, ne - 1);
-                const int nseg = k1 - k0 + 1;
+                const int r0 = s_run[k0], nseg = s_run[k1] - r0 + 1;
                 if (t0 > 0) __syncthreads(); // the previous stage's sums are done with S
                 for (int i = tid; i <= nseg; i += NT) {
-                    S.begin[i] = i < nseg ? max(s_pre[k0 + i], t0) - t0 : t1 - t0;
+                    S.begin[i] = i < nseg ? max(s_runstart[r0 + i], t0) - t0 : t1 - t0;
                     if (i < nseg) {
                         double a, bb, c;
-                        shift_of(s_ucode[k0 + i], a, bb, c);
+                        shift_of(s_runcode[r0 + i], a, bb, c);
                         S.sx[i] = a, S.sy[i] = bb, S.sz[i] = c;
                         S.cnt[i] = 0;
                     }
