@@ -619,8 +619,9 @@ int gather_gemm(const GemmArgs &a, Workspace &ws, cudaStream_t st, int num_sms) 
     // one to a few waves of tiles that the uniform split would cut: the hybrid schedule, when
     // its tail chunks are still at least gemm_min_iters long
     bool hybrid = false;
-    if (tu.gemm_hybrid && nsplit > 1 && base >= resident && base < 8 * (int64_t)resident && base % resident != 0 &&
-        (base % resident) * iters / resident >= tu.gemm_min_iters) {
+    const bool sub_wave = base < resident && a.nslots == 1 && base * iters / resident >= 2 * tu.gemm_min_iters_small;
+    if (tu.gemm_hybrid && nsplit > 1 && (base >= resident || sub_wave) && base < 8 * (int64_t)resident &&
+        base % resident != 0 && (sub_wave || (base % resident) * iters / resident >= tu.gemm_min_iters)) {
         const HybridPlan P = plan_hybrid(ws, rowtiles, coltiles, bnt, resident, (int)iters, st);
         kp.pieces = P.pieces, kp.chunks = P.chunks, kp.tile_parts = P.tile_parts;
         kp.nit_nom = (int)iters;
