@@ -217,6 +217,21 @@ TreeView DeviceTree::view() const {
     return v;
 }
 
+// the root box (level 0: every point, no parent, no children yet)
+__global__ void root_init_kernel(unsigned long long *prefix, int4 *cell, int *parent, int *child, int *isleaf,
+                                 int2 *srng, int2 *trng, int ns, int nt) {
+    const int t = threadIdx.x;
+    if (t < 8) child[t] = -1;
+    if (t == 0) {
+        prefix[0] = 0ull;
+        cell[0] = make_int4(0, 0, 0, 0);
+        parent[0] = -1;
+        isleaf[0] = 1;
+        srng[0] = make_int2(0, ns);
+        trng[0] = make_int2(0, nt);
+    }
+}
+
 void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_trg, int64_t nt, int leaf_capacity,
                 cudaStream_t st, int64_t *launches) {
     if (leaf_capacity < 1) throw InvalidArgument("FmmTree: leaf capacity must be positive");
@@ -258,10 +273,8 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
                                                 pass == 0 ? T.src_perm : T.trg_perm, (int)n, 0, 36, st));
         *launches += 1 + 4;
     }
-    PK_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PK_CUDA(cudaStreamSynchronize(st));
-    if (same) h_flags[0] *= 2; // the reference counts the targets' offenders as well
-    if (h_flags[0] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[0]);
+    // (the outside-domain count is read back with the root level's counts below: one host
+    // round trip fewer; nothing is allocated from the keys before that)
 
     // level-synchronous construction
     size_t cap = 1024, used = 0;
@@ -275,20 +288,8 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         T.trng = grow<int2>(ws, "trng", need, used, st);
     };
     arrays(cap);
-    {
-        const unsigned long long z = 0;
-        const int4 c0 = make_int4(0, 0, 0, 0);
-        const int m1 = -1, one = 1;
-        const int2 sr = make_int2(0, (int)ns), tr = make_int2(0, (int)nt);
-        PK_CUDA(cudaMemcpyAsync(T.prefix, &z, sizeof z, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemcpyAsync(T.cell, &c0, sizeof c0, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemcpyAsync(T.parent, &m1, sizeof m1, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemcpyAsync(T.isleaf, &one, sizeof one, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemcpyAsync(T.srng, &sr, sizeof sr, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemcpyAsync(T.trng, &tr, sizeof tr, cudaMemcpyHostToDevice, st));
-        PK_CUDA(cudaMemsetAsync(T.child, 0xff, 8 * sizeof(int), st));
-        PK_CUDA(cudaStreamSynchronize(st)); // host sources above are stack values
-    }
+    root_init_kernel<<<1, 32, 0, st>>>(T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng, T.trng, (int)ns, (int)nt);
+    *launches += 1;
     T.level_off.assign(1, 0);
     int64_t nl = 1, base = 0;
     used = 1;
@@ -307,8 +308,13 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         PK_CUDA(cub::DeviceScan::ExclusiveSum(stemp, sb, childcnt, childoff, (int)nl + 1, st));
         PK_CUDA(cudaMemcpyAsync(h_flags, childoff + nl, sizeof(int), cudaMemcpyDeviceToHost, st));
         PK_CUDA(cudaMemcpyAsync(h_flags + 1, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (level == 0) PK_CUDA(cudaMemcpyAsync(h_flags + 2, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
         PK_CUDA(cudaStreamSynchronize(st));
         *launches += 2;
+        if (level == 0) {
+            if (same) h_flags[2] *= 2; // the reference counts the targets' offenders as well
+            if (h_flags[2] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[2]);
+        }
         if (h_flags[1])
             throw RuntimeError("FmmTree: leaf over capacity at maximum depth " + std::to_string(kMaxDepth) +
                                " (duplicate point pathology)");
