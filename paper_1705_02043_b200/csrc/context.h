@@ -37,6 +37,7 @@ struct pkgpu_context {
     cudaStream_t stream = nullptr;
     cudaStream_t aux_stream = nullptr;          // list building beside the upward pass (evaluate.cu)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    pkgpu::Workspace ws_aux;                    // buffers of the lattice M2L run on aux_stream
     int64_t launches = 0;
     std::mutex mtx; // calls on one context are serialised (the reference evaluate is reentrant per call)
     pkgpu::OperatorCache ops;

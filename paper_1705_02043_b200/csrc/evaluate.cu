@@ -1228,10 +1228,37 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             for (int j = l; j <= l1; j++) i8_apps[j] = 1;
             l = l1 + 1;
         }
+        // The deepest lattice level's M2L (the bulk of the M2L) depends only on phi_up and adds to
+        // rows of q that nothing else touches before the L2L into that level: it runs on the
+        // auxiliary stream (own workspace) beside the downward chain of the coarser levels,
+        // whose small launches leave most of the GPU idle; joined at that level.
+        int lat_async = -1;
+        if (overlap_lists && tuning().overlap_m2l) {
+            for (int l = 2; l <= T.depth; l++)
+                if (Lay.lat[l]) lat_async = l;
+            if (lat_async >= 2) {
+                PK_CUDA(cudaEventRecord(ctx.ev_fork, st)); // q zeroed, X pass done
+                PK_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.ev_fork, 0));
+                LatticeLevelArgs la;
+                la.level = lat_async;
+                for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
+                la.box0 = T.level_off[lat_async];
+                la.box1 = T.level_off[lat_async + 1];
+                la.cell = T.cell;
+                la.X = Pup;
+                la.Y = Q;
+                la.alpha = std::ldexp(1.0, lat_async); // q += 2^l M_d phi_src (src/fmm.cpp:573)
+                ctx.launches += m2l_lattice_level(ops, la, ctx.ws_aux, ctx.aux_stream);
+                PK_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux_stream));
+            }
+        }
         for (int l = 0; l <= T.depth; l++) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (l >= 1 && Lay.lat[l]) {
+            if (l >= 1 && l == lat_async) {
+                PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join, 0)); // computed on the auxiliary stream
+                lat_apps[l] = 1;
+            } else if (l >= 1 && Lay.lat[l]) {
                 // M2L as a convolution on the level's lattice (m2l_fft.h)
                 pm = prof.begin("m2l");
                 LatticeLevelArgs la;
