@@ -835,13 +835,28 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
     // inputs on the device
     const double *d_src = req.sources, *d_str = req.strengths, *d_trg = req.targets;
     double *d_out = out;
+    bool str_pending = false; // strengths still in flight on the auxiliary stream
+    auto need_strengths = [&]() {
+        if (str_pending) PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join, 0));
+        str_pending = false;
+    };
     if (!req.device_pointers) {
         // targets passed as the sources' own buffer (the usual self-evaluation) go over once
         const bool same = req.targets == req.sources && nt == ns;
         double *s = ws.get<double>("in_src", 3 * ns + 1), *q = ws.get<double>("in_str", ks * ns + 1),
                *t = same ? s : ws.get<double>("in_trg", 3 * nt + 1);
         if (ns) PK_CUDA(cudaMemcpyAsync(s, req.sources, 3 * ns * sizeof(double), cudaMemcpyHostToDevice, st));
-        if (ns) PK_CUDA(cudaMemcpyAsync(q, req.strengths, ks * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        // the tree needs only the positions: the strengths go over on the auxiliary stream, beside
+        // the tree build (awaited before their first use)
+        if (ns && ctx.aux_stream && !partitioned) {
+            PK_CUDA(cudaEventRecord(ctx.ev_fork, st)); // the staging buffer's previous readers are done
+            PK_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.ev_fork, 0));
+            PK_CUDA(cudaMemcpyAsync(q, req.strengths, ks * ns * sizeof(double), cudaMemcpyHostToDevice, ctx.aux_stream));
+            PK_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux_stream));
+            str_pending = true;
+        } else if (ns) {
+            PK_CUDA(cudaMemcpyAsync(q, req.strengths, ks * ns * sizeof(double), cudaMemcpyHostToDevice, st));
+        }
         if (nt && !same) PK_CUDA(cudaMemcpyAsync(t, req.targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, st));
         d_src = s, d_str = q, d_trg = t;
         d_out = ws.get<double>("out", kt * nt + 1);
@@ -851,6 +866,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
     if (periodic && !(kernel == PKGPU_STOKESLET && req.setup.periodicity == PKGPU_TP) && ns > 0) {
         const int nblk = 256;
         double *part = ws.get<double>("compat_part", 4 * nblk);
+        need_strengths();
         compat_partial_kernel<<<nblk, 256, 0, st>>>(d_str, ns, ks, part);
         std::vector<double> h(4 * nblk);
         PK_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -880,6 +896,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
 
     if (req.mode == PKGPU_MODE_DIRECT) {
         // src/fmm.cpp:711-721: all image offsets with max-norm <= ell, skip coincident at 0
+        need_strengths();
         PK_CUDA(cudaEventRecord(ctx.ev[0], st));
         std::vector<std::array<int, 3>> offs =
             periodic ? image_offsets(axes, 0, ell) : std::vector<std::array<int, 3>>{{0, 0, 0}};
@@ -931,6 +948,7 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         int pm = prof.begin("tree");
         DeviceTree &T = ctx.tree;
         build_tree(T, d_src, ns, d_trg, nt, req.leaf_capacity, st, &ctx.launches);
+        need_strengths();
         gather_strengths(T, d_str, ks, st, &ctx.launches);
         prof.end(pm);
         PK_CUDA(cudaEventRecord(ctx.ev[1], st));
