@@ -275,12 +275,21 @@ pkgpu_status pkgpu_context_create(int device, pkgpu_context **ctx, char *err, si
         auto c = std::make_unique<pkgpu_context>();
         c->device = device;
         PK_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-        PK_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        // the work stream and the list stream run at the highest priority, the stream of the
+        // overlapped lattice M2L at the lowest: its big grids fill the SMs the latency-bound
+        // chain leaves idle and yield to the chain's CTAs as soon as those are launched
+        int prio_least = 0, prio_greatest = 0;
+        PK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+        PK_CUDA(cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, prio_greatest));
         c->stream = c->own_stream;
         for (auto &e : c->ev) PK_CUDA(cudaEventCreate(&e));
-        PK_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        PK_CUDA(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, prio_greatest));
+        PK_CUDA(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
         PK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PK_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        PK_CUDA(cudaStreamCreateWithPriority(&c->aux2_stream, cudaStreamNonBlocking, prio_least));
+        PK_CUDA(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
+        PK_CUDA(cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming));
         *ctx = c.release();
     });
 }
@@ -294,6 +303,10 @@ void pkgpu_context_destroy(pkgpu_context *ctx) {
     if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
+    if (ctx->aux2_stream) cudaStreamDestroy(ctx->aux2_stream);
+    if (ctx->ev_fork2) cudaEventDestroy(ctx->ev_fork2);
+    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     delete ctx;
 }

@@ -37,7 +37,10 @@ struct pkgpu_context {
     cudaStream_t stream = nullptr;
     cudaStream_t aux_stream = nullptr;          // list building beside the upward pass (evaluate.cu)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    pkgpu::Workspace ws_aux;                    // buffers of the lattice M2L run on aux_stream
+    cudaStream_t aux2_stream = nullptr;         // the deepest lattice level's M2L, from its pinv_up on (evaluate.cu)
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    cudaEvent_t ev_user = nullptr;              // hand-over between a caller's stream and own_stream (evaluate.cu)
+    pkgpu::Workspace ws_aux;                    // buffers of the lattice M2L run on aux2_stream
     int64_t launches = 0;
     std::mutex mtx; // calls on one context are serialised (the reference evaluate is reentrant per call)
     pkgpu::OperatorCache ops;

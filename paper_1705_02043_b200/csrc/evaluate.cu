@@ -810,6 +810,24 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
               pkgpu_compat *compat, const pkgpu_partition *part) {
     cudaStream_t st = ctx.stream;
     const bool partitioned = part && part->nranks > 1;
+    // A caller's stream (pkgpu_context_set_stream) keeps its ordering but not the work: the
+    // evaluate runs on the context's own high-priority stream between two events on the
+    // caller's stream, so that the overlapped low-priority lattice M2L yields to the
+    // latency-bound chain (a caller's stream usually has the lowest priority itself).
+    // Partitioned evaluates hand `st` to the caller's collectives and stay on it.
+    struct HandBack {
+        pkgpu_context &c;
+        cudaStream_t user, work;
+        ~HandBack() {
+            if (user == work) return;
+            if (cudaEventRecord(c.ev_user, work) == cudaSuccess) cudaStreamWaitEvent(user, c.ev_user, 0);
+        }
+    } hand_back{ctx, st, st};
+    if (!partitioned && st != ctx.own_stream && ctx.own_stream && ctx.ev_user && tuning().overlap_m2l) {
+        PK_CUDA(cudaEventRecord(ctx.ev_user, st));
+        PK_CUDA(cudaStreamWaitEvent(ctx.own_stream, ctx.ev_user, 0));
+        st = hand_back.work = ctx.own_stream;
+    }
     if (partitioned) {
         if (part->rank < 0 || part->rank >= part->nranks || !part->alloc || !part->allreduce)
             throw InvalidArgument("evaluate_partitioned: bad partition descriptor");
@@ -1060,6 +1078,32 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
                                            : ws.get<double>("phi_up", nb * Kp);
         if (!Pup) throw RuntimeError("evaluate_partitioned: allocation callback failed");
         if (partitioned) PK_CUDA(cudaMemsetAsync(Pup, 0, nb * Kp * sizeof(double), st));
+        // The deepest lattice level's M2L (the bulk of the M2L) depends only on that level's
+        // phi_up: it runs on a second auxiliary stream (own workspace) from the moment its
+        // pinv_up is queued, beside the M2M / pinv chain of the coarser levels, the lists and the
+        // coarse levels' downward chain, whose small launches leave most of the GPU idle. The
+        // result stays in the workspace; the scatter into q runs on the work stream where the
+        // downward pass reaches the level (after the X pass: q has one writer at a time). The
+        // lattice check of the lists stage still decides: a level it rejects drops the result.
+        auto lat_args = [&](int l, bool defer) {
+            LatticeLevelArgs la;
+            la.level = l;
+            for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
+            la.box0 = T.level_off[l];
+            la.box1 = T.level_off[l + 1];
+            la.cell = T.cell;
+            la.X = Pup;
+            la.Y = Q;
+            la.alpha = std::ldexp(1.0, l); // q += 2^l M_d phi_src (src/fmm.cpp:573)
+            la.defer_scatter = defer;
+            return la;
+        };
+        int lat_async = -1;
+        if (overlap_lists && tuning().overlap_m2l && ctx.aux2_stream) {
+            for (int l = 2; l <= T.depth; l++)
+                if (Lay.lat[l]) lat_async = l;
+            if (lat_async >= 2) ctx.launches += m2l_fft_prepare(ops, ws, st); // kernel spectra (first use)
+        }
         // ---- upward pass (src/fmm.cpp:532-553) ----
         PK_CUDA(cudaMemsetAsync(Q, 0, nb * Kp * sizeof(double), st));
         pm = prof.begin("s2m");
@@ -1110,6 +1154,14 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             pm = prof.begin("pinv_up");
             pinv_level(ctx, ops, true, lo, hi, l, Q, Tm - lo * Kp, Pup, st, PP, Lay);
             prof.end(pm);
+            if (l == lat_async) {
+                // phi_up of the deepest lattice level is final: its M2L starts here, beside the
+                // rest of the upward pass, the lists and the coarse levels' downward chain
+                PK_CUDA(cudaEventRecord(ctx.ev_fork2, st));
+                PK_CUDA(cudaStreamWaitEvent(ctx.aux2_stream, ctx.ev_fork2, 0));
+                ctx.launches += m2l_lattice_level(ops, lat_args(l, true), ctx.ws_aux, ctx.aux2_stream);
+                PK_CUDA(cudaEventRecord(ctx.ev_join2, ctx.aux2_stream));
+            }
         }
         if (overlap_lists) {
             // the upward pass is queued; build the lists beside it and join
@@ -1246,35 +1298,15 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             for (int j = l; j <= l1; j++) i8_apps[j] = 1;
             l = l1 + 1;
         }
-        // The deepest lattice level's M2L (the bulk of the M2L) depends only on phi_up and adds to
-        // rows of q that nothing else touches before the L2L into that level: it runs on the
-        // auxiliary stream (own workspace) beside the downward chain of the coarser levels,
-        // whose small launches leave most of the GPU idle; joined at that level.
-        int lat_async = -1;
-        if (overlap_lists && tuning().overlap_m2l) {
-            for (int l = 2; l <= T.depth; l++)
-                if (Lay.lat[l]) lat_async = l;
-            if (lat_async >= 2) {
-                PK_CUDA(cudaEventRecord(ctx.ev_fork, st)); // q zeroed, X pass done
-                PK_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.ev_fork, 0));
-                LatticeLevelArgs la;
-                la.level = lat_async;
-                for (int a = 0; a < 3; a++) la.periodic[a] = ls.periodic[a];
-                la.box0 = T.level_off[lat_async];
-                la.box1 = T.level_off[lat_async + 1];
-                la.cell = T.cell;
-                la.X = Pup;
-                la.Y = Q;
-                la.alpha = std::ldexp(1.0, lat_async); // q += 2^l M_d phi_src (src/fmm.cpp:573)
-                ctx.launches += m2l_lattice_level(ops, la, ctx.ws_aux, ctx.aux_stream);
-                PK_CUDA(cudaEventRecord(ctx.ev_join, ctx.aux_stream));
-            }
-        }
         for (int l = 0; l <= T.depth; l++) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (l >= 1 && l == lat_async) {
-                PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join, 0)); // computed on the auxiliary stream
+            if (l >= 1 && l == lat_async) PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join2, 0)); // also when dropped
+            if (l >= 1 && l == lat_async && Lay.lat[l]) {
+                // computed on the second auxiliary stream: add it into q
+                pm = prof.begin("m2l");
+                ctx.launches += m2l_lattice_scatter(ops, lat_args(l, true), ctx.ws_aux, st);
+                prof.end(pm);
                 lat_apps[l] = 1;
             } else if (l >= 1 && Lay.lat[l]) {
                 // M2L as a convolution on the level's lattice (m2l_fft.h)

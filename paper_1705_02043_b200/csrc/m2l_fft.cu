@@ -1194,11 +1194,31 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     }
     }
     launches += lat_fft(A, St, S.m, 1.0, st);
+    if (!a.defer_scatter) {
+        lat_scatter_surface_kernel<<<(unsigned)std::min<int64_t>((M3 * St + 255) / 256, 148 * 32), 256, 0, st>>>(
+            A, box_of, M3, kt, n, a.alpha / ((double)N3 * (double)M3), ops.Kp, a.Y);
+        launches += 1;
+    }
+    PK_CUDA(cudaGetLastError());
+    mark("lat_inv", 0);
+    return launches + 5;
+}
+
+int m2l_lattice_scatter(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st) {
+    FftOps &f = ops.fft;
+    int launches = 0;
+    const auto m = lattice_dims(a.level, a.periodic);
+    LatticeShape &S = lattice_shape(ops, m, st, &launches);
+    const int ks = ops.ks, kt = ops.kt, n = ops.n;
+    const int64_t M3 = S.M3, N3 = (int64_t)f.N * f.N * f.N;
+    const int64_t Ss = (int64_t)8 * ks * n, St = (int64_t)8 * kt * n;
+    // the buffers m2l_lattice_level left (same names and sizes: no reallocation)
+    int *box_of = ws.get<int>("lat_boxof", M3 * 8);
+    double2 *A = reinterpret_cast<double2 *>(ws.get<double>("lat_surf", (size_t)M3 * std::max(Ss, St) * 2));
     lat_scatter_surface_kernel<<<(unsigned)std::min<int64_t>((M3 * St + 255) / 256, 148 * 32), 256, 0, st>>>(
         A, box_of, M3, kt, n, a.alpha / ((double)N3 * (double)M3), ops.Kp, a.Y);
     PK_CUDA(cudaGetLastError());
-    mark("lat_inv", 0);
-    return launches + 6;
+    return launches + 1;
 }
 
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st) {

@@ -77,6 +77,9 @@ struct LatticeLevelArgs {
     const double *X = nullptr;     // phi_up [box][Kp]
     double *Y = nullptr;           // q [box][Kp]: Y += alpha * M2L
     double alpha = 1.0;
+    // defer_scatter: m2l_lattice_level stops after the inverse lattice transform (result left in
+    // the workspace); m2l_lattice_scatter adds it into Y later, on any stream ordered after it
+    bool defer_scatter = false;
     // stage profiler hook (optional): mark(user, stage, 1) before / (.., 0) after the phases
     // "lat_fwd" (gather, lattice FFT, surface DFT), "lat_mul" (pointwise products) and
     // "lat_inv" (surface DFT, lattice FFT, scatter); work(user, stage, units, per_unit)
@@ -94,6 +97,8 @@ int64_t m2l_lattice_bytes(const KifmmOps &ops, int level, const int periodic[3])
 int m2l_lattice_check(KifmmOps &ops, const LatticeLevelArgs &a, const int *table, int64_t ld, const int *out_box,
                       int ncols, int *bad, Workspace &ws, cudaStream_t st);
 int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st);
+// the deferred last step of m2l_lattice_level (same args and workspace): Y += alpha * M2L
+int m2l_lattice_scatter(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, cudaStream_t st);
 
 // builds K^ on first use; returns kernel launches
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st);
