@@ -304,6 +304,7 @@ void pkgpu_context_destroy(pkgpu_context *ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
+    if (ctx->h_layout) cudaFreeHost(ctx->h_layout);
     if (ctx->aux2_stream) cudaStreamDestroy(ctx->aux2_stream);
     if (ctx->ev_fork2) cudaEventDestroy(ctx->ev_fork2);
     if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);

@@ -39,6 +39,7 @@ struct pkgpu_context {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t aux2_stream = nullptr;         // the deepest lattice level's M2L, from its pinv_up on (evaluate.cu)
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    int *h_layout = nullptr;                    // pinned staging of build_layout's small tables (evaluate.cu)
     cudaEvent_t ev_user = nullptr;              // hand-over between a caller's stream and own_stream (evaluate.cu)
     pkgpu::Workspace ws_aux;                    // buffers of the lattice M2L run on aux2_stream
     int64_t launches = 0;

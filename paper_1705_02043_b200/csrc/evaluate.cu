@@ -49,21 +49,13 @@ __global__ void compat_partial_kernel(const double *__restrict__ s, int64_t n, i
         for (int c = 0; c < 4; c++) part[4 * blockIdx.x + c] = red[c][0];
 }
 
-__global__ void layout_keys_kernel(TreeView T, int *keys, int *vals, int *hist) {
-    __shared__ int h[kMaxLevels * 8];
-    for (int i = threadIdx.x; i < kMaxLevels * 8; i += blockDim.x) h[i] = 0;
-    __syncthreads();
+__global__ void layout_keys_kernel(TreeView T, int *keys, int *vals) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < T.nboxes) {
         const int4 c = T.cell[b];
-        const int k = c.w * 8 + ((c.x & 1) | ((c.y & 1) << 1) | ((c.z & 1) << 2));
-        keys[b] = k;
+        keys[b] = c.w * 8 + ((c.x & 1) | ((c.y & 1) << 1) | ((c.z & 1) << 2));
         vals[b] = b;
-        atomicAdd(&h[k], 1);
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kMaxLevels * 8; i += blockDim.x)
-        if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 // Two column layouts per level (see build_layout):
@@ -368,18 +360,20 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     int *keys = ws.get<int>("lay_keys", nb), *vals = ws.get<int>("lay_vals", nb);
     int *skeys = ws.get<int>("lay_skeys", nb), *svals = ws.get<int>("lay_svals", nb);
     constexpr int NK = kMaxLevels * 8;
-    int *d_hist = ws.get<int>("lay_hist", NK);
-    PK_CUDA(cudaMemsetAsync(d_hist, 0, NK * sizeof(int), st));
-    layout_keys_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, keys, vals, d_hist);
+    layout_keys_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, keys, vals);
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, vals, svals, nb, 0, 7, st);
     void *tmp = ws.get<char>("lay_temp", tb);
     PK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, vals, svals, nb, 0, 7, st));
-    ctx.launches += 5;
-    std::vector<int> count(NK, 0), start(NK, 0), ogcol(NK, 0), mgcol(NK, 0), mbase(kMaxLevels + 1, 0),
+    ctx.launches += 4;
+    // boxes per (level, octant): counted by the tree build and read back with its header (no
+    // round trip here); the small tables below go up from pinned staging (no wait either)
+    std::vector<int> count(T.oct_hist), start(NK, 0), ogcol(NK, 0), mgcol(NK, 0), mbase(kMaxLevels + 1, 0),
         grouped(kMaxLevels + 1, 0);
-    PK_CUDA(cudaMemcpyAsync(count.data(), d_hist, NK * sizeof(int), cudaMemcpyDeviceToHost, st));
-    PK_CUDA(cudaStreamSynchronize(st));
+    count.resize(NK, 0);
+    constexpr int kStage = 4 * NK + 4 * (kMaxLevels + 1) + kMaxLevels + 2;
+    if (!ctx.h_layout) PK_CUDA(cudaMallocHost(&ctx.h_layout, kStage * sizeof(int)));
+    int *h_stage = ctx.h_layout;
     Layout L;
     L.colbase.assign(T.depth + 2, 0);
     L.octbase.assign(T.depth + 2, 0);
@@ -453,13 +447,16 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     L.noct = co;
     L.ncols = cm;
     int *d_small = ws.get<int>("lay_small", 4 * NK + 2 * (kMaxLevels + 1));
-    std::vector<int> small;
-    small.insert(small.end(), start.begin(), start.end());
-    small.insert(small.end(), ogcol.begin(), ogcol.end());
-    small.insert(small.end(), mgcol.begin(), mgcol.end());
-    small.insert(small.end(), mbase.begin(), mbase.end());
-    small.insert(small.end(), grouped.begin(), grouped.end());
-    PK_CUDA(cudaMemcpyAsync(d_small, small.data(), small.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    {
+        int *h = h_stage;
+        h = std::copy(start.begin(), start.end(), h);
+        h = std::copy(ogcol.begin(), ogcol.end(), h);
+        h = std::copy(mgcol.begin(), mgcol.end(), h);
+        h = std::copy(mbase.begin(), mbase.end(), h);
+        h = std::copy(grouped.begin(), grouped.end(), h);
+        PK_CUDA(cudaMemcpyAsync(d_small, h_stage, (h - h_stage) * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    int *h_stage2 = h_stage + 4 * NK + 2 * (kMaxLevels + 1); // the M2M tables and lvbase below
     const int64_t C = std::max<int64_t>(cm, 1), CO = std::max<int64_t>(co, 1);
     L.col_of_box = ws.get<int>("col_of_box", nb);
     L.out_box = ws.get<int>("out_box", C);
@@ -488,15 +485,15 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
         L.lvbase.assign(T.depth + 2, 0);
         for (int l = 0; l <= T.depth; l++)
             L.lvbase[l + 1] = L.lvbase[l] + (T.level_off[l + 1] - T.level_off[l] + kI8Tile - 1) / kI8Tile * kI8Tile;
-        std::vector<int> hb(L.lvbase.begin(), L.lvbase.end());
-        int *d_lvbase = ws.get<int>("lvbase", hb.size());
-        PK_CUDA(cudaMemcpyAsync(d_lvbase, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        int *hb = h_stage2 + 2 * (kMaxLevels + 1);
+        std::copy(L.lvbase.begin(), L.lvbase.end(), hb);
+        int *d_lvbase = ws.get<int>("lvbase", L.lvbase.size());
+        PK_CUDA(cudaMemcpyAsync(d_lvbase, hb, L.lvbase.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         L.lvcol = ws.get<int>("lvcol", std::max<int64_t>(L.lvbase[T.depth + 1], 1));
         PK_CUDA(cudaMemsetAsync(L.lvcol, 0xff, std::max<int64_t>(L.lvbase[T.depth + 1], 1) * sizeof(int), st));
         lvcol_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, d_lvbase, L.lvcol);
         PK_CUDA(cudaGetLastError());
         ctx.launches += 2;
-        PK_CUDA(cudaStreamSynchronize(st)); // hb is read by the async copy
     }
     // ---- M2M layout: internal boxes with sources, compacted in BFS order ----
     int *flags = ws.get<int>("m2m_flags", nb), *list = ws.get<int>("m2m_list", nb);
@@ -511,9 +508,12 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st);
     void *ftmp = ws.get<char>("m2m_sel_temp", fb);
     PK_CUDA(cub::DeviceSelect::Flagged(ftmp, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st));
-    std::vector<int> lc(kMaxLevels + 1, 0);
-    PK_CUDA(cudaMemcpyAsync(lc.data(), lcount, lc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
-    PK_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> lc(T.m2m_count); // unmasked: counted by the tree build
+    lc.resize(kMaxLevels + 1, 0);
+    if (mask) {
+        PK_CUDA(cudaMemcpyAsync(lc.data(), lcount, lc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+    }
     std::vector<int> lstart(kMaxLevels + 1, 0), cbase(kMaxLevels + 1, 0);
     L.m2mbase.assign(T.depth + 2, 0);
     int64_t cmm = 0;
@@ -531,9 +531,8 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     L.out_m2m = ws.get<int>("out_m2m", CM);
     L.m2m_src = ws.get<int>("m2m_src", 8 * CM);
     int *d_m2m_small = ws.get<int>("m2m_small", 2 * (kMaxLevels + 1));
-    std::vector<int> msmall(lstart);
-    msmall.insert(msmall.end(), cbase.begin(), cbase.end());
-    PK_CUDA(cudaMemcpyAsync(d_m2m_small, msmall.data(), msmall.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    std::copy(cbase.begin(), cbase.end(), std::copy(lstart.begin(), lstart.end(), h_stage2));
+    PK_CUDA(cudaMemcpyAsync(d_m2m_small, h_stage2, 2 * (kMaxLevels + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
     PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, CM * sizeof(int), st));
     PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * CM * sizeof(int), st));
     if (nint > 0)
@@ -541,7 +540,6 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
                                                                CM, L.out_m2m, L.m2m_src);
     PK_CUDA(cudaGetLastError());
     ctx.launches += 11;
-    PK_CUDA(cudaStreamSynchronize(st)); // host vectors above are read by async copies
     return L;
 }
 

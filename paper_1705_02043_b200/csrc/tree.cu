@@ -8,12 +8,15 @@
 // x >= box_center  <=>  the (l+1)-th most significant bit of floor(x*4096) is set,
 // because box centers (c+1/2)2^-l are exact dyadics (SURVEY.md §8a "Tree semantics").
 #include <algorithm>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <sstream>
 
 #include "tree.h"
 
 namespace pkgpu {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -57,81 +60,6 @@ __device__ __forceinline__ int lower_digit(const unsigned long long *__restrict_
     return lo;
 }
 
-// per box of level l: split decision and child ranges. 16 lanes per box: lane g searches
-// one child boundary (g < 8: sources, digit g; g >= 8: targets, digit g - 8) over the whole
-// box range, so the boundaries come from independent binary searches (one dependent chain
-// of ~log2(n) loads) instead of 14 chained ones -- the top levels, where one box spans all
-// points, were latency-bound
-__global__ void split_kernel(int n, int level, int cap, const int2 *__restrict__ srng, const int2 *__restrict__ trng,
-                             const unsigned long long *__restrict__ skeys, const unsigned long long *__restrict__ tkeys,
-                             int *__restrict__ childcnt, int4 *__restrict__ crange, int *__restrict__ err) {
-    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = gt >> 4, g = gt & 15;
-    const bool live = i < n;
-    const int2 s = live ? srng[i] : make_int2(0, 0), t = live ? trng[i] : make_int2(0, 0);
-    const bool split = live && ((s.y - s.x) > cap || (t.y - t.x) > cap);
-    const bool deep = level >= kMaxDepth;
-    int b = 0;
-    if (split && !deep) {
-        const int shift = 3 * (kMaxDepth - 1 - level);
-        const unsigned o = g & 7;
-        b = g < 8 ? (o == 0 ? s.x : lower_digit(skeys, s.x, s.y, shift, o))
-                  : (o == 0 ? t.x : lower_digit(tkeys, t.x, t.y, shift, o));
-    }
-    // gather the 16 boundaries of the box into its first lane
-    int sb[9], tb[9];
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        sb[k] = __shfl_sync(0xffffffffu, b, (threadIdx.x & 16) + k);
-        tb[k] = __shfl_sync(0xffffffffu, b, (threadIdx.x & 16) + 8 + k);
-    }
-    if (!live || g != 0) return;
-    if (!split) {
-        childcnt[i] = 0;
-        return;
-    }
-    if (deep) {
-        atomicExch(err, 1);
-        childcnt[i] = 0;
-        return;
-    }
-    sb[8] = s.y, tb[8] = t.y;
-    int cnt = 0;
-    for (int o = 0; o < 8; o++) {
-        crange[8 * (int64_t)i + o] = make_int4(sb[o], sb[o + 1], tb[o], tb[o + 1]);
-        cnt += (sb[o + 1] > sb[o] || tb[o + 1] > tb[o]) ? 1 : 0;
-    }
-    childcnt[i] = cnt;
-}
-
-__global__ void emit_kernel(int n, int64_t base_l, int64_t base_next, const int *__restrict__ childcnt,
-                            const int *__restrict__ childoff, const int4 *__restrict__ crange,
-                            unsigned long long *__restrict__ prefix, int4 *__restrict__ cell, int *__restrict__ parent,
-                            int *__restrict__ child, int *__restrict__ isleaf, int2 *__restrict__ srng,
-                            int2 *__restrict__ trng) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t gi = base_l + i;
-    const int cnt = childcnt[i];
-    isleaf[gi] = cnt == 0 ? 1 : 0;
-    if (cnt == 0) return;
-    int j = childoff[i];
-    const unsigned long long pf = prefix[gi];
-    const int4 c = cell[gi];
-    for (int o = 0; o < 8; o++) {
-        const int4 r = crange[8 * (int64_t)i + o];
-        if (r.y == r.x && r.w == r.z) continue;
-        const int64_t gc = base_next + j;
-        prefix[gc] = (pf << 3) | (unsigned long long)o;
-        cell[gc] = make_int4(2 * c.x + (o & 1), 2 * c.y + ((o >> 1) & 1), 2 * c.z + ((o >> 2) & 1), c.w + 1);
-        parent[gc] = (int)gi;
-        srng[gc] = make_int2(r.x, r.y);
-        trng[gc] = make_int2(r.z, r.w);
-        child[8 * gi + o] = (int)gc;
-        j++;
-    }
-}
-
 __global__ void gather_pos_kernel(const double *__restrict__ pts, const int *__restrict__ perm, int64_t n,
                                   double4 *__restrict__ out) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -151,25 +79,225 @@ __global__ void gather_str_kernel(const double *__restrict__ str, const int *__r
         f[i] = make_double4(str[3 * j], str[3 * j + 1], str[3 * j + 2], 0.0);
 }
 
-__global__ void leaf_flags_kernel(int n, const int *__restrict__ isleaf, int *__restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = isleaf[i];
+// ---------------------------------------------------------------------------
+// The level loop as ONE cooperative kernel (grid-wide barriers instead of a host round trip
+// per level: the level's box count decides the next level's launch, and at cfg2 those seven
+// round trips were 0.25 ms of a 3.9 ms evaluate). CTA c owns a contiguous chunk of the
+// level's boxes, so child offsets are the CTA totals' prefix plus a block scan inside the
+// chunk -- the same order as the exclusive sum over the whole level. The arrays have a
+// capacity fixed at launch; a level that would not fit sets hdr->need and every CTA stops
+// (the host grows the arrays and runs the kernel again). After the last level the same
+// scheme compacts the leaves (BFS order).
+struct TreeHeader {
+    int depth, nboxes, nleaves, err_deep;
+    long long need; // boxes needed when the capacity was exceeded (0: fits)
+    int level_off[kMaxLevels + 2];
+    int oct_hist[kMaxLevels * 8];    // boxes per (level, octant of the cell in its parent)
+    int m2m_count[kMaxLevels + 1];   // internal boxes with sources per level
+};
+
+struct TreeLoopArgs {
+    int cap, leaf_cap;
+    const unsigned long long *skeys, *tkeys;
+    unsigned long long *prefix;
+    int4 *cell;
+    int *parent, *child, *isleaf;
+    int2 *srng, *trng;
+    int *childcnt; // [cap]
+    int4 *crange;  // [8 cap]
+    int *ctatotal; // [gridDim.x]
+    int *leaves;   // [cap]
+    TreeHeader *hdr;
+};
+
+constexpr int TL_THREADS = 256;
+
+// exclusive prefix of ctatotal at this CTA and the grid total (every thread gets both)
+__device__ __forceinline__ void cta_offsets(const int *ctatotal, int &before, int &total, int *s_red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int b = 0, t = 0;
+    for (int c = tid; c < (int)gridDim.x; c += TL_THREADS) {
+        const int v = __ldcg(ctatotal + c);
+        t += v;
+        if (c < (int)blockIdx.x) b += v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    __syncthreads();
+    if (lane == 0) s_red[warp] = b, s_red[8 + warp] = t;
+    __syncthreads();
+    before = total = 0;
+#pragma unroll
+    for (int w = 0; w < TL_THREADS / 32; w++) before += s_red[w], total += s_red[8 + w];
 }
 
-// growable device array inside a Workspace (contents preserved on growth)
-template <class T> T *grow(Workspace &ws, const std::string &name, size_t need, size_t used, cudaStream_t st) {
-    auto &b = ws.bufs[name];
-    if (!b) b = std::make_unique<DevBuf>();
-    if (need * sizeof(T) <= b->bytes) return static_cast<T *>(b->ptr);
-    const size_t nb = std::max(need * sizeof(T), b->bytes * 2);
-    void *p = nullptr;
-    PK_CUDA(cudaMalloc(&p, nb));
-    if (used && b->ptr) PK_CUDA(cudaMemcpyAsync(p, b->ptr, used * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    PK_CUDA(cudaStreamSynchronize(st));
-    if (b->ptr) PK_CUDA(cudaFree(b->ptr));
-    b->ptr = p;
-    b->bytes = nb;
-    return static_cast<T *>(p);
+// block-wide exclusive scan of one value per thread; returns the exclusive prefix, sum in `total`
+__device__ __forceinline__ int block_excl_scan(int v, int &total, int *s_red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    __syncthreads();
+    if (lane == 31) s_red[warp] = inc;
+    __syncthreads();
+    int wbase = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < TL_THREADS / 32; w++) {
+        if (w < warp) wbase += s_red[w];
+        total += s_red[w];
+    }
+    return wbase + inc - v;
+}
+
+__global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_red[16];
+    __shared__ int s_total;
+    const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
+    int base = 0, nl = 1, level = 0;
+    bool overflow = false;
+    for (;; level++) {
+        if (c == 0 && tid == 0) a.hdr->level_off[level + 1] = base + nl;
+        const int chunk = (nl + G - 1) / G;
+        const int i0 = min(nl, c * chunk), i1 = min(nl, i0 + chunk);
+        // ---- split: 16 lanes per box. Lane g searches one child boundary (g < 8: sources,
+        // digit g; g >= 8: targets, digit g - 8) over the whole box range, so the boundaries
+        // come from independent binary searches (one dependent chain of ~log2(n) loads)
+        // instead of 14 chained ones: the top levels, one box spanning all points, are
+        // latency-bound ----
+        if (tid == 0) s_total = 0;
+        __syncthreads();
+        int mine = 0;
+        const bool deep = level >= kMaxDepth;
+        const int shift = deep ? 0 : 3 * (kMaxDepth - 1 - level);
+        for (int ib = i0; ib < i1; ib += TL_THREADS / 16) {
+            const int i = ib + (tid >> 4), g = tid & 15;
+            const bool live = i < i1;
+            const int2 s = live ? __ldcg(a.srng + base + i) : make_int2(0, 0);
+            const int2 t = live ? __ldcg(a.trng + base + i) : make_int2(0, 0);
+            const bool split = live && ((s.y - s.x) > a.leaf_cap || (t.y - t.x) > a.leaf_cap);
+            int b = 0;
+            if (split && !deep) {
+                const unsigned o = g & 7;
+                b = g < 8 ? (o == 0 ? s.x : lower_digit(a.skeys, s.x, s.y, shift, o))
+                          : (o == 0 ? t.x : lower_digit(a.tkeys, t.x, t.y, shift, o));
+            }
+            int sb[9], tb[9];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                sb[k] = __shfl_sync(0xffffffffu, b, (tid & 16) + k);
+                tb[k] = __shfl_sync(0xffffffffu, b, (tid & 16) + 8 + k);
+            }
+            if (!live || g != 0) continue;
+            int cnt = 0;
+            if (split && deep) {
+                atomicExch(&a.hdr->err_deep, 1);
+            } else if (split) {
+                sb[8] = s.y, tb[8] = t.y;
+                for (int o = 0; o < 8; o++) {
+                    a.crange[8 * (int64_t)i + o] = make_int4(sb[o], sb[o + 1], tb[o], tb[o + 1]);
+                    cnt += (sb[o + 1] > sb[o] || tb[o + 1] > tb[o]) ? 1 : 0;
+                }
+            }
+            a.childcnt[i] = cnt;
+            mine += cnt;
+        }
+        if (mine) atomicAdd(&s_total, mine);
+        __syncthreads();
+        if (tid == 0) a.ctatotal[c] = s_total;
+        grid.sync();
+        // ---- emit: children in box order, octant order within a box ----
+        int before, nnext;
+        cta_offsets(a.ctatotal, before, nnext, s_red);
+        if ((long long)base + nl + nnext > a.cap) {
+            if (c == 0 && tid == 0) a.hdr->need = (long long)base + nl + nnext;
+            overflow = true;
+            break; // uniform over the grid
+        }
+        int run = before;
+        for (int ib = i0; ib < i1; ib += TL_THREADS) {
+            const int i = ib + tid;
+            const bool live = i < i1;
+            const int cnt = live ? a.childcnt[i] : 0;
+            int tot;
+            int j = run + block_excl_scan(cnt, tot, s_red);
+            run += tot;
+            if (!live) continue;
+            const int gi = base + i;
+            a.isleaf[gi] = cnt == 0 ? 1 : 0;
+            if (cnt == 0) continue;
+            const unsigned long long pf = __ldcg(a.prefix + gi);
+            const int4 cc = __ldcg(a.cell + gi);
+            for (int o = 0; o < 8; o++) {
+                const int4 r = a.crange[8 * (int64_t)i + o];
+                if (r.y == r.x && r.w == r.z) continue;
+                const int gc = base + nl + j;
+                a.prefix[gc] = (pf << 3) | (unsigned long long)o;
+                a.cell[gc] = make_int4(2 * cc.x + (o & 1), 2 * cc.y + ((o >> 1) & 1), 2 * cc.z + ((o >> 2) & 1), cc.w + 1);
+                a.parent[gc] = gi;
+                a.srng[gc] = make_int2(r.x, r.y);
+                a.trng[gc] = make_int2(r.z, r.w);
+                int4 *ch = reinterpret_cast<int4 *>(a.child + 8 * (int64_t)gc);
+                ch[0] = ch[1] = make_int4(-1, -1, -1, -1);
+                a.child[8 * (int64_t)gi + o] = gc;
+                j++;
+            }
+        }
+        base += nl;
+        nl = nnext;
+        if (nnext == 0) break; // uniform
+        grid.sync(); // the new level's ranges are read by every CTA
+    }
+    if (overflow) return;
+    grid.sync(); // isleaf of the last level
+    // ---- leaves, BFS order ----
+    const int nb = base;
+    const int chunk = (nb + G - 1) / G;
+    const int i0 = min(nb, c * chunk), i1 = min(nb, i0 + chunk);
+    // (the same pass counts what the column layouts of the evaluate need: boxes per level and
+    // octant, internal boxes with sources per level)
+    __shared__ int s_hist[kMaxLevels * 8 + kMaxLevels + 1];
+    for (int k = tid; k < kMaxLevels * 8 + kMaxLevels + 1; k += TL_THREADS) s_hist[k] = 0;
+    if (tid == 0) s_total = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int i = i0 + tid; i < i1; i += TL_THREADS) {
+        const int leaf = __ldcg(a.isleaf + i);
+        mine += leaf ? 1 : 0;
+        const int4 cc = __ldcg(a.cell + i);
+        atomicAdd(&s_hist[cc.w * 8 + ((cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2))], 1);
+        const int2 sr = __ldcg(a.srng + i);
+        if (!leaf && sr.y > sr.x) atomicAdd(&s_hist[kMaxLevels * 8 + cc.w], 1);
+    }
+    if (mine) atomicAdd(&s_total, mine);
+    __syncthreads();
+    for (int k = tid; k < kMaxLevels * 8 + kMaxLevels + 1; k += TL_THREADS)
+        if (s_hist[k]) atomicAdd(k < kMaxLevels * 8 ? &a.hdr->oct_hist[k] : &a.hdr->m2m_count[k - kMaxLevels * 8], s_hist[k]);
+    if (tid == 0) a.ctatotal[c] = s_total;
+    grid.sync();
+    int before, nleaves;
+    cta_offsets(a.ctatotal, before, nleaves, s_red);
+    int run = before;
+    for (int ib = i0; ib < i1; ib += TL_THREADS) {
+        const int i = ib + tid;
+        const int f = i < i1 && __ldcg(a.isleaf + i) ? 1 : 0;
+        int tot;
+        const int j = run + block_excl_scan(f, tot, s_red);
+        run += tot;
+        if (f) a.leaves[j] = i;
+    }
+    if (c == 0 && tid == 0) {
+        a.hdr->depth = level;
+        a.hdr->nboxes = nb;
+        a.hdr->nleaves = nleaves;
+    }
 }
 
 std::string fmt_g(double v) {
@@ -273,88 +401,84 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
                                                 pass == 0 ? T.src_perm : T.trg_perm, (int)n, 0, 36, st));
         *launches += 1 + 4;
     }
-    // (the outside-domain count is read back with the root level's counts below: one host
-    // round trip fewer; nothing is allocated from the keys before that)
-
-    // level-synchronous construction
-    size_t cap = 1024, used = 0;
-    auto arrays = [&](size_t need) {
-        T.prefix = grow<unsigned long long>(ws, "prefix", need, used, st);
-        T.cell = grow<int4>(ws, "cell", need, used, st);
-        T.parent = grow<int>(ws, "parent", need, used, st);
-        T.child = grow<int>(ws, "child", 8 * need, 8 * used, st);
-        T.isleaf = grow<int>(ws, "isleaf", need, used, st);
-        T.srng = grow<int2>(ws, "srng", need, used, st);
-        T.trng = grow<int2>(ws, "trng", need, used, st);
-    };
-    arrays(cap);
-    root_init_kernel<<<1, 32, 0, st>>>(T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng, T.trng, (int)ns, (int)nt);
-    *launches += 1;
-    T.level_off.assign(1, 0);
-    int64_t nl = 1, base = 0;
-    used = 1;
-    int level = 0;
-    for (;; level++) {
-        T.level_off.push_back(base + nl);
-        int *childcnt = ws.get<int>("childcnt", nl + 1);
-        int *childoff = ws.get<int>("childoff", nl + 1);
-        int4 *crange = ws.get<int4>("crange", 8 * nl);
-        split_kernel<<<blocks_for(16 * nl, 128), 128, 0, st>>>((int)nl, level, leaf_capacity, T.srng + base,
-                                                          T.trng + base, skeys, tkeys, childcnt, crange, flags + 1);
-        size_t sb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, sb, childcnt, childoff, (int)nl + 1, st);
-        void *stemp = ws.get<char>("scan_temp", sb);
-        PK_CUDA(cudaMemsetAsync(childcnt + nl, 0, sizeof(int), st));
-        PK_CUDA(cub::DeviceScan::ExclusiveSum(stemp, sb, childcnt, childoff, (int)nl + 1, st));
-        PK_CUDA(cudaMemcpyAsync(h_flags, childoff + nl, sizeof(int), cudaMemcpyDeviceToHost, st));
-        PK_CUDA(cudaMemcpyAsync(h_flags + 1, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-        if (level == 0) PK_CUDA(cudaMemcpyAsync(h_flags + 2, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
-        PK_CUDA(cudaStreamSynchronize(st));
-        *launches += 2;
-        if (level == 0) {
-            if (same) h_flags[2] *= 2; // the reference counts the targets' offenders as well
-            if (h_flags[2] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[2]);
-        }
-        if (h_flags[1])
-            throw RuntimeError("FmmTree: leaf over capacity at maximum depth " + std::to_string(kMaxDepth) +
-                               " (duplicate point pathology)");
-        const int64_t nnext = h_flags[0];
-        if (nnext > 0) {
-            arrays(base + nl + nnext);
-            PK_CUDA(cudaMemsetAsync(T.child + 8 * (base + nl), 0xff, 8 * nnext * sizeof(int), st));
-        }
-        emit_kernel<<<blocks_for(nl, 128), 128, 0, st>>>((int)nl, base, base + nl, childcnt, childoff, crange,
-                                                         T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng,
-                                                         T.trng);
-        *launches += 1;
-        used = base + nl + nnext;
-        base += nl;
-        nl = nnext;
-        if (nnext == 0) break;
-    }
-    T.depth = level;
-    T.nboxes = base;
-    // leaves (BFS order)
-    int *lflags = ws.get<int>("lflags", T.nboxes);
-    T.leaves = ws.get<int>("leaves", T.nboxes);
-    int *nsel = ws.get<int>("nsel", 1);
-    leaf_flags_kernel<<<blocks_for(T.nboxes, 256), 256, 0, st>>>((int)T.nboxes, T.isleaf, lflags);
-    size_t fb = 0;
-    cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), lflags, T.leaves, nsel,
-                               (int)T.nboxes, st);
-    void *ftemp = ws.get<char>("flag_temp", fb);
-    PK_CUDA(cub::DeviceSelect::Flagged(ftemp, fb, cub::CountingInputIterator<int>(0), lflags, T.leaves, nsel,
-                                       (int)T.nboxes, st));
-    PK_CUDA(cudaMemcpyAsync(h_flags, nsel, sizeof(int), cudaMemcpyDeviceToHost, st));
-    // sorted point coordinates
+    // sorted point coordinates (need only the sort: queued before the level loop's read-back)
     T.src_pos = ws.get<double4>("src_pos", std::max<int64_t>(ns, 1));
     T.src_f = ws.get<double4>("src_f", std::max<int64_t>(ns, 1));
     T.trg_pos = ws.get<double4>("trg_pos", std::max<int64_t>(nt, 1));
     if (ns) gather_pos_kernel<<<blocks_for(ns, 256), 256, 0, st>>>(d_src, T.src_perm, ns, T.src_pos);
     if (nt) gather_pos_kernel<<<blocks_for(nt, 256), 256, 0, st>>>(d_trg, T.trg_perm, nt, T.trg_pos);
-    *launches += 4;
-    PK_CUDA(cudaStreamSynchronize(st));
-    T.nleaves = h_flags[0];
+    *launches += 2;
+
+    // level loop and leaf compaction: one cooperative kernel, one host round trip (the header,
+    // with the outside-domain count). The box arrays keep their capacity between calls; the
+    // first guess is four boxes per full leaf, and a tree that does not fit is rebuilt after
+    // growing to what the overflowing level asked for.
+    static_assert(sizeof(TreeHeader) % sizeof(int) == 0, "header is copied as ints");
+    if (!T.h_header) PK_CUDA(cudaMallocHost(&T.h_header, sizeof(TreeHeader)));
+    TreeHeader *hh = static_cast<TreeHeader *>(T.h_header);
+    TreeHeader *d_hdr = reinterpret_cast<TreeHeader *>(ws.get<char>("tree_header", sizeof(TreeHeader)));
+    int dev = 0, nsm = 0, per_sm = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    PK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tree_loop_kernel, TL_THREADS, 0));
+    if (per_sm < 1) throw RuntimeError("FmmTree: the level-loop kernel does not fit an SM");
+    const int grid = nsm * std::min(per_sm, 2);
+    size_t cap = std::max<size_t>(T.box_capacity,
+                                  std::max<size_t>(1024, 4 * (size_t)((ns + nt) / leaf_capacity) + 64));
+    for (bool first = true;; first = false) {
+        T.prefix = ws.get<unsigned long long>("prefix", cap);
+        T.cell = ws.get<int4>("cell", cap);
+        T.parent = ws.get<int>("parent", cap);
+        T.child = ws.get<int>("child", 8 * cap);
+        T.isleaf = ws.get<int>("isleaf", cap);
+        T.srng = ws.get<int2>("srng", cap);
+        T.trng = ws.get<int2>("trng", cap);
+        T.leaves = ws.get<int>("leaves", cap);
+        T.box_capacity = cap;
+        TreeLoopArgs a;
+        a.cap = (int)std::min<size_t>(cap, (size_t)INT32_MAX);
+        a.leaf_cap = leaf_capacity;
+        a.skeys = skeys;
+        a.tkeys = tkeys;
+        a.prefix = T.prefix;
+        a.cell = T.cell;
+        a.parent = T.parent;
+        a.child = T.child;
+        a.isleaf = T.isleaf;
+        a.srng = T.srng;
+        a.trng = T.trng;
+        a.childcnt = ws.get<int>("childcnt", cap);
+        a.crange = ws.get<int4>("crange", 8 * cap);
+        a.ctatotal = ws.get<int>("ctatotal", grid);
+        a.leaves = T.leaves;
+        a.hdr = d_hdr;
+        PK_CUDA(cudaMemsetAsync(d_hdr, 0, sizeof(TreeHeader), st));
+        root_init_kernel<<<1, 32, 0, st>>>(T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng, T.trng, (int)ns, (int)nt);
+        void *kargs[] = {&a};
+        PK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(tree_loop_kernel), dim3(grid), dim3(TL_THREADS), kargs,
+                                            0, st));
+        *launches += 2;
+        PK_CUDA(cudaMemcpyAsync(hh, d_hdr, sizeof(TreeHeader), cudaMemcpyDeviceToHost, st));
+        if (first) PK_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PK_CUDA(cudaStreamSynchronize(st));
+        if (first) {
+            if (same) h_flags[0] *= 2; // the reference counts the targets' offenders as well
+            if (h_flags[0] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[0]);
+        }
+        if (hh->need == 0) break;
+        if (hh->need > (long long)INT32_MAX) throw RuntimeError("FmmTree: more than 2^31-1 boxes");
+        cap = std::max<size_t>((size_t)hh->need + (size_t)hh->need / 2, 2 * cap);
+        cap = std::min<size_t>(cap, (size_t)INT32_MAX);
+    }
+    if (hh->err_deep)
+        throw RuntimeError("FmmTree: leaf over capacity at maximum depth " + std::to_string(kMaxDepth) +
+                           " (duplicate point pathology)");
+    T.depth = hh->depth;
+    T.nboxes = hh->nboxes;
+    T.nleaves = hh->nleaves;
+    T.level_off.assign(hh->level_off, hh->level_off + T.depth + 2);
+    T.oct_hist.assign(hh->oct_hist, hh->oct_hist + kMaxLevels * 8);
+    T.m2m_count.assign(hh->m2m_count, hh->m2m_count + kMaxLevels + 1);
 }
 
 void gather_strengths(DeviceTree &T, const double *d_str, int ks, cudaStream_t st, int64_t *launches) {

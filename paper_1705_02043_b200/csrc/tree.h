@@ -33,6 +33,8 @@ struct DeviceTree {
     int depth = 0;
     int64_t nboxes = 0, nleaves = 0;
     std::vector<int64_t> level_off; // size depth + 2
+    std::vector<int> oct_hist;      // boxes per (level, octant): [kMaxLevels * 8]
+    std::vector<int> m2m_count;     // internal boxes with sources per level: [kMaxLevels + 1]
     Workspace ws;                   // owns all device arrays below
     unsigned long long *prefix = nullptr;
     int4 *cell = nullptr;
@@ -44,8 +46,11 @@ struct DeviceTree {
     double4 *src_f = nullptr;                     // sorted Stokes forces (f0, f1, f2, 0)
     double4 *trg_pos = nullptr;                   // sorted targets (x, y, z, 0)
     int *h_flags = nullptr;                       // pinned host scratch (4 ints), allocated once
+    void *h_header = nullptr;                     // pinned copy of the level loop's header (tree.cu)
+    size_t box_capacity = 0;                      // boxes the arrays above hold (kept between builds)
     ~DeviceTree() {
         if (h_flags) cudaFreeHost(h_flags);
+        if (h_header) cudaFreeHost(h_header);
     }
 
     TreeView view() const;
