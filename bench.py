@@ -402,6 +402,9 @@ def run_ours(args):
     # ---- profiled pass (not the timed region): per-stage CUDA events on the work stream
     # and algorithmic work counts, for the stage table and the rooflines ----
     ctx.set_profiling(True)
+    # one untimed evaluate first: with profiling on every level's lattice M2L runs in the work
+    # stream's workspace, which grows (cudaFree / cudaMalloc) on its first use there
+    pk.evaluate(req, context=ctx, out=d_out, comm=comm)
     ctx.reset_stats()
     barrier()
     pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--evals", type=int, default=3)
     ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--profiling", action="store_true", help="stage profiler on (everything on the work stream)")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -31,6 +32,7 @@ def main():
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     req, pts, q = request_for(a.cfg)
     out = torch.empty(req.kernel.kt * len(pts), dtype=torch.float64, device="cuda")
+    ctx.set_profiling(a.profiling)
     for _ in range(3):
         pk.evaluate(req, context=ctx, out=out)
     torch.cuda.synchronize()
