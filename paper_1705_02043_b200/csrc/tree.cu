@@ -91,6 +91,8 @@ __global__ void gather_str_kernel(const double *__restrict__ str, const int *__r
 struct TreeHeader {
     int depth, nboxes, nleaves, err_deep;
     long long need; // boxes needed when the capacity was exceeded (0: fits)
+    int need_bits;  // a box had to split on key bits below the sorted ones (sort all 36 and rebuild)
+    int pad_;
     int level_off[kMaxLevels + 2];
     int oct_hist[kMaxLevels * 8];    // boxes per (level, octant of the cell in its parent)
     int m2m_count[kMaxLevels + 1];   // internal boxes with sources per level
@@ -98,6 +100,7 @@ struct TreeHeader {
 
 struct TreeLoopArgs {
     int cap, leaf_cap;
+    int min_bit; // the keys are sorted on bits [min_bit, 36) only
     const unsigned long long *skeys, *tkeys;
     unsigned long long *prefix;
     int4 *cell;
@@ -184,7 +187,9 @@ __global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
             const int2 t = live ? __ldcg(a.trng + base + i) : make_int2(0, 0);
             const bool split = live && ((s.y - s.x) > a.leaf_cap || (t.y - t.x) > a.leaf_cap);
             int b = 0;
-            if (split && !deep) {
+            if (split && !deep && shift < a.min_bit) {
+                if (g == 0) atomicExch(&a.hdr->need_bits, 1);
+            } else if (split && !deep) {
                 const unsigned o = g & 7;
                 b = g < 8 ? (o == 0 ? s.x : lower_digit(a.skeys, s.x, s.y, shift, o))
                           : (o == 0 ? t.x : lower_digit(a.tkeys, t.x, t.y, shift, o));
@@ -216,6 +221,10 @@ __global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
         // ---- emit: children in box order, octant order within a box ----
         int before, nnext;
         cta_offsets(a.ctatotal, before, nnext, s_red);
+        if (a.min_bit > 0 && __ldcg(&a.hdr->need_bits)) {
+            overflow = true;
+            break; // uniform over the grid (written before the barrier)
+        }
         if ((long long)base + nl + nnext > a.cap) {
             if (c == 0 && tid == 0) a.hdr->need = (long long)base + nl + nnext;
             overflow = true;
@@ -380,34 +389,42 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     if (!T.h_flags) PK_CUDA(cudaMallocHost(&T.h_flags, 4 * sizeof(int)));
     int *h_flags = T.h_flags;
 
-    PK_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), st));
-    // keys + sort, sources then targets (the "bad" counter accumulates both)
+    // keys + sort, sources then targets (the "bad" counter accumulates both). The sort covers
+    // the key bits of the first 8 levels only (three 8-bit passes instead of five) unless a
+    // tree of this context has needed more: a box that must split at level >= 8 makes the
+    // level loop ask for the full sort (need_bits), once, and the context remembers.
     size_t temp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, k_in, skeys, i_in, T.src_perm, (int)nmax, 0, 36, st);
     void *temp = ws.get<char>("sort_temp", temp_bytes);
     // targets that are the sources (same buffer) sort once; the keys and order are copied
     const bool same = d_trg == d_src && nt == ns;
-    for (int pass = 0; pass < 2; pass++) {
-        const int64_t n = pass == 0 ? ns : nt;
-        if (n == 0) continue;
-        if (pass == 1 && same) {
-            PK_CUDA(cudaMemcpyAsync(tkeys, skeys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-            PK_CUDA(cudaMemcpyAsync(T.trg_perm, T.src_perm, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
-            continue;
-        }
-        keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(pass == 0 ? d_src : d_trg, n, k_in, i_in, flags);
-        size_t tb = temp_bytes;
-        PK_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k_in, pass == 0 ? skeys : tkeys, i_in,
-                                                pass == 0 ? T.src_perm : T.trg_perm, (int)n, 0, 36, st));
-        *launches += 1 + 4;
-    }
-    // sorted point coordinates (need only the sort: queued before the level loop's read-back)
     T.src_pos = ws.get<double4>("src_pos", std::max<int64_t>(ns, 1));
     T.src_f = ws.get<double4>("src_f", std::max<int64_t>(ns, 1));
     T.trg_pos = ws.get<double4>("trg_pos", std::max<int64_t>(nt, 1));
-    if (ns) gather_pos_kernel<<<blocks_for(ns, 256), 256, 0, st>>>(d_src, T.src_perm, ns, T.src_pos);
-    if (nt) gather_pos_kernel<<<blocks_for(nt, 256), 256, 0, st>>>(d_trg, T.trg_perm, nt, T.trg_pos);
-    *launches += 2;
+    auto sort_points = [&](int min_bit) {
+        PK_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), st));
+        for (int pass = 0; pass < 2; pass++) {
+            const int64_t n = pass == 0 ? ns : nt;
+            if (n == 0) continue;
+            if (pass == 1 && same) {
+                PK_CUDA(cudaMemcpyAsync(tkeys, skeys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+                PK_CUDA(cudaMemcpyAsync(T.trg_perm, T.src_perm, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+                continue;
+            }
+            keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(pass == 0 ? d_src : d_trg, n, k_in, i_in, flags);
+            size_t tb = temp_bytes;
+            PK_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k_in, pass == 0 ? skeys : tkeys, i_in,
+                                                    pass == 0 ? T.src_perm : T.trg_perm, (int)n, min_bit, 36, st));
+            *launches += 1 + 4;
+        }
+        // sorted point coordinates (need only the sort: queued before the level loop's read-back)
+        if (ns) gather_pos_kernel<<<blocks_for(ns, 256), 256, 0, st>>>(d_src, T.src_perm, ns, T.src_pos);
+        if (nt) gather_pos_kernel<<<blocks_for(nt, 256), 256, 0, st>>>(d_trg, T.trg_perm, nt, T.trg_pos);
+        *launches += 2;
+    };
+    constexpr int kPartialSortBit = 3 * (kMaxDepth - 8); // levels 0..7 split on bits >= this
+    int min_bit = T.full_sort ? 0 : kPartialSortBit;
+    sort_points(min_bit);
 
     // level loop and leaf compaction: one cooperative kernel, one host round trip (the header,
     // with the outside-domain count). The box arrays keep their capacity between calls; the
@@ -438,6 +455,7 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         TreeLoopArgs a;
         a.cap = (int)std::min<size_t>(cap, (size_t)INT32_MAX);
         a.leaf_cap = leaf_capacity;
+        a.min_bit = min_bit;
         a.skeys = skeys;
         a.tkeys = tkeys;
         a.prefix = T.prefix;
@@ -464,6 +482,12 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         if (first) {
             if (same) h_flags[0] *= 2; // the reference counts the targets' offenders as well
             if (h_flags[0] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[0]);
+        }
+        if (hh->need_bits) {
+            T.full_sort = true;
+            min_bit = 0;
+            sort_points(0);
+            continue;
         }
         if (hh->need == 0) break;
         if (hh->need > (long long)INT32_MAX) throw RuntimeError("FmmTree: more than 2^31-1 boxes");

@@ -47,6 +47,7 @@ struct DeviceTree {
     double4 *trg_pos = nullptr;                   // sorted targets (x, y, z, 0)
     int *h_flags = nullptr;                       // pinned host scratch (4 ints), allocated once
     void *h_header = nullptr;                     // pinned copy of the level loop's header (tree.cu)
+    bool full_sort = false;                       // a tree here needed more than 8 levels: sort all 36 key bits
     size_t box_capacity = 0;                      // boxes the arrays above hold (kept between builds)
     ~DeviceTree() {
         if (h_flags) cudaFreeHost(h_flags);
