@@ -459,16 +459,16 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     int *h_stage2 = h_stage + 4 * NK + 2 * (kMaxLevels + 1); // the M2M tables and lvbase below
     const int64_t C = std::max<int64_t>(cm, 1), CO = std::max<int64_t>(co, 1);
     L.col_of_box = ws.get<int>("col_of_box", nb);
-    L.out_box = ws.get<int>("out_box", C);
-    L.m2l_table = ws.get<int>("m2l_table", (size_t)kNumM2L * C);
-    L.out_oct = ws.get<int>("out_oct", CO);
-    L.l2l_src = ws.get<int>("l2l_src", CO);
+    // the -1-initialised tables share one buffer (one memset instead of four; C, CO are
+    // multiples of 64, so every table stays 256-byte aligned)
+    int *ff = ws.get<int>("lay_ff", (size_t)C + 2 * (size_t)CO + (size_t)kNumM2L * C);
+    L.out_box = ff;
+    L.out_oct = ff + C;
+    L.l2l_src = L.out_oct + CO;
+    L.m2l_table = L.l2l_src + CO;
     L.tile_oct = ws.get<int>("tile_oct", CO / BN + 1);
     PK_CUDA(cudaMemsetAsync(L.tile_oct, 0, (CO / BN + 1) * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.out_box, 0xff, C * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.m2l_table, 0xff, (size_t)kNumM2L * C * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.out_oct, 0xff, CO * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.l2l_src, 0xff, CO * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(ff, 0xff, ((size_t)C + 2 * (size_t)CO + (size_t)kNumM2L * C) * sizeof(int), st));
     layout_fill_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(
         tv, skeys, svals, d_small, d_small + NK, d_small + 2 * NK, d_small + 3 * NK, d_small + 3 * NK + kMaxLevels + 1,
         L.col_of_box, L.out_box, L.out_oct, L.l2l_src, L.tile_oct);
@@ -496,23 +496,27 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
         ctx.launches += 2;
     }
     // ---- M2M layout: internal boxes with sources, compacted in BFS order ----
-    int *flags = ws.get<int>("m2m_flags", nb), *list = ws.get<int>("m2m_list", nb);
-    int *lcount = ws.get<int>("m2m_lcount", kMaxLevels + 1), *nsel = ws.get<int>("m2m_nsel", 1);
-    PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
-    if (mask && !ctx.i8.trans) {
-        mask_oct_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(mask, CO, L.out_oct, L.l2l_src);
-        ctx.launches += 1;
-    }
-    m2m_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, mask, flags, lcount);
-    size_t fb = 0;
-    cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st);
-    void *ftmp = ws.get<char>("m2m_sel_temp", fb);
-    PK_CUDA(cub::DeviceSelect::Flagged(ftmp, fb, cub::CountingInputIterator<int>(0), flags, list, nsel, nb, st));
-    std::vector<int> lc(T.m2m_count); // unmasked: counted by the tree build
+    // (unmasked: the tree build has listed and counted them; a partition's mask selects here)
+    const int *list = T.m2m_list;
+    std::vector<int> lc(T.m2m_count);
     lc.resize(kMaxLevels + 1, 0);
     if (mask) {
+        int *flags = ws.get<int>("m2m_flags", nb), *sel = ws.get<int>("m2m_list", nb);
+        int *lcount = ws.get<int>("m2m_lcount", kMaxLevels + 1), *nsel = ws.get<int>("m2m_nsel", 1);
+        PK_CUDA(cudaMemsetAsync(lcount, 0, (kMaxLevels + 1) * sizeof(int), st));
+        if (!ctx.i8.trans) {
+            mask_oct_kernel<<<blocks_for(CO, 256), 256, 0, st>>>(mask, CO, L.out_oct, L.l2l_src);
+            ctx.launches += 1;
+        }
+        m2m_flags_kernel<<<blocks_for(nb, 256), 256, 0, st>>>(tv, mask, flags, lcount);
+        size_t fb = 0;
+        cub::DeviceSelect::Flagged(nullptr, fb, cub::CountingInputIterator<int>(0), flags, sel, nsel, nb, st);
+        void *ftmp = ws.get<char>("m2m_sel_temp", fb);
+        PK_CUDA(cub::DeviceSelect::Flagged(ftmp, fb, cub::CountingInputIterator<int>(0), flags, sel, nsel, nb, st));
         PK_CUDA(cudaMemcpyAsync(lc.data(), lcount, lc.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         PK_CUDA(cudaStreamSynchronize(st));
+        list = sel;
+        ctx.launches += 4;
     }
     std::vector<int> lstart(kMaxLevels + 1, 0), cbase(kMaxLevels + 1, 0);
     L.m2mbase.assign(T.depth + 2, 0);
@@ -528,18 +532,17 @@ Layout build_layout(pkgpu_context &ctx, const DeviceTree &T, const int *mask, co
     L.m2mbase[T.depth + 1] = cmm;
     L.nm2m = cmm;
     const int64_t CM = std::max<int64_t>(cmm, 1);
-    L.out_m2m = ws.get<int>("out_m2m", CM);
-    L.m2m_src = ws.get<int>("m2m_src", 8 * CM);
+    L.out_m2m = ws.get<int>("m2m_ff", 9 * CM); // out_m2m [CM] and m2m_src [8][CM]: one -1 fill
+    L.m2m_src = L.out_m2m + CM;
     int *d_m2m_small = ws.get<int>("m2m_small", 2 * (kMaxLevels + 1));
     std::copy(cbase.begin(), cbase.end(), std::copy(lstart.begin(), lstart.end(), h_stage2));
     PK_CUDA(cudaMemcpyAsync(d_m2m_small, h_stage2, 2 * (kMaxLevels + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
-    PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, CM * sizeof(int), st));
-    PK_CUDA(cudaMemsetAsync(L.m2m_src, 0xff, 8 * CM * sizeof(int), st));
+    PK_CUDA(cudaMemsetAsync(L.out_m2m, 0xff, 9 * CM * sizeof(int), st));
     if (nint > 0)
         m2m_fill_kernel<<<blocks_for(nint, 256), 256, 0, st>>>(tv, list, nint, d_m2m_small, d_m2m_small + kMaxLevels + 1,
                                                                CM, L.out_m2m, L.m2m_src);
     PK_CUDA(cudaGetLastError());
-    ctx.launches += 11;
+    ctx.launches += 6;
     return L;
 }
 

@@ -108,8 +108,9 @@ struct TreeLoopArgs {
     int2 *srng, *trng;
     int *childcnt; // [cap]
     int4 *crange;  // [8 cap]
-    int *ctatotal; // [gridDim.x]
+    int *ctatotal; // [2 gridDim.x]
     int *leaves;   // [cap]
+    int *m2m_list; // [cap]: internal boxes with sources, BFS order (the evaluate's M2M columns)
     TreeHeader *hdr;
 };
 
@@ -289,18 +290,32 @@ __global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
     __syncthreads();
     for (int k = tid; k < kMaxLevels * 8 + kMaxLevels + 1; k += TL_THREADS)
         if (s_hist[k]) atomicAdd(k < kMaxLevels * 8 ? &a.hdr->oct_hist[k] : &a.hdr->m2m_count[k - kMaxLevels * 8], s_hist[k]);
-    if (tid == 0) a.ctatotal[c] = s_total;
+    if (tid == 0) {
+        a.ctatotal[c] = s_total;
+        int m2m = 0; // this CTA's boxes are a BFS range: its per-level counts add up to its share
+        for (int l = 0; l <= kMaxLevels; l++) m2m += s_hist[kMaxLevels * 8 + l];
+        a.ctatotal[G + c] = m2m;
+    }
     grid.sync();
-    int before, nleaves;
+    int before, nleaves, before2, nm2m;
     cta_offsets(a.ctatotal, before, nleaves, s_red);
-    int run = before;
+    cta_offsets(a.ctatotal + G, before2, nm2m, s_red);
+    int run = before, run2 = before2;
     for (int ib = i0; ib < i1; ib += TL_THREADS) {
         const int i = ib + tid;
-        const int f = i < i1 && __ldcg(a.isleaf + i) ? 1 : 0;
+        const int leaf = i < i1 && __ldcg(a.isleaf + i) ? 1 : 0;
+        int f2 = 0;
+        if (i < i1 && !leaf) {
+            const int2 sr = __ldcg(a.srng + i);
+            f2 = sr.y > sr.x ? 1 : 0;
+        }
         int tot;
-        const int j = run + block_excl_scan(f, tot, s_red);
+        const int j = run + block_excl_scan(leaf, tot, s_red);
         run += tot;
-        if (f) a.leaves[j] = i;
+        if (leaf) a.leaves[j] = i;
+        const int j2 = run2 + block_excl_scan(f2, tot, s_red);
+        run2 += tot;
+        if (f2) a.m2m_list[j2] = i;
     }
     if (c == 0 && tid == 0) {
         a.hdr->depth = level;
@@ -451,6 +466,7 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         T.srng = ws.get<int2>("srng", cap);
         T.trng = ws.get<int2>("trng", cap);
         T.leaves = ws.get<int>("leaves", cap);
+        T.m2m_list = ws.get<int>("m2m_list", cap);
         T.box_capacity = cap;
         TreeLoopArgs a;
         a.cap = (int)std::min<size_t>(cap, (size_t)INT32_MAX);
@@ -467,8 +483,9 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         a.trng = T.trng;
         a.childcnt = ws.get<int>("childcnt", cap);
         a.crange = ws.get<int4>("crange", 8 * cap);
-        a.ctatotal = ws.get<int>("ctatotal", grid);
+        a.ctatotal = ws.get<int>("ctatotal", 2 * grid);
         a.leaves = T.leaves;
+        a.m2m_list = T.m2m_list;
         a.hdr = d_hdr;
         PK_CUDA(cudaMemsetAsync(d_hdr, 0, sizeof(TreeHeader), st));
         root_init_kernel<<<1, 32, 0, st>>>(T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng, T.trng, (int)ns, (int)nt);

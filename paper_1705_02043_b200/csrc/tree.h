@@ -42,6 +42,7 @@ struct DeviceTree {
     int2 *srng = nullptr, *trng = nullptr;
     int *src_perm = nullptr, *trg_perm = nullptr; // sorted position -> original index
     int *leaves = nullptr;                        // leaf box ids, BFS order
+    int *m2m_list = nullptr;                      // internal boxes with sources, BFS order (sum of m2m_count)
     double4 *src_pos = nullptr;                   // sorted sources (x, y, z, charge-or-0)
     double4 *src_f = nullptr;                     // sorted Stokes forces (f0, f1, f2, 0)
     double4 *trg_pos = nullptr;                   // sorted targets (x, y, z, 0)
