@@ -101,6 +101,7 @@ struct TreeHeader {
 struct TreeLoopArgs {
     int cap, leaf_cap;
     int min_bit; // the keys are sorted on bits [min_bit, 36) only
+    int ns, nt;  // the root's ranges
     const unsigned long long *skeys, *tkeys;
     unsigned long long *prefix;
     int4 *cell;
@@ -167,6 +168,17 @@ __global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
     const int tid = threadIdx.x, G = gridDim.x, c = blockIdx.x;
     int base = 0, nl = 1, level = 0;
     bool overflow = false;
+    // the root box (level 0: every point, no parent, no children yet); its ranges come from
+    // the arguments at level 0, so no barrier is needed before the first split
+    if (c == 0 && tid < 8) a.child[tid] = -1;
+    if (c == 0 && tid == 0) {
+        a.prefix[0] = 0ull;
+        a.cell[0] = make_int4(0, 0, 0, 0);
+        a.parent[0] = -1;
+        a.isleaf[0] = 1;
+        a.srng[0] = make_int2(0, a.ns);
+        a.trng[0] = make_int2(0, a.nt);
+    }
     for (;; level++) {
         if (c == 0 && tid == 0) a.hdr->level_off[level + 1] = base + nl;
         const int chunk = (nl + G - 1) / G;
@@ -184,8 +196,8 @@ __global__ void __launch_bounds__(TL_THREADS) tree_loop_kernel(TreeLoopArgs a) {
         for (int ib = i0; ib < i1; ib += TL_THREADS / 16) {
             const int i = ib + (tid >> 4), g = tid & 15;
             const bool live = i < i1;
-            const int2 s = live ? __ldcg(a.srng + base + i) : make_int2(0, 0);
-            const int2 t = live ? __ldcg(a.trng + base + i) : make_int2(0, 0);
+            const int2 s = !live ? make_int2(0, 0) : level == 0 ? make_int2(0, a.ns) : __ldcg(a.srng + base + i);
+            const int2 t = !live ? make_int2(0, 0) : level == 0 ? make_int2(0, a.nt) : __ldcg(a.trng + base + i);
             const bool split = live && ((s.y - s.x) > a.leaf_cap || (t.y - t.x) > a.leaf_cap);
             int b = 0;
             if (split && !deep && shift < a.min_bit) {
@@ -369,21 +381,6 @@ TreeView DeviceTree::view() const {
     return v;
 }
 
-// the root box (level 0: every point, no parent, no children yet)
-__global__ void root_init_kernel(unsigned long long *prefix, int4 *cell, int *parent, int *child, int *isleaf,
-                                 int2 *srng, int2 *trng, int ns, int nt) {
-    const int t = threadIdx.x;
-    if (t < 8) child[t] = -1;
-    if (t == 0) {
-        prefix[0] = 0ull;
-        cell[0] = make_int4(0, 0, 0, 0);
-        parent[0] = -1;
-        isleaf[0] = 1;
-        srng[0] = make_int2(0, ns);
-        trng[0] = make_int2(0, nt);
-    }
-}
-
 void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_trg, int64_t nt, int leaf_capacity,
                 cudaStream_t st, int64_t *launches) {
     if (leaf_capacity < 1) throw InvalidArgument("FmmTree: leaf capacity must be positive");
@@ -400,7 +397,10 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     unsigned long long *tkeys = ws.get<unsigned long long>("tkeys", std::max<int64_t>(nt, 1));
     T.src_perm = ws.get<int>("src_perm", std::max<int64_t>(ns, 1));
     T.trg_perm = ws.get<int>("trg_perm", std::max<int64_t>(nt, 1));
-    int *flags = ws.get<int>("flags", 4);
+    // the level loop's header and the outside-domain counter share one buffer (one memset)
+    static_assert(sizeof(TreeHeader) % sizeof(int) == 0, "flags follow the header");
+    TreeHeader *d_hdr = reinterpret_cast<TreeHeader *>(ws.get<char>("tree_header", sizeof(TreeHeader) + 4 * sizeof(int)));
+    int *flags = reinterpret_cast<int *>(d_hdr + 1);
     if (!T.h_flags) PK_CUDA(cudaMallocHost(&T.h_flags, 4 * sizeof(int)));
     int *h_flags = T.h_flags;
 
@@ -415,17 +415,18 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     const bool same = d_trg == d_src && nt == ns;
     T.src_pos = ws.get<double4>("src_pos", std::max<int64_t>(ns, 1));
     T.src_f = ws.get<double4>("src_f", std::max<int64_t>(ns, 1));
-    T.trg_pos = ws.get<double4>("trg_pos", std::max<int64_t>(nt, 1));
+    // (readers of trg_pos use x, y, z only: the sources' w, the Laplace charge, does not matter)
+    T.trg_pos = same ? T.src_pos : ws.get<double4>("trg_pos", std::max<int64_t>(nt, 1));
+    if (same) {
+        tkeys = skeys;
+        T.trg_perm = T.src_perm;
+    }
     auto sort_points = [&](int min_bit) {
-        PK_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), st));
+        PK_CUDA(cudaMemsetAsync(d_hdr, 0, sizeof(TreeHeader) + 4 * sizeof(int), st));
         for (int pass = 0; pass < 2; pass++) {
             const int64_t n = pass == 0 ? ns : nt;
             if (n == 0) continue;
-            if (pass == 1 && same) {
-                PK_CUDA(cudaMemcpyAsync(tkeys, skeys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-                PK_CUDA(cudaMemcpyAsync(T.trg_perm, T.src_perm, n * sizeof(int), cudaMemcpyDeviceToDevice, st));
-                continue;
-            }
+            if (pass == 1 && same) continue; // the targets alias the sources' keys, order and positions
             keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(pass == 0 ? d_src : d_trg, n, k_in, i_in, flags);
             size_t tb = temp_bytes;
             PK_CUDA(cub::DeviceRadixSort::SortPairs(temp, tb, k_in, pass == 0 ? skeys : tkeys, i_in,
@@ -434,8 +435,8 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         }
         // sorted point coordinates (need only the sort: queued before the level loop's read-back)
         if (ns) gather_pos_kernel<<<blocks_for(ns, 256), 256, 0, st>>>(d_src, T.src_perm, ns, T.src_pos);
-        if (nt) gather_pos_kernel<<<blocks_for(nt, 256), 256, 0, st>>>(d_trg, T.trg_perm, nt, T.trg_pos);
-        *launches += 2;
+        if (nt && !same) gather_pos_kernel<<<blocks_for(nt, 256), 256, 0, st>>>(d_trg, T.trg_perm, nt, T.trg_pos);
+        *launches += same ? 1 : 2;
     };
     constexpr int kPartialSortBit = 3 * (kMaxDepth - 8); // levels 0..7 split on bits >= this
     int min_bit = T.full_sort ? 0 : kPartialSortBit;
@@ -446,9 +447,8 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     // first guess is four boxes per full leaf, and a tree that does not fit is rebuilt after
     // growing to what the overflowing level asked for.
     static_assert(sizeof(TreeHeader) % sizeof(int) == 0, "header is copied as ints");
-    if (!T.h_header) PK_CUDA(cudaMallocHost(&T.h_header, sizeof(TreeHeader)));
+    if (!T.h_header) PK_CUDA(cudaMallocHost(&T.h_header, sizeof(TreeHeader) + 4 * sizeof(int)));
     TreeHeader *hh = static_cast<TreeHeader *>(T.h_header);
-    TreeHeader *d_hdr = reinterpret_cast<TreeHeader *>(ws.get<char>("tree_header", sizeof(TreeHeader)));
     int dev = 0, nsm = 0, per_sm = 0;
     PK_CUDA(cudaGetDevice(&dev));
     PK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -487,16 +487,17 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
         a.leaves = T.leaves;
         a.m2m_list = T.m2m_list;
         a.hdr = d_hdr;
-        PK_CUDA(cudaMemsetAsync(d_hdr, 0, sizeof(TreeHeader), st));
-        root_init_kernel<<<1, 32, 0, st>>>(T.prefix, T.cell, T.parent, T.child, T.isleaf, T.srng, T.trng, (int)ns, (int)nt);
+        a.ns = (int)ns;
+        a.nt = (int)nt;
+        if (!first) PK_CUDA(cudaMemsetAsync(d_hdr, 0, sizeof(TreeHeader), st)); // (first: zeroed with the sort)
         void *kargs[] = {&a};
         PK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(tree_loop_kernel), dim3(grid), dim3(TL_THREADS), kargs,
                                             0, st));
-        *launches += 2;
-        PK_CUDA(cudaMemcpyAsync(hh, d_hdr, sizeof(TreeHeader), cudaMemcpyDeviceToHost, st));
-        if (first) PK_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+        *launches += 1;
+        PK_CUDA(cudaMemcpyAsync(hh, d_hdr, sizeof(TreeHeader) + 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
         PK_CUDA(cudaStreamSynchronize(st));
         if (first) {
+            h_flags[0] = reinterpret_cast<const int *>(hh + 1)[0]; // points outside the domain
             if (same) h_flags[0] *= 2; // the reference counts the targets' offenders as well
             if (h_flags[0] > 0) outside_message(d_src, ns, d_trg, nt, h_flags[0]);
         }
