@@ -454,7 +454,10 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     PK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tree_loop_kernel, TL_THREADS, 0));
     if (per_sm < 1) throw RuntimeError("FmmTree: the level-loop kernel does not fit an SM");
-    const int grid = nsm * std::min(per_sm, 2);
+    // CTAs per SM: the barriers cost more with more CTAs and a small tree is bound by them; a
+    // large one by the latency of its boundary searches, which more resident warps hide
+    const int64_t npts = ns + nt;
+    const int grid = nsm * std::min(per_sm, npts > 4000000 ? 4 : npts > 400000 ? 2 : 1);
     size_t cap = std::max<size_t>(T.box_capacity,
                                   std::max<size_t>(1024, 4 * (size_t)((ns + nt) / leaf_capacity) + 64));
     for (bool first = true;; first = false) {
