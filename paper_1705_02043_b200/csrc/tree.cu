@@ -13,6 +13,7 @@
 #include <sstream>
 
 #include "tree.h"
+#include "tuning.h"
 
 namespace pkgpu {
 
@@ -460,6 +461,7 @@ void build_tree(DeviceTree &T, const double *d_src, int64_t ns, const double *d_
     const int grid = nsm * std::min(per_sm, npts > 4000000 ? 4 : npts > 400000 ? 2 : 1);
     size_t cap = std::max<size_t>(T.box_capacity,
                                   std::max<size_t>(1024, 4 * (size_t)((ns + nt) / leaf_capacity) + 64));
+    if (tuning().tree_cap > 0) cap = std::max<size_t>(T.box_capacity, (size_t)tuning().tree_cap);
     for (bool first = true;; first = false) {
         T.prefix = ws.get<unsigned long long>("prefix", cap);
         T.cell = ws.get<int4>("cell", cap);

@@ -43,6 +43,7 @@ const Tuning &tuning() {
         r.gemm_skinny_apps = env_int("PKGPU_GEMM_SKINNY", r.gemm_skinny_apps, 0);
         r.overlap_lists = env_int("PKGPU_OVERLAP_LISTS", 1, 0) != 0;
         r.overlap_m2l = env_int("PKGPU_OVERLAP_M2L", 1, 0) != 0;
+        r.tree_cap = env_int("PKGPU_TREE_CAP", 0, 0);
         r.list_warp_max = env_int("PKGPU_LIST_WARP_MAX", r.list_warp_max, 0);
         r.leaf_tt = (int)env_int("PKGPU_LEAF_TT", r.leaf_tt, 1);
         r.m2l_lattice = env_int("PKGPU_M2L_LATTICE", 1, 0) != 0;

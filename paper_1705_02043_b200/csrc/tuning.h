@@ -35,6 +35,8 @@ struct Tuning {
     bool overlap_lists = true;         // PKGPU_OVERLAP_LISTS = 0 | 1: lists on the auxiliary stream beside the upward pass
     bool overlap_m2l = true;           // PKGPU_OVERLAP_M2L = 0 | 1: the deepest lattice level's M2L on the auxiliary
                                        // stream beside the coarse levels' downward chain
+    int64_t tree_cap = 0;              // PKGPU_TREE_CAP: first box capacity of the tree arrays (0: four boxes per full
+                                       // leaf); a small value exercises the grow-and-rebuild path (tests)
     int64_t list_warp_max = 50000;     // PKGPU_LIST_WARP_MAX: trees up to this size list a warp per box
     int leaf_tt = 2;                   // PKGPU_LEAF_TT = 1 | 2 | 4: targets per thread in the leaf pass
     bool m2l_lattice = true;           // PKGPU_M2L_LATTICE = 0 | 1: filled levels by the lattice FFT M2L

@@ -141,6 +141,20 @@ def test_structure_hash_at_baseline_sizes(cfg, kind, n, leaf, ks, kw, expect):
     assert t.structure_hash() == expect
 
 
+def test_tree_rebuild_paths():
+    """The level loop runs in one kernel over arrays of fixed capacity: a level that does not
+    fit makes it report what it needs and the host rebuilds (PKGPU_TREE_CAP=8 forces that on
+    every golden tree; the knob is read once per process). The adaptive tree also splits
+    below level 8, i.e. past the key bits of the first sort (the full-sort fallback)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, PKGPU_TREE_CAP="8")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__, "-k",
+                        "test_tree_bit_exact or test_lists_bit_exact"], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_tree_errors():
     pts = np.array([[0.5, 0.5, 0.5], [1.0, 0.2, 0.2], [0.1, -0.3, 0.2]])
     with pytest.raises(ValueError, match=r"FmmTree: 2 points outside \[0,1\)\^3: source\[1\]=\(1,0.2,0.2\)"):
