@@ -885,62 +885,86 @@ __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 t) {
     acc.y = fma(a.x, t.y, fma(a.y, t.x, acc.y));
 }
 
+// Two groups g (lattice frequency, octant, component) per CTA, side by side: stages 1 and 2
+// have P^2 and P NH columns per group -- 64 each at p = 8, half of a 128-thread CTA, always
+// the same two warps (the same two of the SM's four schedulers) -- so the second group takes
+// the other half; stage 3 runs both groups' columns over all threads.
 template <int P>
 __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restrict__ A, int n,
-                                                         const int *__restrict__ gidx, double2 *__restrict__ Psi) {
+                                                         const int *__restrict__ gidx, double2 *__restrict__ Psi,
+                                                         int64_t ngroups) {
     constexpr int N = fft_edge(P), NH = N / 2 + 1, NW = N * N * NH;
+    constexpr int CUBE = P * P * P, F1 = P * P * NH, F2 = P * N * NH;
     extern __shared__ double2 lt_sm[];
-    double2 *tw = lt_sm;                 // [N]
-    double2 *cube = tw + N;              // [P^3]
-    double2 *f1 = cube + P * P * P;      // [x][y][kz]
-    double2 *f2 = f1 + P * P * NH;       // [x][ky][kz]
-    const int64_t g = blockIdx.x;
-    const double2 *in = A + g * n;
-    double2 *out = Psi + g * NW;
+    double2 *tw = lt_sm;             // [N]
+    double2 *cube = tw + N;          // 2 x [P^3]
+    double2 *f1 = cube + 2 * CUBE;   // 2 x [x][y][kz]
+    double2 *f2 = f1 + 2 * F1;       // 2 x [x][ky][kz]
+    const int64_t g0 = 2 * (int64_t)blockIdx.x;
+    const int ng = g0 + 1 < ngroups ? 2 : 1;
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int k = tid; k < N; k += nt) {
         double s, c;
         sincospi(-2.0 * k / N, &s, &c);
         tw[k] = make_double2(c, s);
     }
-    for (int e = tid; e < P * P * P; e += nt) cube[e] = make_double2(0.0, 0.0);
+    for (int e = tid; e < 2 * CUBE; e += nt) cube[e] = make_double2(0.0, 0.0);
     __syncthreads();
-    for (int i = tid; i < n; i += nt) {
+    for (int e = tid; e < ng * n; e += nt) {
+        const int h = e / n, i = e % n;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
-        cube[(x * P + y) * P + z] = in[i];
+        cube[h * CUBE + (x * P + y) * P + z] = A[(g0 + h) * n + i];
     }
     __syncthreads();
-    for (int xy = tid; xy < P * P; xy += nt) { // z: P -> NH
-        double2 v[P];
+    const int half = nt / 2; // threads per group in stages 1 and 2
+    {
+        const int h = tid / half, t = tid % half;
+        if (h < ng) {
+            const double2 *cb = cube + h * CUBE;
+            double2 *o1 = f1 + h * F1;
+            for (int xy = t; xy < P * P; xy += half) { // z: P -> NH
+                double2 v[P];
 #pragma unroll
-        for (int z = 0; z < P; z++) v[z] = cube[xy * P + z];
+                for (int z = 0; z < P; z++) v[z] = cb[xy * P + z];
 #pragma unroll
-        for (int kz = 0; kz < NH; kz++) {
-            double2 acc = make_double2(0.0, 0.0);
+                for (int kz = 0; kz < NH; kz++) {
+                    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int z = 0; z < P; z++) cmac(acc, v[z], tw[(kz * z) % N]);
-            f1[xy * NH + kz] = acc;
+                    for (int z = 0; z < P; z++) cmac(acc, v[z], tw[(kz * z) % N]);
+                    o1[xy * NH + kz] = acc;
+                }
+            }
         }
     }
     __syncthreads();
-    for (int col = tid; col < P * NH; col += nt) { // y: P -> N, column (x, kz)
-        const int x = col / NH, kz = col % NH;
-        double2 v[P];
+    {
+        const int h = tid / half, t = tid % half;
+        if (h < ng) {
+            const double2 *i1 = f1 + h * F1;
+            double2 *o2 = f2 + h * F2;
+            for (int col = t; col < P * NH; col += half) { // y: P -> N, column (x, kz)
+                const int x = col / NH, kz = col % NH;
+                double2 v[P];
 #pragma unroll
-        for (int y = 0; y < P; y++) v[y] = f1[(x * P + y) * NH + kz];
+                for (int y = 0; y < P; y++) v[y] = i1[(x * P + y) * NH + kz];
 #pragma unroll
-        for (int ky = 0; ky < N; ky++) {
-            double2 acc = make_double2(0.0, 0.0);
+                for (int ky = 0; ky < N; ky++) {
+                    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int y = 0; y < P; y++) cmac(acc, v[y], tw[(ky * y) % N]);
-            f2[(x * N + ky) * NH + kz] = acc;
+                    for (int y = 0; y < P; y++) cmac(acc, v[y], tw[(ky * y) % N]);
+                    o2[(x * N + ky) * NH + kz] = acc;
+                }
+            }
         }
     }
     __syncthreads();
-    for (int r = tid; r < N * NH; r += nt) { // x: P -> N, column (ky, kz), straight out
+    for (int e = tid; e < ng * N * NH; e += nt) { // x: P -> N, column (h, ky, kz), straight out
+        const int h = e / (N * NH), r = e % (N * NH);
+        const double2 *i2 = f2 + h * F2;
+        double2 *out = Psi + (g0 + h) * NW;
         double2 v[P];
 #pragma unroll
-        for (int x = 0; x < P; x++) v[x] = f2[x * N * NH + r];
+        for (int x = 0; x < P; x++) v[x] = i2[x * N * NH + r];
 #pragma unroll
         for (int kx = 0; kx < N; kx++) {
             double2 acc = make_double2(0.0, 0.0);
@@ -1141,9 +1165,10 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
 #define LAT_FWD(PP)                                                                                                    \
     case PP: {                                                                                                         \
         constexpr int NN = fft_edge(PP), HH = NN / 2 + 1;                                                              \
-        const size_t sm = (size_t)(NN + PP * PP * PP + PP * PP * HH + PP * NN * HH) * 16;                              \
+        const size_t sm = (size_t)(NN + 2 * (PP * PP * PP + PP * PP * HH + PP * NN * HH)) * 16;                        \
         set_smem_once(lat_surface_fwd_t<PP>, sm);                                                                      \
-        lat_surface_fwd_t<PP><<<(unsigned)ng, tpb, sm, st>>>(A, n, f.gidx, reinterpret_cast<double2 *>(psi));          \
+        lat_surface_fwd_t<PP><<<(unsigned)((ng + 1) / 2), tpb, sm, st>>>(A, n, f.gidx,                                 \
+                                                                         reinterpret_cast<double2 *>(psi), ng);        \
         break;                                                                                                         \
     }
         LAT_FWD(4) LAT_FWD(5) LAT_FWD(6) LAT_FWD(7) LAT_FWD(8) LAT_FWD(9) LAT_FWD(10)
