@@ -894,7 +894,10 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
                                                          const int *__restrict__ gidx, double2 *__restrict__ Psi,
                                                          int64_t ngroups) {
     constexpr int N = fft_edge(P), NH = N / 2 + 1, NW = N * N * NH;
-    constexpr int CUBE = P * P * P, F1 = P * P * NH, F2 = P * N * NH;
+    // rows of 8 complex values are 128 bytes: threads that walk one row each would all start in
+    // the same bank (8-way conflicts on every access), so those rows get one element of padding
+    constexpr int PZ = P + 1, NHP = NH + 1;
+    constexpr int CUBE = P * P * PZ, F1 = P * P * NHP, F2 = P * N * NH;
     extern __shared__ double2 lt_sm[];
     double2 *tw = lt_sm;             // [N]
     double2 *cube = tw + N;          // 2 x [P^3]
@@ -913,7 +916,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
     for (int e = tid; e < ng * n; e += nt) {
         const int h = e / n, i = e % n;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
-        cube[h * CUBE + (x * P + y) * P + z] = A[(g0 + h) * n + i];
+        cube[h * CUBE + (x * P + y) * PZ + z] = A[(g0 + h) * n + i];
     }
     __syncthreads();
     const int half = nt / 2; // threads per group in stages 1 and 2
@@ -925,13 +928,13 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
             for (int xy = t; xy < P * P; xy += half) { // z: P -> NH
                 double2 v[P];
 #pragma unroll
-                for (int z = 0; z < P; z++) v[z] = cb[xy * P + z];
+                for (int z = 0; z < P; z++) v[z] = cb[xy * PZ + z];
 #pragma unroll
                 for (int kz = 0; kz < NH; kz++) {
                     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int z = 0; z < P; z++) cmac(acc, v[z], tw[(kz * z) % N]);
-                    o1[xy * NH + kz] = acc;
+                    o1[xy * NHP + kz] = acc;
                 }
             }
         }
@@ -946,7 +949,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
                 const int x = col / NH, kz = col % NH;
                 double2 v[P];
 #pragma unroll
-                for (int y = 0; y < P; y++) v[y] = i1[(x * P + y) * NH + kz];
+                for (int y = 0; y < P; y++) v[y] = i1[(x * P + y) * NHP + kz];
 #pragma unroll
                 for (int ky = 0; ky < N; ky++) {
                     double2 acc = make_double2(0.0, 0.0);
@@ -982,8 +985,9 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
     constexpr int N = fft_edge(P), NH = N / 2 + 1, NW = N * N * NH;
     extern __shared__ double2 lt_sm[];
     double2 *tw = lt_sm;                             // [N]
+    constexpr int NHP = NH + 1;                  // padded row of b2 (see lat_surface_fwd_t)
     double2 *const b1 = tw + N;                  // 2 x [x][ky][kz] (per half)
-    double2 *const b2 = b1 + 2 * P * N * NH;     // 2 x [x][y][kz]
+    double2 *const b2 = b1 + 2 * P * N * NH;     // 2 x [x][y][kz (padded)]
     const int64_t pr = pairs[blockIdx.x / (8 * kt)];
     const int oa = blockIdx.x % (8 * kt);
     const int64_t kap[2] = {pr & 0xffffffffLL, pr >> 32};
@@ -1020,15 +1024,15 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
             for (int ky = 0; ky < N; ky++) cmac(acc, v[ky], tw[(ky * y) % N]);
-            b2[h * P * P * NH + (x * P + y) * NH + kz] = acc;
+            b2[h * P * P * NHP + (x * P + y) * NHP + kz] = acc;
         }
     }
     __syncthreads();
     for (int e = tid; e < nh * n; e += nt) { // z at the surface points
         const int h = e / n, i = e % n;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
-        const double2 *own = b2 + h * P * P * NH + (x * P + y) * NH;
-        const double2 *oth = b2 + (nh == 2 ? 1 - h : 0) * P * P * NH + (x * P + y) * NH;
+        const double2 *own = b2 + h * P * P * NHP + (x * P + y) * NHP;
+        const double2 *oth = b2 + (nh == 2 ? 1 - h : 0) * P * P * NHP + (x * P + y) * NHP;
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int kz = 0; kz < NH; kz++) cmac(acc, own[kz], tw[(kz * z) % N]);
@@ -1165,7 +1169,7 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
 #define LAT_FWD(PP)                                                                                                    \
     case PP: {                                                                                                         \
         constexpr int NN = fft_edge(PP), HH = NN / 2 + 1;                                                              \
-        const size_t sm = (size_t)(NN + 2 * (PP * PP * PP + PP * PP * HH + PP * NN * HH)) * 16;                        \
+        const size_t sm = (size_t)(NN + 2 * (PP * PP * (PP + 1) + PP * PP * (HH + 1) + PP * NN * HH)) * 16;            \
         set_smem_once(lat_surface_fwd_t<PP>, sm);                                                                      \
         lat_surface_fwd_t<PP><<<(unsigned)((ng + 1) / 2), tpb, sm, st>>>(A, n, f.gidx,                                 \
                                                                          reinterpret_cast<double2 *>(psi), ng);        \
@@ -1203,7 +1207,7 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
 #define LAT_INV(PP)                                                                                                    \
     case PP: {                                                                                                         \
         constexpr int NN = fft_edge(PP), HH = NN / 2 + 1;                                                              \
-        const size_t sm = (size_t)(NN + 2 * PP * NN * HH + 2 * PP * PP * HH) * 16;                                     \
+        const size_t sm = (size_t)(NN + 2 * PP * NN * HH + 2 * PP * PP * (HH + 1)) * 16;                               \
         set_smem_once(lat_surface_inv_t<PP>, sm);                                                                      \
         lat_surface_inv_t<PP><<<(unsigned)(S.npairs * 8 * kt), tpb, sm, st>>>(reinterpret_cast<const double2 *>(q),   \
                                                                                S.pairs, kt, n, f.gidx, A);             \
