@@ -876,10 +876,14 @@ __global__ void __launch_bounds__(LS_THREADS) lat_surface_inv_kernel(const doubl
 // The same two transforms with p a compile-time constant: every twiddle index is a
 // constant, each thread keeps one input column in registers and produces all its outputs
 // (no per-term index arithmetic, one shared-memory read per input).
-template <int P> struct Tw {
-    static constexpr int N = fft_edge(P);
-};
-template <int P> __device__ __forceinline__ double2 twid(const double2 *tw, int k) { return tw[k % fft_edge(P)]; }
+// exp(-2 pi i k / N), N = fft_edge(P), per compile-time P: with constant indices the twiddles
+// are constant-bank operands of the DFMAs themselves (no shared-memory load per term)
+constexpr int kLatTwMaxP = 10, kLatTwMaxN = 32;
+__constant__ double2 c_lat_tw[kLatTwMaxP + 1][kLatTwMaxN];
+template <int P, int SIGN> __device__ __forceinline__ double2 ctw(int k) {
+    const double2 t = c_lat_tw[P][k];
+    return SIGN < 0 ? t : make_double2(t.x, -t.y);
+}
 __device__ __forceinline__ void cmac(double2 &acc, double2 a, double2 t) {
     acc.x = fma(a.x, t.x, fma(-a.y, t.y, acc.x));
     acc.y = fma(a.x, t.y, fma(a.y, t.x, acc.y));
@@ -906,11 +910,6 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
     const int64_t g0 = 2 * (int64_t)blockIdx.x;
     const int ng = g0 + 1 < ngroups ? 2 : 1;
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int k = tid; k < N; k += nt) {
-        double s, c;
-        sincospi(-2.0 * k / N, &s, &c);
-        tw[k] = make_double2(c, s);
-    }
     for (int e = tid; e < 2 * CUBE; e += nt) cube[e] = make_double2(0.0, 0.0);
     __syncthreads();
     for (int e = tid; e < ng * n; e += nt) {
@@ -933,7 +932,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
                 for (int kz = 0; kz < NH; kz++) {
                     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-                    for (int z = 0; z < P; z++) cmac(acc, v[z], tw[(kz * z) % N]);
+                    for (int z = 0; z < P; z++) cmac(acc, v[z], ctw<P, -1>((kz * z) % N));
                     o1[xy * NHP + kz] = acc;
                 }
             }
@@ -954,7 +953,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
                 for (int ky = 0; ky < N; ky++) {
                     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-                    for (int y = 0; y < P; y++) cmac(acc, v[y], tw[(ky * y) % N]);
+                    for (int y = 0; y < P; y++) cmac(acc, v[y], ctw<P, -1>((ky * y) % N));
                     o2[(x * N + ky) * NH + kz] = acc;
                 }
             }
@@ -972,7 +971,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
         for (int kx = 0; kx < N; kx++) {
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int x = 0; x < P; x++) cmac(acc, v[x], tw[(kx * x) % N]);
+            for (int x = 0; x < P; x++) cmac(acc, v[x], ctw<P, -1>((kx * x) % N));
             out[kx * N * NH + r] = acc;
         }
     }
@@ -1009,7 +1008,7 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
         for (int x = 0; x < P; x++) {
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int kx = 0; kx < N; kx++) cmac(acc, v[kx], tw[(kx * x) % N]);
+            for (int kx = 0; kx < N; kx++) cmac(acc, v[kx], ctw<P, 1>((kx * x) % N));
             b1[h * P * N * NH + x * N * NH + r] = acc;
         }
     }
@@ -1023,7 +1022,7 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
         for (int y = 0; y < P; y++) {
             double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int ky = 0; ky < N; ky++) cmac(acc, v[ky], tw[(ky * y) % N]);
+            for (int ky = 0; ky < N; ky++) cmac(acc, v[ky], ctw<P, 1>((ky * y) % N));
             b2[h * P * P * NHP + (x * P + y) * NHP + kz] = acc;
         }
     }
@@ -1250,9 +1249,29 @@ int m2l_lattice_scatter(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws,
     return launches + 1;
 }
 
+// the constant twiddle tables of the templated surface transforms, once per device
+void upload_lattice_twiddles() {
+    static std::mutex mtx;
+    static bool done[64] = {false};
+    int dev = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mtx);
+    if (dev < 64 && done[dev]) return;
+    static double2 h[kLatTwMaxP + 1][kLatTwMaxN];
+    const double pi = 3.14159265358979323846;
+    for (int p = 2; p <= kLatTwMaxP; p++) {
+        const int N = fft_edge(p);
+        for (int k = 0; k < N && k < kLatTwMaxN; k++)
+            h[p][k] = make_double2(std::cos(-2.0 * pi * k / N), std::sin(-2.0 * pi * k / N));
+    }
+    PK_CUDA(cudaMemcpyToSymbol(c_lat_tw, h, sizeof h));
+    if (dev < 64) done[dev] = true;
+}
+
 int m2l_fft_prepare(KifmmOps &ops, Workspace &ws, cudaStream_t st) {
     FftOps &f = ops.fft;
     if (f.ready) return 0;
+    upload_lattice_twiddles();
     const int p = ops.p, ks = ops.ks, kt = ops.kt;
     f.N = fft_edge(p);
     f.nw = f.N * f.N * (f.N / 2 + 1);
