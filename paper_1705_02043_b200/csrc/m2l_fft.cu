@@ -1200,6 +1200,9 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     if (a.work) // algorithmic bytes: M (14 classes x symmetric components) + Psi~ in, Q~ out, 16 B each
         a.work(a.user, "lat_mul", (double)M3 * f.nw, 16.0 * (LAT_E * (ks * (ks + 1) / 2) + 8 * ks + 8 * kt));
     mark("lat_inv", 1);
+    // (a CTA takes a conjugate pair of lattice frequencies: 2 N NH first-stage columns, one round
+    // of global loads with twice the threads)
+    const int tpb_inv = std::min(256, (2 * f.N * NH + 31) / 32 * 32);
     // surface values per lattice frequency -> inverse lattice transform -> check potentials
     // (unnormalised transforms: 1 / (N^3 M3))
     switch (p) {
@@ -1208,7 +1211,7 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
         constexpr int NN = fft_edge(PP), HH = NN / 2 + 1;                                                              \
         const size_t sm = (size_t)(NN + 2 * PP * NN * HH + 2 * PP * PP * (HH + 1)) * 16;                               \
         set_smem_once(lat_surface_inv_t<PP>, sm);                                                                      \
-        lat_surface_inv_t<PP><<<(unsigned)(S.npairs * 8 * kt), tpb, sm, st>>>(reinterpret_cast<const double2 *>(q),   \
+        lat_surface_inv_t<PP><<<(unsigned)(S.npairs * 8 * kt), tpb_inv, sm, st>>>(reinterpret_cast<const double2 *>(q),\
                                                                                S.pairs, kt, n, f.gidx, A);             \
         break;                                                                                                         \
     }
