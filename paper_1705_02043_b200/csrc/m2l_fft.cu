@@ -902,27 +902,27 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
     // the same bank (8-way conflicts on every access), so those rows get one element of padding
     constexpr int PZ = P + 1, NHP = NH + 1;
     constexpr int CUBE = P * P * PZ, F1 = P * P * NHP, F2 = P * N * NH;
+    constexpr int RA = CUBE > F2 ? CUBE : F2; // the cube is dead when stage 2 writes f2: one region for both
     extern __shared__ double2 lt_sm[];
-    double2 *tw = lt_sm;             // [N]
-    double2 *cube = tw + N;          // 2 x [P^3]
-    double2 *f1 = cube + 2 * CUBE;   // 2 x [x][y][kz]
-    double2 *f2 = f1 + 2 * F1;       // 2 x [x][ky][kz]
+    double2 *cube = lt_sm;           // 2 x [x][y][z (padded)], stride RA
+    double2 *f2 = lt_sm;             // 2 x [x][ky][kz], stride RA (over the cube)
+    double2 *f1 = lt_sm + 2 * RA;    // 2 x [x][y][kz (padded)]
     const int64_t g0 = 2 * (int64_t)blockIdx.x;
     const int ng = g0 + 1 < ngroups ? 2 : 1;
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < 2 * CUBE; e += nt) cube[e] = make_double2(0.0, 0.0);
+    for (int e = tid; e < 2 * RA; e += nt) cube[e] = make_double2(0.0, 0.0);
     __syncthreads();
     for (int e = tid; e < ng * n; e += nt) {
         const int h = e / n, i = e % n;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
-        cube[h * CUBE + (x * P + y) * PZ + z] = A[(g0 + h) * n + i];
+        cube[h * RA + (x * P + y) * PZ + z] = A[(g0 + h) * n + i];
     }
     __syncthreads();
     const int half = nt / 2; // threads per group in stages 1 and 2
     {
         const int h = tid / half, t = tid % half;
         if (h < ng) {
-            const double2 *cb = cube + h * CUBE;
+            const double2 *cb = cube + h * RA;
             double2 *o1 = f1 + h * F1;
             for (int xy = t; xy < P * P; xy += half) { // z: P -> NH
                 double2 v[P];
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
         const int h = tid / half, t = tid % half;
         if (h < ng) {
             const double2 *i1 = f1 + h * F1;
-            double2 *o2 = f2 + h * F2;
+            double2 *o2 = f2 + h * RA;
             for (int col = t; col < P * NH; col += half) { // y: P -> N, column (x, kz)
                 const int x = col / NH, kz = col % NH;
                 double2 v[P];
@@ -962,7 +962,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
     __syncthreads();
     for (int e = tid; e < ng * N * NH; e += nt) { // x: P -> N, column (h, ky, kz), straight out
         const int h = e / (N * NH), r = e % (N * NH);
-        const double2 *i2 = f2 + h * F2;
+        const double2 *i2 = f2 + h * RA;
         double2 *out = Psi + (g0 + h) * NW;
         double2 v[P];
 #pragma unroll
@@ -1168,7 +1168,7 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
 #define LAT_FWD(PP)                                                                                                    \
     case PP: {                                                                                                         \
         constexpr int NN = fft_edge(PP), HH = NN / 2 + 1;                                                              \
-        const size_t sm = (size_t)(NN + 2 * (PP * PP * (PP + 1) + PP * PP * (HH + 1) + PP * NN * HH)) * 16;            \
+        const size_t sm = (size_t)(2 * (std::max(PP * PP * (PP + 1), PP * NN * HH) + PP * PP * (HH + 1))) * 16;        \
         set_smem_once(lat_surface_fwd_t<PP>, sm);                                                                      \
         lat_surface_fwd_t<PP><<<(unsigned)((ng + 1) / 2), tpb, sm, st>>>(A, n, f.gidx,                                 \
                                                                          reinterpret_cast<double2 *>(psi), ng);        \
