@@ -288,8 +288,9 @@ pkgpu_status pkgpu_context_create(int device, pkgpu_context **ctx, char *err, si
         PK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         PK_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         PK_CUDA(cudaStreamCreateWithPriority(&c->aux2_stream, cudaStreamNonBlocking, prio_least));
-        PK_CUDA(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
-        PK_CUDA(cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming));
+        PK_CUDA(cudaStreamCreateWithPriority(&c->aux3_stream, cudaStreamNonBlocking, (prio_least + prio_greatest) / 2));
+        for (auto &e : c->ev_lat_fork) PK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto &e : c->ev_lat_join) PK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *ctx = c.release();
     });
 }
@@ -306,8 +307,11 @@ void pkgpu_context_destroy(pkgpu_context *ctx) {
     if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
     if (ctx->h_layout) cudaFreeHost(ctx->h_layout);
     if (ctx->aux2_stream) cudaStreamDestroy(ctx->aux2_stream);
-    if (ctx->ev_fork2) cudaEventDestroy(ctx->ev_fork2);
-    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
+    if (ctx->aux3_stream) cudaStreamDestroy(ctx->aux3_stream);
+    for (auto e : ctx->ev_lat_fork)
+        if (e) cudaEventDestroy(e);
+    for (auto e : ctx->ev_lat_join)
+        if (e) cudaEventDestroy(e);
     for (auto e : ctx->evpool) cudaEventDestroy(e);
     delete ctx;
 }

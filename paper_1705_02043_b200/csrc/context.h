@@ -37,11 +37,14 @@ struct pkgpu_context {
     cudaStream_t stream = nullptr;
     cudaStream_t aux_stream = nullptr;          // list building beside the upward pass (evaluate.cu)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    cudaStream_t aux2_stream = nullptr;         // the deepest lattice level's M2L, from its pinv_up on (evaluate.cu)
-    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    // lattice levels' M2L queued from their pinv_up on (evaluate.cu): the deepest level on
+    // aux2_stream (lowest priority), the coarser ones on aux3_stream (between it and the work
+    // stream); per level a fork / join event pair and a workspace
+    cudaStream_t aux2_stream = nullptr, aux3_stream = nullptr;
+    cudaEvent_t ev_lat_fork[pkgpu::kMaxLevels + 1] = {}, ev_lat_join[pkgpu::kMaxLevels + 1] = {};
+    pkgpu::Workspace ws_lat[pkgpu::kMaxLevels + 1];
     int *h_layout = nullptr;                    // pinned staging of build_layout's small tables (evaluate.cu)
     cudaEvent_t ev_user = nullptr;              // hand-over between a caller's stream and own_stream (evaluate.cu)
-    pkgpu::Workspace ws_aux;                    // buffers of the lattice M2L run on aux2_stream
     int64_t launches = 0;
     std::mutex mtx; // calls on one context are serialised (the reference evaluate is reentrant per call)
     pkgpu::OperatorCache ops;

@@ -1099,10 +1099,14 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             la.defer_scatter = defer;
             return la;
         };
+        // (the coarser lattice levels likewise, on a third stream of middle priority: small, but
+        // they sat on the chain, which ends the overlapped region once the deepest level's M2L
+        // has become cheaper than it)
         int lat_async = -1;
-        if (overlap_lists && tuning().overlap_m2l && ctx.aux2_stream) {
+        bool lat_early[kMaxLevels + 1] = {false};
+        if (overlap_lists && tuning().overlap_m2l && ctx.aux2_stream && ctx.aux3_stream) {
             for (int l = 2; l <= T.depth; l++)
-                if (Lay.lat[l]) lat_async = l;
+                if (Lay.lat[l]) lat_async = l, lat_early[l] = true;
             if (lat_async >= 2) ctx.launches += m2l_fft_prepare(ops, ws, st); // kernel spectra (first use)
         }
         // ---- upward pass (src/fmm.cpp:532-553) ----
@@ -1155,13 +1159,14 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
             pm = prof.begin("pinv_up");
             pinv_level(ctx, ops, true, lo, hi, l, Q, Tm - lo * Kp, Pup, st, PP, Lay);
             prof.end(pm);
-            if (l == lat_async) {
-                // phi_up of the deepest lattice level is final: its M2L starts here, beside the
-                // rest of the upward pass, the lists and the coarse levels' downward chain
-                PK_CUDA(cudaEventRecord(ctx.ev_fork2, st));
-                PK_CUDA(cudaStreamWaitEvent(ctx.aux2_stream, ctx.ev_fork2, 0));
-                ctx.launches += m2l_lattice_level(ops, lat_args(l, true), ctx.ws_aux, ctx.aux2_stream);
-                PK_CUDA(cudaEventRecord(ctx.ev_join2, ctx.aux2_stream));
+            if (lat_early[l]) {
+                // phi_up of this lattice level is final: its M2L starts here, beside the rest of
+                // the upward pass, the lists and the coarse levels' downward chain
+                cudaStream_t ls = l == lat_async ? ctx.aux2_stream : ctx.aux3_stream;
+                PK_CUDA(cudaEventRecord(ctx.ev_lat_fork[l], st));
+                PK_CUDA(cudaStreamWaitEvent(ls, ctx.ev_lat_fork[l], 0));
+                ctx.launches += m2l_lattice_level(ops, lat_args(l, true), ctx.ws_lat[l], ls);
+                PK_CUDA(cudaEventRecord(ctx.ev_lat_join[l], ls));
             }
         }
         if (overlap_lists) {
@@ -1326,11 +1331,11 @@ void evaluate(pkgpu_context &ctx, const pkgpu_request &req, double *out, pkgpu_t
         for (int l = 0; l <= T.depth; l++) {
             const int64_t lo = T.level_off[l], hi = T.level_off[l + 1];
             const int64_t c0 = Lay.colbase[l], c1 = Lay.colbase[l + 1];
-            if (l >= 1 && l == lat_async) PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_join2, 0)); // also when dropped
-            if (l >= 1 && l == lat_async && Lay.lat[l]) {
-                // computed on the second auxiliary stream: add it into q
+            if (lat_early[l]) PK_CUDA(cudaStreamWaitEvent(st, ctx.ev_lat_join[l], 0)); // also when dropped
+            if (lat_early[l] && Lay.lat[l]) {
+                // computed on an auxiliary stream: add it into q
                 pm = prof.begin("m2l");
-                ctx.launches += m2l_lattice_scatter(ops, lat_args(l, true), ctx.ws_aux, st);
+                ctx.launches += m2l_lattice_scatter(ops, lat_args(l, true), ctx.ws_lat[l], st);
                 prof.end(pm);
                 lat_apps[l] = 1;
             } else if (l >= 1 && Lay.lat[l]) {
