@@ -1,10 +1,12 @@
 // Device octree build: FmmTree::FmmTree (src/fmm.cpp:301-389) restated as
 //   36-bit Morton keys (x = least significant bit of each triple) from floor(x*4096)
-//   -> stable radix sort of (key, index) for sources and targets
+//   -> stable radix sort of (key, index) for sources and targets (the key bits of the first
+//      8 levels; all 36 once a tree has needed more)
 //   -> level-synchronous splitting: a box splits iff |src| > s or |trg| > s; its
 //      children are the non-empty next-octant-digit sub-ranges, emitted in octant
 //      order, so boxes come out level-major and Morton-ordered within a level —
-//      exactly the reference's BFS numbering.
+//      exactly the reference's BFS numbering. All levels run in ONE cooperative kernel
+//      (tree_loop_kernel: grid barriers between levels, one header read back at the end).
 // x >= box_center  <=>  the (l+1)-th most significant bit of floor(x*4096) is set,
 // because box centers (c+1/2)2^-l are exact dyadics (SURVEY.md §8a "Tree semantics").
 #include <algorithm>
