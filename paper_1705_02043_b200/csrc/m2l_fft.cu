@@ -898,6 +898,7 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
                                                          const int *__restrict__ gidx, double2 *__restrict__ Psi,
                                                          int64_t ngroups) {
     constexpr int N = fft_edge(P), NH = N / 2 + 1, NW = N * N * NH;
+    constexpr int NS = P * P * P - (P - 2) * (P - 2) * (P - 2); // surface points (= n: constant divisors)
     // rows of 8 complex values are 128 bytes: threads that walk one row each would all start in
     // the same bank (8-way conflicts on every access), so those rows get one element of padding
     constexpr int PZ = P + 1, NHP = NH + 1;
@@ -912,10 +913,10 @@ __global__ void __launch_bounds__(256) lat_surface_fwd_t(const double2 *__restri
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < 2 * RA; e += nt) cube[e] = make_double2(0.0, 0.0);
     __syncthreads();
-    for (int e = tid; e < ng * n; e += nt) {
-        const int h = e / n, i = e % n;
+    for (int e = tid; e < ng * NS; e += nt) {
+        const int h = e / NS, i = e % NS;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
-        cube[h * RA + (x * P + y) * PZ + z] = A[(g0 + h) * n + i];
+        cube[h * RA + (x * P + y) * PZ + z] = A[(g0 + h) * NS + i];
     }
     __syncthreads();
     const int half = nt / 2; // threads per group in stages 1 and 2
@@ -1027,8 +1028,9 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
         }
     }
     __syncthreads();
-    for (int e = tid; e < nh * n; e += nt) { // z at the surface points
-        const int h = e / n, i = e % n;
+    constexpr int NS = P * P * P - (P - 2) * (P - 2) * (P - 2); // surface points (= n: constant divisors)
+    for (int e = tid; e < nh * NS; e += nt) { // z at the surface points
+        const int h = e / NS, i = e % NS;
         const int gi = gidx[i], x = gi / (N * N), y = (gi / N) % N, z = gi % N;
         const double2 *own = b2 + h * P * P * NHP + (x * P + y) * NHP;
         const double2 *oth = b2 + (nh == 2 ? 1 - h : 0) * P * P * NHP + (x * P + y) * NHP;
@@ -1040,7 +1042,7 @@ __global__ void __launch_bounds__(256) lat_surface_inv_t(const double2 *__restri
             const double2 q = oth[N - kz];
             cmac(acc, make_double2(q.x, -q.y), tw[(kz * z) % N]);
         }
-        A[(kap[h] * 8 * kt + oa) * n + i] = acc;
+        A[(kap[h] * 8 * kt + oa) * NS + i] = acc;
     }
 }
 
@@ -1146,6 +1148,8 @@ int m2l_lattice_level(KifmmOps &ops, const LatticeLevelArgs &a, Workspace &ws, c
     const auto m = lattice_dims(a.level, a.periodic);
     LatticeShape &S = lattice_shape(ops, m, st, &launches);
     const int ks = ops.ks, kt = ops.kt, n = ops.n;
+    if (n != ops.p * ops.p * ops.p - (ops.p - 2) * (ops.p - 2) * (ops.p - 2))
+        throw RuntimeError("lattice M2L: surface point count does not match p"); // the kernels' constant
     const int64_t M3 = S.M3, N3 = (int64_t)f.N * f.N * f.N, nl = a.box1 - a.box0;
     int *box_of = ws.get<int>("lat_boxof", M3 * 8);
     auto mark = [&](const char *stage, int begin) {
